@@ -1,0 +1,307 @@
+"""CPU oracle for the butterfly / HOD-BF multi-RHS apply.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this module.
+It shares no code with ``paper_2007_00202_b200`` (the CUDA path); both read factors
+from ``bfinputs`` (pure storage, no apply arithmetic).
+
+What it computes, in complex128 throughout:
+  * Butterfly, Eq. (3.1): at the centre level lc every block is
+        K(O_tau, S_nu) = Uhat_{tau,nu} B_{tau,nu} Vthat_{tau,nu}
+    with the nested bases of Eq. (3.2):
+        Uhat_{tau,nu} = U_tau                                        (l = L)
+                      = diag(Uhat_{2tau,nu>>1}, Uhat_{2tau+1,nu>>1}) R_{tau,nu}   (l < L)
+        Vthat_{tau,nu} = Vt_nu                                       (l = 0)
+                       = W_{tau,nu} diag(Vthat_{tau>>1,2nu}, Vthat_{tau>>1,2nu+1}) (l > 0)
+    (children of tau are 2tau, 2tau+1; parent of nu is nu>>1 -- P:291-295).
+    The blocks at level lc tile K (complementary low-rank partition).
+    User order: K_user[row_perm[i], col_perm[j]] = K[i, j].  Forward Y = K_user X,
+    adjoint Y = K_user^H X, transpose Y = K_user^T X.
+  * HOD-BF: A = blkdiag(D_t) at the leaves of T_H plus, for every pair of
+    siblings tau1, tau2 on every level, A(T_tau1, T_tau2) = B_tau1 (a butterfly over
+    the sibling subtrees).  Y = A X / A^H X.
+  * Sampled rows / columns for sizes whose dense K does not fit (C2 step 5): the same
+    Eq. (3.1)-(3.2) definitions restricted to selected rows (or columns).
+Parity pins for every function are in tests/test_oracle_pins.py.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+
+C128 = np.complex128
+
+
+# ----------------------------------------------------------------------------------
+# rank-chain validation (mirrors the checks the C-ABI documents)
+# ----------------------------------------------------------------------------------
+def validate(bf):
+    L, lc = bf.L, bf.lc
+    assert 0 <= lc <= L, "need 0 <= lc <= L"
+    nb = 1 << L
+    rl, cl = bf.row_leaf_ptr, bf.col_leaf_ptr
+    assert len(rl) == nb + 1 and len(cl) == nb + 1
+    assert rl[0] == 0 and cl[0] == 0 and rl[-1] == bf.m and cl[-1] == bf.n
+    assert np.all(np.diff(rl) >= 0) and np.all(np.diff(cl) >= 0)
+    assert np.array_equal(np.sort(bf.row_perm), np.arange(bf.m))
+    assert np.array_equal(np.sort(bf.col_perm), np.arange(bf.n))
+    for tau in range(nb):
+        assert bf.Ub(tau).shape[0] == rl[tau + 1] - rl[tau]
+    for nu in range(nb):
+        assert bf.Vtb(nu).shape[1] == cl[nu + 1] - cl[nu]
+
+    def r(l, tau, nu):
+        return bf.Ub(tau).shape[1] if l == L else bf.Rb(l, tau, nu).shape[1]
+
+    def c(l, tau, nu):
+        return bf.Vtb(nu).shape[0] if l == 0 else bf.Wb(l, tau, nu).shape[0]
+
+    for l in range(lc, L):
+        for tau in range(1 << l):
+            for nu in range(1 << (L - l)):
+                assert bf.Rb(l, tau, nu).shape[0] == r(l + 1, 2 * tau, nu >> 1) + r(l + 1, 2 * tau + 1, nu >> 1)
+    for l in range(1, lc + 1):
+        for tau in range(1 << l):
+            for nu in range(1 << (L - l)):
+                assert bf.Wb(l, tau, nu).shape[1] == c(l - 1, tau >> 1, 2 * nu) + c(l - 1, tau >> 1, 2 * nu + 1)
+    for tau in range(1 << lc):
+        for nu in range(1 << (L - lc)):
+            assert bf.Bb(tau, nu).shape == (r(lc, tau, nu), c(lc, tau, nu))
+
+
+# ----------------------------------------------------------------------------------
+# Eq. (3.2) nested bases
+# ----------------------------------------------------------------------------------
+class _Bases:
+    def __init__(self, bf):
+        self.bf = bf
+        self.Um = {}
+        self.Vm = {}
+
+    def Uhat(self, l, tau, nu):
+        """Uhat_{tau,nu}: |O_tau| x r^l_{tau,nu} (Eq. 3.2 left)."""
+        key = (l, tau, nu)
+        if key not in self.Um:
+            bf = self.bf
+            if l == bf.L:
+                assert nu == 0
+                val = np.asarray(bf.Ub(tau), dtype=C128)
+            else:
+                top = self.Uhat(l + 1, 2 * tau, nu >> 1)
+                bot = self.Uhat(l + 1, 2 * tau + 1, nu >> 1)
+                val = sla.block_diag(top, bot) @ np.asarray(bf.Rb(l, tau, nu), dtype=C128)
+            self.Um[key] = val
+        return self.Um[key]
+
+    def Vthat(self, l, tau, nu):
+        """Vthat_{tau,nu}: c^l_{tau,nu} x |S_nu| (Eq. 3.2 right)."""
+        key = (l, tau, nu)
+        if key not in self.Vm:
+            bf = self.bf
+            if l == 0:
+                assert tau == 0
+                val = np.asarray(bf.Vtb(nu), dtype=C128)
+            else:
+                left = self.Vthat(l - 1, tau >> 1, 2 * nu)
+                right = self.Vthat(l - 1, tau >> 1, 2 * nu + 1)
+                val = np.asarray(bf.Wb(l, tau, nu), dtype=C128) @ sla.block_diag(left, right)
+            self.Vm[key] = val
+        return self.Vm[key]
+
+
+def _O(bf, l, tau):
+    w = 1 << (bf.L - l)
+    return int(bf.row_leaf_ptr[tau * w]), int(bf.row_leaf_ptr[(tau + 1) * w])
+
+
+def _S(bf, lev, nu):
+    """Column range of T_S node nu at T_S level `lev`."""
+    w = 1 << (bf.L - lev)
+    return int(bf.col_leaf_ptr[nu * w]), int(bf.col_leaf_ptr[(nu + 1) * w])
+
+
+def bf_dense_tree(bf) -> np.ndarray:
+    """K in tree order, assembled block by block at level lc (Eq. 3.1)."""
+    L, lc = bf.L, bf.lc
+    K = np.zeros((bf.m, bf.n), dtype=C128)
+    bases = _Bases(bf)
+    for tau in range(1 << lc):
+        r0, r1 = _O(bf, lc, tau)
+        for nu in range(1 << (L - lc)):
+            c0, c1 = _S(bf, L - lc, nu)
+            K[r0:r1, c0:c1] = bases.Uhat(lc, tau, nu) @ np.asarray(bf.Bb(tau, nu), dtype=C128) @ bases.Vthat(lc, tau, nu)
+    return K
+
+
+def bf_dense(bf) -> np.ndarray:
+    """K_user: K_user[row_perm[i], col_perm[j]] = K_tree[i, j]."""
+    Kt = bf_dense_tree(bf)
+    K = np.zeros_like(Kt)
+    K[np.ix_(bf.row_perm, bf.col_perm)] = Kt
+    return K
+
+
+def apply_op(K: np.ndarray, X: np.ndarray, op: str) -> np.ndarray:
+    X = np.asarray(X, dtype=C128)
+    if op == "N":
+        return K @ X
+    if op == "C":
+        return K.conj().T @ X
+    if op == "T":
+        return K.T @ X
+    raise ValueError(op)
+
+
+def bf_apply(bf, X, op: str = "N") -> np.ndarray:
+    """Y = K_user X (op N), K_user^H X (op C) or K_user^T X (op T)."""
+    return apply_op(bf_dense(bf), X, op)
+
+
+# ----------------------------------------------------------------------------------
+# sampled rows / columns (C2 step 5)
+# ----------------------------------------------------------------------------------
+def bf_rows_apply(bf, user_rows, X) -> np.ndarray:
+    """(K_user X)[user_rows, :] without forming K: rows of Eq. (3.1) blocks.
+
+    For each sampled row i (tree position p) in centre node tau_c, row p of
+    Uhat_{tau_c,nu} follows Eq. (3.2) restricted to that row; Vthat_{tau_c,nu} is
+    formed in full; the K row block over S_nu is (Uhat[p] B) Vthat, then times X(S_nu).
+    """
+    L, lc = bf.L, bf.lc
+    assert len(np.unique(user_rows)) == len(user_rows), "sampled rows must be unique"
+    X = np.asarray(X, dtype=C128)
+    inv_row = np.empty(bf.m, dtype=np.int64)
+    inv_row[bf.row_perm] = np.arange(bf.m)
+    tree_rows = inv_row[np.asarray(user_rows, dtype=np.int64)]
+    Xt = X[bf.col_perm, :]                     # X in column-tree order
+    out = np.zeros((len(tree_rows), X.shape[1]), dtype=C128)
+    w_c = 1 << (L - lc)
+    centre = np.searchsorted(bf.row_leaf_ptr, tree_rows, side="right") - 1
+    centre = centre // w_c
+    for tau_c in np.unique(centre):
+        sel = np.nonzero(centre == tau_c)[0]
+        order = np.argsort(tree_rows[sel], kind="stable")
+        sel = sel[order]
+        rows = tree_rows[sel]                   # sorted, unique (caller's rows are unique)
+        bases = _Bases(bf)
+
+        def urows(l, tau, nu):
+            """(rows of O_tau among `rows`, Uhat_{tau,nu}[those rows, :])."""
+            o0, o1 = _O(bf, l, tau)
+            mine = rows[(rows >= o0) & (rows < o1)]
+            if l == L:
+                return mine, np.asarray(bf.Ub(tau), dtype=C128)[mine - o0, :]
+            R = np.asarray(bf.Rb(l, tau, nu), dtype=C128)
+            mt, ut = urows(l + 1, 2 * tau, nu >> 1)
+            mb, ub = urows(l + 1, 2 * tau + 1, nu >> 1)
+            # rows of diag(Uhat_top, Uhat_bot) R
+            full = sla.block_diag(ut, ub) @ R
+            return np.concatenate([mt, mb]), full
+
+        for nu in range(1 << (L - lc)):
+            c0, c1 = _S(bf, L - lc, nu)
+            rr, ur = urows(lc, int(tau_c), nu)
+            Krow = ur @ np.asarray(bf.Bb(int(tau_c), nu), dtype=C128) @ bases.Vthat(lc, int(tau_c), nu)
+            out[sel[np.searchsorted(rows, rr)], :] += Krow @ Xt[c0:c1, :]
+            # drop memoised bases of this nu's column chain to bound memory
+            bases.Vm.clear()
+    return out
+
+
+def bf_cols_apply_adj(bf, user_cols, X) -> np.ndarray:
+    """(K_user^H X)[user_cols, :] via sampled columns of Eq. (3.1) blocks."""
+    L, lc = bf.L, bf.lc
+    assert len(np.unique(user_cols)) == len(user_cols), "sampled columns must be unique"
+    X = np.asarray(X, dtype=C128)
+    inv_col = np.empty(bf.n, dtype=np.int64)
+    inv_col[bf.col_perm] = np.arange(bf.n)
+    tree_cols = inv_col[np.asarray(user_cols, dtype=np.int64)]
+    Xt = X[bf.row_perm, :]                     # X in row-tree order
+    out = np.zeros((len(tree_cols), X.shape[1]), dtype=C128)
+    w_c = 1 << lc                               # leaves per T_S node at level L - lc
+    centre = (np.searchsorted(bf.col_leaf_ptr, tree_cols, side="right") - 1) // w_c
+    for nu_c in np.unique(centre):
+        sel = np.nonzero(centre == nu_c)[0]
+        order = np.argsort(tree_cols[sel], kind="stable")
+        sel = sel[order]
+        cols = tree_cols[sel]                   # sorted, unique
+        bases = _Bases(bf)
+
+        def vcols(l, tau, nu):
+            """(cols of S_nu among `cols`, Vthat_{tau,nu}[:, those cols])."""
+            s0, s1 = _S(bf, L - l, nu)
+            mine = cols[(cols >= s0) & (cols < s1)]
+            if l == 0:
+                return mine, np.asarray(bf.Vtb(nu), dtype=C128)[:, mine - s0]
+            Wb = np.asarray(bf.Wb(l, tau, nu), dtype=C128)
+            ml, vl = vcols(l - 1, tau >> 1, 2 * nu)
+            mr, vr = vcols(l - 1, tau >> 1, 2 * nu + 1)
+            return np.concatenate([ml, mr]), Wb @ sla.block_diag(vl, vr)
+
+        for tau in range(1 << lc):
+            r0, r1 = _O(bf, lc, tau)
+            cc, vc = vcols(lc, tau, int(nu_c))
+            Kcol = bases.Uhat(lc, tau, int(nu_c)) @ np.asarray(bf.Bb(tau, int(nu_c)), dtype=C128) @ vc
+            out[sel[np.searchsorted(cols, cc)], :] += Kcol.conj().T @ Xt[r0:r1, :]
+            bases.Um.clear()
+    return out
+
+
+# ----------------------------------------------------------------------------------
+# HOD-BF
+# ----------------------------------------------------------------------------------
+def hodbf_dense_tree(H) -> np.ndarray:
+    """A in T_H tree order: blkdiag(D_t) + sibling off-diagonal butterflies."""
+    A = np.zeros((H.n, H.n), dtype=C128)
+    for t in range(1 << H.LH):
+        a, b = int(H.leaf_ptr[t]), int(H.leaf_ptr[t + 1])
+        A[a:b, a:b] = np.asarray(H.D.block(t), dtype=C128)
+    for l in range(1, H.LH + 1):
+        for tau in range(1 << l):
+            r0, r1 = H.node_range(l, tau)
+            c0, c1 = H.node_range(l, tau ^ 1)
+            A[r0:r1, c0:c1] = bf_dense_tree(H.offdiag[l - 1][tau])
+    return A
+
+
+def hodbf_dense(H) -> np.ndarray:
+    At = hodbf_dense_tree(H)
+    A = np.zeros_like(At)
+    A[np.ix_(H.perm, H.perm)] = At
+    return A
+
+
+def hodbf_apply(H, X, op: str = "N") -> np.ndarray:
+    """Y = A X (op N) or A^H X (op C) or A^T X (op T), block by block.
+
+    Never forms the full A: Y(T_t) = D_t X(T_t) at the leaves, and for every sibling
+    pair Y(T_tau1) += B_tau1 X(T_tau2) (adjoint: Y(T_tau2) += B_tau1^H X(T_tau1)), with
+    each B densified by Eq. (3.1)-(3.2).
+    """
+    X = np.asarray(X, dtype=C128)
+    Xt = X[H.perm, :]
+    Yt = np.zeros_like(Xt)
+    for t in range(1 << H.LH):
+        a, b = int(H.leaf_ptr[t]), int(H.leaf_ptr[t + 1])
+        Yt[a:b] += apply_op(np.asarray(H.D.block(t), dtype=C128), Xt[a:b], op)
+    for l in range(1, H.LH + 1):
+        for tau in range(1 << l):
+            r0, r1 = H.node_range(l, tau)
+            c0, c1 = H.node_range(l, tau ^ 1)
+            Kb = bf_dense_tree(H.offdiag[l - 1][tau])
+            if op == "N":
+                Yt[r0:r1] += Kb @ Xt[c0:c1]
+            elif op == "C":
+                Yt[c0:c1] += Kb.conj().T @ Xt[r0:r1]
+            else:
+                Yt[c0:c1] += Kb.T @ Xt[r0:r1]
+    Y = np.zeros_like(Yt)
+    Y[H.perm, :] = Yt
+    return Y
+
+
+def rel_err(Y, Yref) -> float:
+    """||Y - Yref||_F / ||Yref||_F (the parity metric)."""
+    Yref = np.asarray(Yref, dtype=C128)
+    nrm = np.linalg.norm(Yref)
+    return float(np.linalg.norm(np.asarray(Y, dtype=C128) - Yref) / (nrm if nrm > 0 else 1.0))
