@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark: multi-RHS butterfly apply on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype c128|c64] [--op N|C]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+    python bench.py --impl reference            # the CPU oracle arm (rank 0 only)
+
+Workload (BASELINE.json configs[4], the config the metric's 1/2/4/8-GPU sweep is quoted
+on): random-factor butterfly, n = m = 2^20, L = 14, lc = 7, leaf 64, rank 16, nrhs 32,
+seed 1, complex128 (default) or complex64.  One step = one full apply Y = K X (all
+SURVEY 8(a) rows a1-a5; a6 with --op C), inputs resident in HBM.  The factors (2.48 GB
+c128 / 1.24 GB c64) are far larger than the 126 MB L2, so every step streams them from
+HBM; no L2 flush is needed between steps.
+
+value = algorithmic bytes / time (all factor entries once + X read once + Y written
+once), whole job.  Multi-GPU: the butterfly is split by column subtrees
+(V, W, B) and row subtrees (R, U) with one NCCL all-to-all of the centre slabs; total
+work is fixed (strong scaling).  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "butterfly apply GB/s and RHS-columns/s, % of B200 HBM roofline, 1/2/4/8 GPUs"
+WORKLOAD = "cfg5: random-factor butterfly n=m=2^20, L=14, lc=7, leaf 64, r=16, nrhs=32, seed 1"
+
+
+def _peaks():
+    p = {"hbm_gbs": 6555.8, "source": "MEASURED_PEAKS.json"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p.update(json.load(f))
+    except OSError:
+        p = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+    try:
+        with open(os.path.join(ROOT, "profiles", "pipe_peaks.json")) as f:
+            p["pipes"] = json.load(f)
+    except OSError:
+        p["pipes"] = None
+    return p
+
+
+class ClockSampler:
+    """Polls NVML (SM clock + throttle reasons) on a thread during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device_index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0, "source": "nvml" if self.ok else "unavailable"}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def oracle_sample(bf, X, nrows=(16, 64), centre=3):
+    """Time the CPU oracle (sampled-row reconstruction) on rows of one
+    centre node and extrapolate to the full apply with a two-point model
+    T(rows) = setup + rows * per_row, full = 2^lc * setup + m * per_row."""
+    import oracle
+    w = bf.m >> bf.lc
+    ts = []
+    for r in nrows:
+        rows = centre * w + np.arange(r)
+        t0 = time.perf_counter()
+        oracle.bf_rows_apply(bf, rows, X)
+        ts.append(time.perf_counter() - t0)
+    per_row = max((ts[1] - ts[0]) / (nrows[1] - nrows[0]), 1e-9)
+    setup = max(ts[0] - nrows[0] * per_row, 0.0)
+    full = (1 << bf.lc) * setup + bf.m * per_row
+    return full, sum(ts), (f"oracle rows {nrows[0]} and {nrows[1]} of centre node {centre} "
+                           f"({sum(ts):.1f} s total); full apply extrapolated as 2^lc*setup + m*per_row "
+                           f"(setup {setup:.2f} s, per row {per_row*1e3:.2f} ms)")
+
+
+def build_inputs(dtype_s, nrhs):
+    from bfinputs.configs import cfg5
+    dt = np.complex128 if dtype_s == "c128" else np.complex64
+    return cfg5(dt, nrhs=nrhs)
+
+
+def alg_bytes(bf, nrhs, cs):
+    return (bf.nnz() + (bf.m + bf.n) * nrhs) * cs
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    bf, X = build_inputs(args.dtype, args.nrhs)
+    cs = 16 if args.dtype == "c128" else 8
+    ab = alg_bytes(bf, args.nrhs, cs)
+    times = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        full, spent, sample = oracle_sample(bf, X, nrows=(4, 12), centre=1 + (i % 8))
+        if i >= args.warmup:
+            times.append(full)
+    t = float(np.median(times))
+    val = ab / t / 1e9
+    cores = cpu_threads()
+    line = {"metric": METRIC, "value": val, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": WORKLOAD, "op": args.op, "nrhs": args.nrhs},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                             "sample": sample + " (each step one such sample; value from the median extrapolation)"},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
+    ap.add_argument("--op", default="N", choices=["N", "C"])
+    ap.add_argument("--nrhs", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2007_00202_b200 as pkg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = _peaks()
+    bf, X = build_inputs(args.dtype, args.nrhs)
+    cs = 16 if args.dtype == "c128" else 8
+    ab = alg_bytes(bf, args.nrhs, cs)
+    nrhs = args.nrhs
+    stream = torch.cuda.current_stream()
+    if world == 1:
+        h = pkg.BFHandle(bf, local)
+        rin, rout = (bf.n, bf.m) if args.op == "N" else (bf.m, bf.n)
+        assert bf.m == bf.n, "config 5 is square: the same X block serves op N and op C"
+        Xh = torch.from_numpy(np.ascontiguousarray(X.T))
+        Xd = Xh.cuda()
+        Yd = torch.empty((nrhs, rout), dtype=Xd.dtype, device="cuda")
+        work = torch.empty(h.workspace_size(nrhs), dtype=torch.uint8, device="cuda")
+        rounds = h.rounds(args.op)
+        launches = len(rounds)
+
+        def step(evs=None):
+            if evs is None:
+                h.apply(Xd, args.op, out=Yd, work=work)
+            else:
+                h.apply_events(Xd, evs, args.op, out=Yd, work=work)
+    else:
+        from paper_2007_00202_b200.dist import DistBFHandle
+        h = DistBFHandle(bf, rank, world, local)
+        Xloc = h.local_input(X, args.op)
+        Xd = torch.from_numpy(np.ascontiguousarray(Xloc.T)).cuda()
+        Yd = h.empty_output(nrhs, args.op)
+        launches = h.launches(args.op)
+        rounds = None
+
+        def step(evs=None):
+            h.apply(Xd, args.op, out=Yd)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # per-round events inside the timed region (N = 1): one set per step
+    ev_sets = None
+    if rounds is not None:
+        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(rounds) + 1)] for _ in range(args.steps)]
+        for s in ev_sets:
+            for e in s:
+                e.record(stream)
+        torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(args.steps):
+            step(ev_sets[k] if ev_sets else None)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = ab / (ms * 1e-3) / 1e9
+
+    roofline = None
+    per_round = None
+    if ev_sets is not None:
+        times = np.array([[s[i].elapsed_time(s[i + 1]) for i in range(len(rounds))] for s in ev_sets])
+        mean = times.mean(axis=0)
+        per_round = []
+        by_kernel = {}
+        for i, r in enumerate(rounds):
+            b = (r["factor_entries"] + (r["user_rows_in"] + r["user_rows_out"]) * nrhs) * cs
+            per_round.append({"round": i, "kernel": r["name"], "ms": float(mean[i]), "alg_bytes": int(b),
+                              "gbs": b / (mean[i] * 1e-3) / 1e9})
+            k = by_kernel.setdefault(r["name"], [0.0, 0, 0])
+            k[0] += mean[i]
+            k[1] += b
+            k[2] += 1
+        name, (kms, kb, kn) = max(by_kernel.items(), key=lambda kv: kv[1][0])
+        achieved = kb / kn / (kms / kn * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": name,
+                    "share_of_step": kms / float(mean.sum()), "launches_per_step": kn,
+                    "peak_source": peaks.get("source")}
+        flops = 8.0 * bf.nnz() * nrhs
+        pp = peaks.get("pipes") or {}
+        fp = pp.get("dfma_tflops" if args.dtype == "c128" else "ffma_tflops")
+        roofline["pipe"] = {"tflops": flops / (ms * 1e-3) / 1e12, "peak_tflops": fp,
+                            "frac": (flops / (ms * 1e-3) / 1e12 / fp) if fp else None,
+                            "note": "whole apply, 8 flops per complex MAC, vs measured CUDA-core peak"}
+
+    e2e = None
+    if not args.no_e2e and world == 1:
+        Xp = Xh.pin_memory()
+        Yp = torch.empty((nrhs, Yd.shape[1]), dtype=Xd.dtype).pin_memory()
+        wh = torch.empty(max(h.workspace_size(nrhs), 1) + 2 * (Xd.numel() + Yd.numel()) * cs + 4096,
+                         dtype=torch.uint8, device="cuda")
+        for _ in range(2):
+            h.apply_host(Xp, args.op, out=Yp, work=wh)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ke = max(3, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(ke):
+            h.apply_host(Xp, args.op, out=Yp, work=wh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / ke
+        e2e = {"value": ab / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(Xp.numel() * cs), "d2h_bytes_per_step": int(Yp.numel() * cs),
+               "api": "bf_apply_host (pinned host X/Y, copies inside the timed region)"}
+    elif not args.no_e2e and world > 1:
+        e2e = h.time_e2e(X_loc_host=Xd.cpu(), op=args.op, steps=max(3, min(args.steps, 10)), alg_bytes=ab)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        full, spent, sample = oracle_sample(bf, X)
+        cpu = {"value": ab / full / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+                "config": {"workload": WORKLOAD, "op": args.op, "nrhs": nrhs, "n": bf.n, "L": bf.L,
+                           "factor_entries": bf.nnz(), "alg_bytes_per_step": ab,
+                           "l2": "inputs larger than L2 (factors %.2f GB >> 126 MB); no flush" % (bf.nnz() * cs / 1e9),
+                           "parallelism": "single GPU" if world == 1 else
+                           f"tree split over {world} GPUs (column subtrees -> NCCL all-to-all -> row subtrees)"},
+                "rhs_cols_per_s": nrhs / (ms * 1e-3), "hbm_frac": value / peaks["hbm_gbs"],
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches * args.steps, "clocks": clk.summary(), "per_round": per_round}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,218 @@
+/*
+ * bfapply.h -- C-ABI of libbfapply: multi-RHS application of butterfly and HOD-BF
+ * compressed matrices on NVIDIA B200 (sm_100a).
+ *
+ * What is applied (PAPER.md = arxiv 2007.00202, cited as P:<line>):
+ *   * a butterfly K(O,S) in the factored ("hybrid") form of Eq. (3.3)
+ *         K = (U^L R^{L-1} ... R^{lc}) B^{lc} (W^{lc} ... W^1 V^0),
+ *     with the block structure of P:322-354 and the nested bases of Eq. (3.2)
+ *     (P:302-317); "storage and application costs ... scale as O(n log n)";
+ *   * an HOD-BF matrix: dense leaf diagonal blocks D_tau plus, for every
+ *     pair of siblings tau1, tau2 of T_H, the butterflies A(T_tau1, T_tau2) and
+ *     A(T_tau2, T_tau1); O(n log^2 n) to apply.
+ * to a block of nrhs right-hand sides, forward (K X) or conjugate-transposed (K^H X).
+ *
+ * Indexing (same as bfinputs/factors.py and DESIGN.md):
+ *   level l in [0, L]; block (tau, nu) pairs tau, a level-l node of T_O, with nu, a
+ *   level-(L-l) node of T_S, both numbered left to right; children of x are 2x, 2x+1.
+ *   Canonical block order within a level: idx = tau * 2^(L-l) + nu.
+ *   Row ranks  r^l_{tau,nu}, l = lc..L   (r^L_{tau,0} = columns of U_tau)
+ *   Col ranks  c^l_{tau,nu}, l = 0..lc   (c^0_{0,nu} = rows of Vt_nu)
+ *   Factor block shapes (ranks may differ per block, B may be rectangular):
+ *     U_tau      : m_tau x r^L_{tau,0}
+ *     R_{tau,nu} : (r^{l+1}_{2tau,nu>>1} + r^{l+1}_{2tau+1,nu>>1}) x r^l_{tau,nu}, l = lc..L-1
+ *     B_{tau,nu} : r^{lc}_{tau,nu} x c^{lc}_{tau,nu}
+ *     W_{tau,nu} : c^l_{tau,nu} x (c^{l-1}_{tau>>1,2nu} + c^{l-1}_{tau>>1,2nu+1}), l = 1..lc
+ *     Vt_nu      : c^0_{0,nu} x n_nu        (stored as it multiplies; never conjugated)
+ *   Each factor array holds its blocks column-major, back to back, levels ascending and
+ *   blocks in canonical order within a level.  Complex numbers are interleaved
+ *   (re, im) -- the layout of torch.complex64 / complex128 and numpy complex64/128.
+ *
+ * Right-hand sides / results are column-major with a leading dimension (BLAS
+ * convention): element (i, j) of X is X[i + j*ldx].  A C-contiguous torch tensor of
+ * shape (nrhs, n) is exactly that layout with ldx = n.
+ *
+ * Ownership: *_create deep-copies every host array to the device (the caller may
+ * free them on return); the handle owns that device memory until *_destroy.  X, Y and
+ * the workspace of *_apply are caller-owned DEVICE buffers; the apply makes no
+ * allocation, no host synchronisation and launches only on the given stream.
+ * Handles are immutable after create: concurrent applies on different streams with
+ * distinct workspaces are legal.  A handle is bound to one device.
+ *
+ * Errors: every entry point returns a bf_status; no exception crosses the ABI.  A
+ * thread-local message is available from bf_last_error().  Asynchronous CUDA faults
+ * surface as BF_ERR_CUDA on a later call.  There is no CPU fallback: without a CUDA
+ * device every create/apply returns BF_ERR_DEVICE.
+ */
+#ifndef BFAPPLY_H
+#define BFAPPLY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bf_s* bf_handle;
+typedef struct hodbf_s* hodbf_handle;
+typedef void* bf_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+typedef enum { BF_C64 = 1, BF_C128 = 2 } bf_dtype;
+
+/* N: Y = K X.  C: Y = K^H X (conjugate transpose, the north-star "adjoint").
+ * T: Y = K^T X (plain transpose, SPEC's A^T X). */
+typedef enum { BF_OP_N = 0, BF_OP_T = 1, BF_OP_C = 2 } bf_op;
+
+typedef enum {
+  BF_OK = 0,
+  BF_ERR_ARG = -1,    /* NULL / negative argument, aliasing X == Y, workspace too small   */
+  BF_ERR_SHAPE = -2,  /* leaf offsets not monotone / not summing to m, n; L out of range  */
+  BF_ERR_RANK = -3,   /* negative rank, or factor lengths inconsistent with the ranks     */
+  BF_ERR_PERM = -4,   /* a permutation is not a bijection                                 */
+  BF_ERR_CUDA = -5,   /* a CUDA runtime error (including earlier asynchronous faults)     */
+  BF_ERR_OOM = -6,    /* device allocation failed                                         */
+  BF_ERR_NCCL = -7,   /* distributed layout not supported for this rank count             */
+  BF_ERR_DEVICE = -8  /* no CUDA device / wrong device / not an sm_100 device             */
+} bf_status;
+
+/* Butterfly descriptor.  All pointers are HOST pointers. */
+typedef struct {
+  int32_t dtype;                 /* bf_dtype                                                  */
+  int32_t L;                     /* number of levels, 0 <= L <= 24                           */
+  int32_t lc;                    /* centre level, 0 <= lc <= L; pass -1 for floor(L/2) (A2)  */
+  int32_t reserved;
+  int64_t m, n;                  /* rows (|O|) and columns (|S|)                             */
+  const int64_t* row_leaf_ptr;   /* 2^L + 1 offsets of T_O leaves in tree order              */
+  const int64_t* col_leaf_ptr;   /* 2^L + 1 offsets of T_S leaves                            */
+  const int64_t* row_perm;       /* m: tree position -> user row; NULL = identity           */
+  const int64_t* col_perm;       /* n: tree position -> user column; NULL = identity        */
+  const int32_t* rank_row;       /* (L-lc+1) * 2^L: r^l_{tau,nu}, l = lc..L, canonical order  */
+  const int32_t* rank_col;       /* (lc+1) * 2^L:   c^l_{tau,nu}, l = 0..lc                   */
+  const void *U, *R, *B, *W, *Vt;/* packed factor arrays (see above)                          */
+  int64_t len_U, len_R, len_B, len_W, len_Vt; /* element counts of the five arrays; must equal
+                                                the counts implied by the ranks (BF_ERR_RANK) */
+} bf_desc;
+
+/* HOD-BF descriptor.  offdiag has sum_{l=1..LH} 2^l entries, level-major:
+ * entry (l, tau) at index 2^l - 2 + tau is the butterfly of A(T_tau, T_{tau^1}) with
+ * L = LH - l levels, tree-local (NULL) perms, and leaf offsets equal to leaf_ptr's
+ * slices for T_tau (rows) and T_{tau^1} (columns), rebased to 0. */
+typedef struct {
+  int32_t dtype;
+  int32_t LH;                    /* HOD-BF levels, 0 <= LH <= 20                             */
+  int64_t n;
+  const int64_t* leaf_ptr;       /* 2^LH + 1 offsets of T_H leaves (tree order)              */
+  const int64_t* perm;           /* n: tree position -> user index; NULL = identity          */
+  const void* D;                 /* 2^LH dense leaf blocks, column-major, back to back       */
+  int64_t len_D;
+  const bf_desc* offdiag;
+} hodbf_desc;
+
+/* Run-time information about a handle (for benchmarks / roofline accounting). */
+typedef struct {
+  int64_t factor_entries;        /* stored complex factor entries (algorithmic)               */
+  int64_t device_bytes;          /* device memory owned by the handle                        */
+  int32_t launches_n;            /* kernel launches per apply, op N                          */
+  int32_t launches_c;            /* kernel launches per apply, op C / T                      */
+  int64_t rows_in, rows_out;     /* rows of X and Y for op N (n, m)                          */
+} bf_info_t;
+
+/* ---- butterfly --------------------------------------------------------------------- */
+int bf_create(const bf_desc* desc, int device, bf_handle* out);
+int bf_destroy(bf_handle h);
+int bf_info(bf_handle h, bf_info_t* info);
+/* Bytes of device workspace one apply with `nrhs` columns needs (any op). */
+int bf_workspace_size(bf_handle h, int64_t nrhs, size_t* bytes);
+/* Y (m x nrhs) <- K X (X: n x nrhs). */
+int bf_apply(bf_handle h, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+             void* work, size_t work_bytes, bf_stream_t stream);
+/* Y (n x nrhs) <- K^H X (X: m x nrhs). */
+int bf_apply_adj(bf_handle h, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                 void* work, size_t work_bytes, bf_stream_t stream);
+/* General form; bf_apply / bf_apply_adj are op N / op C. */
+int bf_apply_op(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y,
+                int64_t ldy, void* work, size_t work_bytes, bf_stream_t stream);
+/* End-to-end form with HOST X / Y (pinned for full speed): H2D copy of X, apply, D2H copy
+ * of Y, all stream-ordered on `stream` (the caller synchronises).  The workspace must be
+ * at least bf_workspace_size_host bytes (it also holds the device copies of X and Y). */
+int bf_workspace_size_host(bf_handle h, int op, int64_t nrhs, size_t* bytes);
+int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* X_host, int64_t ldx,
+                  void* Y_host, int64_t ldy, void* work, size_t work_bytes, bf_stream_t stream);
+
+/* ---- HOD-BF ------------------------------------------------------------------------ */
+int hodbf_create(const hodbf_desc* desc, int device, hodbf_handle* out);
+int hodbf_destroy(hodbf_handle h);
+int hodbf_info(hodbf_handle h, bf_info_t* info);
+int hodbf_workspace_size(hodbf_handle h, int64_t nrhs, size_t* bytes);
+/* Y (n x nrhs) <- A X, A^T X or A^H X. */
+int hodbf_apply(hodbf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y,
+                int64_t ldy, void* work, size_t work_bytes, bf_stream_t stream);
+int hodbf_workspace_size_host(hodbf_handle h, int64_t nrhs, size_t* bytes);
+int hodbf_apply_host(hodbf_handle h, int op, int64_t nrhs, const void* X_host, int64_t ldx,
+                     void* Y_host, int64_t ldy, void* work, size_t work_bytes,
+                     bf_stream_t stream);
+
+/* ---- distributed butterfly (one process per GPU) ------------------------
+ * P = nranks = 2^p GPUs, p <= min(lc, L - lc).  Rank g owns the column subtree nu_g at
+ * level p of T_S (its V leaves, W stages and B blocks) and the row subtree tau_g at level p
+ * of T_O (its R stages and U leaves).  Forward: X_loc = rows of X in S_{nu_g}, Y_loc = rows
+ * of Y in O_{tau_g}; adjoint: the other way round.  Local rows are in user order restricted
+ * to the subtree, which must map to a contiguous user range (else BF_ERR_PERM).
+ * An apply is  pre -> all-to-all of the centre slabs -> post:
+ *   bf_dist_apply_pre  writes the send region of `work` (slabs grouped by destination);
+ *   the caller exchanges send -> recv with an all-to-all (NCCL) using bf_dist_layout;
+ *   bf_dist_apply_post reads the recv region and writes Y_loc.
+ * `desc` is the FULL descriptor (every rank passes the same); only the rank's blocks are
+ * uploaded.  nranks = 1 runs the same path with a self exchange. */
+int bf_dist_create(const bf_desc* desc, int rank, int nranks, int device, bf_handle* out);
+/* Workspace bytes, and the send/recv regions: byte offsets into work plus per-peer
+ * ELEMENT counts (complex entries) -- arrays of length nranks.  Op selects N or C/T. */
+int bf_dist_layout(bf_handle h, int op, int64_t nrhs, size_t* work_bytes, size_t* send_off,
+                   size_t* recv_off, int64_t* send_counts, int64_t* recv_counts);
+int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out,
+                       int64_t* user_off_in, int64_t* user_off_out);
+int bf_dist_apply_pre(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx,
+                      void* work, size_t work_bytes, bf_stream_t stream);
+int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy,
+                       void* work, size_t work_bytes, bf_stream_t stream);
+
+/* ---- introspection / in-situ timing ------------------------------------------------------
+ * An apply is a fixed sequence of kernel launches ("rounds").  bf_round_info describes round
+ * `round` of op `op`: the kernel variant, the number of independent block products, and the
+ * algorithmic traffic of that round (factor entries read once; user rows of X read / of Y
+ * written; slab rows produced).  *_apply_events records events[i] on `stream` right before
+ * round i and events[nrounds] after the last one (nevents must be >= nrounds + 1; the events
+ * are caller-created cudaEvent_t handles), so a caller can time every round inside its own
+ * timed region. */
+typedef struct {
+  int32_t kernel;                /* kernel variant id (see name)                             */
+  int32_t ntasks;                /* independent output slabs in the launch                   */
+  int64_t factor_entries;        /* factor entries the round reads                           */
+  int64_t user_rows_in;          /* rows of X read (leaf rounds)                             */
+  int64_t user_rows_out;         /* rows of Y written (leaf rounds)                          */
+  int64_t slab_rows_in;          /* intermediate slab rows read                              */
+  int64_t slab_rows_out;         /* intermediate slab rows written                           */
+  char name[48];
+} bf_round_info_t;
+int bf_rounds(bf_handle h, int op, int32_t* nrounds);
+int bf_round_info(bf_handle h, int op, int32_t round, bf_round_info_t* info);
+int bf_apply_op_events(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y,
+                       int64_t ldy, void* work, size_t work_bytes, bf_stream_t stream,
+                       void* const* events, int32_t nevents);
+int hodbf_rounds(hodbf_handle h, int op, int32_t* nrounds);
+int hodbf_round_info(hodbf_handle h, int op, int32_t round, bf_round_info_t* info);
+int hodbf_apply_events(hodbf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y,
+                       int64_t ldy, void* work, size_t work_bytes, bf_stream_t stream,
+                       void* const* events, int32_t nevents);
+
+/* ---- misc ---------------------------------------------------------------------------- */
+const char* bf_status_string(int status);
+const char* bf_last_error(void);
+/* Library version and the compile target, e.g. "bfapply 0.1 sm_100a". */
+const char* bf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFAPPLY_H */

@@ -1,0 +1,70 @@
+// Shared definitions of libbfapply (host + device).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "bfapply.h"
+
+namespace bfa {
+
+// One product A * In that contributes to a task's output rows.
+//   A(i, k) = pool[a_off + i * a_rs + k * a_cs]   (conjugated if conj ^ conj_flip)
+//   In(k, :) = slab-space row (in_row + k)        when in_kind == 0
+//            = X row perm[in_row + k]             when in_kind == 1 (user X, column-major)
+struct Term {
+  int64_t a_off;
+  int64_t in_row;
+  int32_t a_rs, a_cs;
+  int32_t k;
+  int16_t conj, in_kind;
+};
+
+// One output slab: rows [out_row, out_row + m) of the slab space (out_kind 0) or the user
+// rows perm[out_row + i] of Y (out_kind 1) receive sum_t A_t In_t.
+struct Task {
+  int64_t out_row;
+  int32_t m;
+  int32_t term0;
+  int32_t nterm;
+  int32_t pad;
+};
+
+// One kernel launch of a plan (a "round": every task in it is independent).
+struct Round {
+  const Task* tasks;   // device
+  const Term* terms;   // device
+  int32_t ntasks;
+  int32_t out_kind;    // 0 slab space, 1 user Y
+  int32_t max_m;
+  int32_t max_k;
+  int32_t fast;        // specialised kernel id (0 = generic)
+  int32_t pad;
+  // algorithmic accounting (host only)
+  int64_t factor_entries, user_in, user_out, slab_in, slab_out;
+};
+
+struct StageArgs {
+  const Task* tasks;
+  const Term* terms;
+  const void* pool;
+  const void* X;
+  int64_t ldx;
+  const int64_t* xperm;
+  void* S;
+  int64_t ldS;
+  void* Y;
+  int64_t ldy;
+  const int64_t* yperm;
+  int32_t out_kind;
+  int32_t conj_flip;
+  int32_t nrhs;
+  int32_t pad;
+};
+
+void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);
+const char* round_kernel_name(int dtype, const Round& r, int* id);
+
+}  // namespace bfa

@@ -1,0 +1,1400 @@
+// Host side of libbfapply: descriptor validation, device upload, and the per-op plans
+// (Task / Term tables) that turn Eq. (3.3) into a short sequence of batched launches.
+//
+// Butterfly, op N (Y = K X), one launch ("round") per stage -- SURVEY 8(a) a1-a5:
+//   r0            a1  z^0_{0,nu}   = Vt_nu X(col_perm[S_nu])
+//   r1 .. r_lc    a2  z^l_{tau,nu} = W_{tau,nu} [z^{l-1}_{tau>>1,2nu}; z^{l-1}_{tau>>1,2nu+1}]
+//   r_lc+1        a3  y^lc_{tau,nu} = B_{tau,nu} z^lc_{tau,nu}
+//   ...           a4  y^{l+1}_{t',nu'} = sum_s R_{t'>>1,2nu'+s}[rows of child t'&1] y^l_{t'>>1,2nu'+s}
+//                     (the gather form of [y_{2tau}; y_{2tau+1}] += R_{tau,nu} y_{tau,nu})
+//   r_L+2         a5  Y(row_perm[O_tau]) = U_tau y^L_{tau,0}
+// op C (Y = K^H X) runs the same rounds backwards with conjugate-transposed factor views;
+// op T reuses the op-C tables with the conjugation flipped.
+// Intermediates live in one "slab space" in the workspace: every (space, level, block)
+// owns rank x nrhs entries (nrhs fastest), so no stage ever overwrites another stage's
+// data and no atomics are needed (each output slab is written by exactly one task).
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace bfa {
+
+thread_local std::string g_last_error;
+
+struct Err {
+  int code;
+  std::string msg;
+};
+
+#define BF_CK(call)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw Err{e_ == cudaErrorMemoryAllocation ? BF_ERR_OOM : BF_ERR_CUDA,               \
+                std::string(#call) + ": " + cudaGetErrorString(e_)};                      \
+  } while (0)
+
+static void require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw Err{code, msg};
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) BF_CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+static size_t csize(int dtype) { return dtype == BF_C128 ? 16 : 8; }
+
+// --------------------------------------------------------------------------------------
+// geometry of one butterfly (ranks, leaves, factor block offsets)
+// --------------------------------------------------------------------------------------
+struct Geom {
+  int L = 0, lc = 0;
+  int64_t m = 0, n = 0, nb = 1;
+  std::vector<int64_t> rlp, clp;
+  std::vector<int32_t> rr, rc;
+  std::vector<int64_t> u_off, vt_off, b_off;
+  std::vector<std::vector<int64_t>> r_off, w_off;  // indexed by level l
+  int64_t len_U = 0, len_R = 0, len_B = 0, len_W = 0, len_Vt = 0;
+
+  int64_t idx(int l, int64_t tau, int64_t nu) const { return (tau << (L - l)) | nu; }
+  int r(int l, int64_t i) const { return rr[(size_t)(l - lc) * nb + i]; }
+  int c(int l, int64_t i) const { return rc[(size_t)l * nb + i]; }
+  int64_t mt(int64_t tau) const { return rlp[tau + 1] - rlp[tau]; }
+  int64_t nv(int64_t nu) const { return clp[nu + 1] - clp[nu]; }
+  int R_rows(int l, int64_t tau, int64_t nu) const {
+    return r(l + 1, idx(l + 1, 2 * tau, nu >> 1)) + r(l + 1, idx(l + 1, 2 * tau + 1, nu >> 1));
+  }
+  int W_cols(int l, int64_t tau, int64_t nu) const {
+    return c(l - 1, idx(l - 1, tau >> 1, 2 * nu)) + c(l - 1, idx(l - 1, tau >> 1, 2 * nu + 1));
+  }
+};
+
+static void check_leafptr(const int64_t* p, int64_t nb, int64_t total, const char* what) {
+  require(p != nullptr, BF_ERR_ARG, std::string(what) + " is NULL");
+  require(p[0] == 0, BF_ERR_SHAPE, std::string(what) + "[0] != 0");
+  for (int64_t i = 0; i < nb; ++i)
+    require(p[i + 1] >= p[i], BF_ERR_SHAPE, std::string(what) + " not monotone");
+  require(p[nb] == total, BF_ERR_SHAPE, std::string(what) + " does not end at the dimension");
+}
+
+static void check_perm(const int64_t* p, int64_t n, const char* what) {
+  if (!p) return;
+  std::vector<char> seen((size_t)n, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    require(p[i] >= 0 && p[i] < n && !seen[(size_t)p[i]], BF_ERR_PERM,
+            std::string(what) + " is not a permutation");
+    seen[(size_t)p[i]] = 1;
+  }
+}
+
+static Geom make_geom(const bf_desc& d) {
+  Geom g;
+  require(d.dtype == BF_C64 || d.dtype == BF_C128, BF_ERR_ARG, "dtype must be BF_C64 or BF_C128");
+  require(d.L >= 0 && d.L <= 24, BF_ERR_SHAPE, "L out of range [0, 24]");
+  g.L = d.L;
+  g.lc = d.lc < 0 ? d.L / 2 : d.lc;
+  require(g.lc >= 0 && g.lc <= g.L, BF_ERR_SHAPE, "lc out of range [0, L]");
+  require(d.m >= 0 && d.n >= 0, BF_ERR_SHAPE, "negative dimension");
+  g.m = d.m;
+  g.n = d.n;
+  g.nb = int64_t(1) << g.L;
+  check_leafptr(d.row_leaf_ptr, g.nb, d.m, "row_leaf_ptr");
+  check_leafptr(d.col_leaf_ptr, g.nb, d.n, "col_leaf_ptr");
+  g.rlp.assign(d.row_leaf_ptr, d.row_leaf_ptr + g.nb + 1);
+  g.clp.assign(d.col_leaf_ptr, d.col_leaf_ptr + g.nb + 1);
+  require(d.rank_row && d.rank_col, BF_ERR_ARG, "rank arrays are NULL");
+  g.rr.assign(d.rank_row, d.rank_row + (size_t)(g.L - g.lc + 1) * g.nb);
+  g.rc.assign(d.rank_col, d.rank_col + (size_t)(g.lc + 1) * g.nb);
+  for (int32_t v : g.rr) require(v >= 0, BF_ERR_RANK, "negative row rank");
+  for (int32_t v : g.rc) require(v >= 0, BF_ERR_RANK, "negative column rank");
+  // rank_row at l = L must be zero for nu != 0 slots? Level L has 2^L tau and one nu:
+  // the canonical index tau*2^0 + 0 covers all 2^L entries, so nothing is unused.
+  int64_t o = 0;
+  g.u_off.resize(g.nb);
+  for (int64_t t = 0; t < g.nb; ++t) {
+    g.u_off[t] = o;
+    o += g.mt(t) * g.r(g.L, t);
+  }
+  g.len_U = o;
+  o = 0;
+  g.r_off.assign(g.L + 1, {});
+  for (int l = g.lc; l < g.L; ++l) {
+    g.r_off[l].resize(g.nb);
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (g.L - l)); ++nu) {
+        g.r_off[l][g.idx(l, tau, nu)] = o;
+        o += int64_t(g.R_rows(l, tau, nu)) * g.r(l, g.idx(l, tau, nu));
+      }
+  }
+  g.len_R = o;
+  o = 0;
+  g.b_off.resize(g.nb);
+  for (int64_t i = 0; i < g.nb; ++i) {
+    g.b_off[i] = o;
+    o += int64_t(g.r(g.lc, i)) * g.c(g.lc, i);
+  }
+  g.len_B = o;
+  o = 0;
+  g.w_off.assign(g.lc + 1, {});
+  for (int l = 1; l <= g.lc; ++l) {
+    g.w_off[l].resize(g.nb);
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (g.L - l)); ++nu) {
+        g.w_off[l][g.idx(l, tau, nu)] = o;
+        o += int64_t(g.c(l, g.idx(l, tau, nu))) * g.W_cols(l, tau, nu);
+      }
+  }
+  g.len_W = o;
+  o = 0;
+  g.vt_off.resize(g.nb);
+  for (int64_t nu = 0; nu < g.nb; ++nu) {
+    g.vt_off[nu] = o;
+    o += int64_t(g.c(0, nu)) * g.nv(nu);
+  }
+  g.len_Vt = o;
+  require(d.len_U == g.len_U && d.len_R == g.len_R && d.len_B == g.len_B && d.len_W == g.len_W &&
+              d.len_Vt == g.len_Vt,
+          BF_ERR_RANK, "factor array lengths do not match the rank chains");
+  require((g.len_U == 0 || d.U) && (g.len_R == 0 || d.R) && (g.len_B == 0 || d.B) &&
+              (g.len_W == 0 || d.W) && (g.len_Vt == 0 || d.Vt),
+          BF_ERR_ARG, "factor array is NULL");
+  return g;
+}
+
+// factor-pool base offsets (elements) of one butterfly's five arrays
+struct FBase {
+  int64_t u = 0, r = 0, b = 0, w = 0, vt = 0;
+};
+
+// slab-space row offsets of one butterfly's coefficient slabs
+struct Slabs {
+  std::vector<int64_t> row;  // (l - lc) * nb + i, l = lc..L
+  std::vector<int64_t> col;  // l * nb + i,        l = 0..lc
+  int xspace = 0;            // 0 none, 1 row space at lc (op N exchange), 2 col space at lc (op C)
+  std::vector<int64_t> xout, xin;
+  int64_t row_out(const Geom& g, int l, int64_t i) const {
+    return (xspace == 1 && l == g.lc) ? xout[i] : row[(size_t)(l - g.lc) * g.nb + i];
+  }
+  int64_t row_in(const Geom& g, int l, int64_t i) const {
+    return (xspace == 1 && l == g.lc) ? xin[i] : row[(size_t)(l - g.lc) * g.nb + i];
+  }
+  int64_t col_out(const Geom& g, int l, int64_t i) const {
+    return (xspace == 2 && l == g.lc) ? xout[i] : col[(size_t)l * g.nb + i];
+  }
+  int64_t col_in(const Geom& g, int l, int64_t i) const {
+    return (xspace == 2 && l == g.lc) ? xin[i] : col[(size_t)l * g.nb + i];
+  }
+};
+
+// ownership of blocks for the distributed split; p = log2(ranks)
+struct Own {
+  int p = 0;
+  int64_t g = 0;
+  // column side: nu at T_S level L - l lies under nu_g (level p)
+  bool col(const Geom& G, int l, int64_t nu) const { return p == 0 || (nu >> (G.L - l - p)) == g; }
+  // row side: tau at T_O level l lies under tau_g
+  bool row(int l, int64_t tau) const { return p == 0 || (tau >> (l - p)) == g; }
+};
+
+struct PlanBuilder {
+  std::vector<std::vector<Task>> tasks;
+  std::vector<std::vector<Term>> terms;
+  std::vector<int> okind;
+  void add(int round, int out_kind, int64_t out_row, int64_t m, const Term* t, int nt) {
+    if (m <= 0) return;
+    if ((int)tasks.size() <= round) {
+      tasks.resize(round + 1);
+      terms.resize(round + 1);
+      okind.resize(round + 1, -1);
+    }
+    require(okind[round] == -1 || okind[round] == out_kind, BF_ERR_ARG, "internal: mixed out kinds");
+    okind[round] = out_kind;
+    Task tk{};
+    tk.out_row = out_row;
+    tk.m = (int32_t)m;
+    tk.term0 = (int32_t)terms[round].size();
+    tk.nterm = 0;
+    for (int q = 0; q < nt; ++q) {
+      if (t[q].k <= 0) continue;
+      terms[round].push_back(t[q]);
+      tk.nterm++;
+    }
+    tasks[round].push_back(tk);
+  }
+};
+
+static Term mk(int64_t a_off, int a_rs, int a_cs, int64_t k, int64_t in_row, int in_kind, int conj) {
+  Term t{};
+  t.a_off = a_off;
+  t.in_row = in_row;
+  t.a_rs = a_rs;
+  t.a_cs = a_cs;
+  t.k = (int32_t)k;
+  t.conj = (int16_t)conj;
+  t.in_kind = (int16_t)in_kind;
+  return t;
+}
+
+struct EmitOpts {
+  bool leaf_in = true, leaf_out = true;  // emit the V / U leaf stages (HOD-BF fuses them)
+  int64_t x_base = 0, y_base = 0;        // tree position of local X / Y row 0
+  Own own;
+};
+
+// op N rounds: 0 leaf V, 1..lc W, lc+1 B, lc+2.. R, L+2 leaf U
+static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& S, const EmitOpts& o) {
+  const int L = G.L, lc = G.lc;
+  if (o.leaf_in)
+    for (int64_t nu = 0; nu < G.nb; ++nu) {
+      if (!o.own.col(G, 0, nu)) continue;
+      const int c = G.c(0, nu);
+      Term t = mk(F.vt + G.vt_off[nu], 1, c, G.nv(nu), G.clp[nu] - o.x_base, 1, 0);
+      pb.add(0, 0, S.col_out(G, 0, nu), c, &t, 1);
+    }
+  for (int l = 1; l <= lc; ++l)
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        if (!o.own.col(G, l, nu)) continue;
+        const int64_t i = G.idx(l, tau, nu);
+        const int64_t i1 = G.idx(l - 1, tau >> 1, 2 * nu), i2 = i1 + 1;
+        const int c = G.c(l, i), c1 = G.c(l - 1, i1), c2 = G.c(l - 1, i2);
+        Term t[2] = {mk(F.w + G.w_off[l][i], 1, c, c1, S.col_in(G, l - 1, i1), 0, 0),
+                     mk(F.w + G.w_off[l][i] + int64_t(c1) * c, 1, c, c2, S.col_in(G, l - 1, i2), 0, 0)};
+        if (c1 > 0 && c2 > 0 && t[1].in_row == t[0].in_row + c1) {  // adjacent inputs: one term
+          t[0].k = c1 + c2;
+          pb.add(l, 0, S.col_out(G, l, i), c, t, 1);
+        } else {
+          pb.add(l, 0, S.col_out(G, l, i), c, t, 2);
+        }
+      }
+  for (int64_t i = 0; i < G.nb; ++i) {
+    const int64_t nu = i & ((int64_t(1) << (L - lc)) - 1);
+    if (!o.own.col(G, lc, nu)) continue;
+    const int r = G.r(lc, i), c = G.c(lc, i);
+    Term t = mk(F.b + G.b_off[i], 1, r, c, S.col_in(G, lc, i), 0, 0);
+    pb.add(lc + 1, 0, S.row_out(G, lc, i), r, &t, 1);
+  }
+  for (int l = lc; l < L; ++l)
+    for (int64_t tp = 0; tp < (int64_t(1) << (l + 1)); ++tp)
+      for (int64_t np = 0; np < (int64_t(1) << (L - l - 1)); ++np) {
+        if (!o.own.row(l + 1, tp)) continue;
+        const int64_t a = tp >> 1;
+        const int part = (int)(tp & 1);
+        const int rt = G.r(l + 1, G.idx(l + 1, 2 * a, np)), rb = G.r(l + 1, G.idx(l + 1, 2 * a + 1, np));
+        Term t[2];
+        for (int s = 0; s < 2; ++s) {
+          const int64_t i = G.idx(l, a, 2 * np + s);
+          t[s] = mk(F.r + G.r_off[l][i] + (part ? rt : 0), 1, rt + rb, G.r(l, i), S.row_in(G, l, i), 0, 0);
+        }
+        const int64_t io = G.idx(l + 1, tp, np);
+        pb.add(lc + 2 + (l - lc), 0, S.row_out(G, l + 1, io), G.r(l + 1, io), t, 2);
+      }
+  if (o.leaf_out)
+    for (int64_t tau = 0; tau < G.nb; ++tau) {
+      if (!o.own.row(L, tau)) continue;
+      Term t = mk(F.u + G.u_off[tau], 1, (int)G.mt(tau), G.r(L, tau), S.row_in(G, L, tau), 0, 0);
+      pb.add(L + 2, 1, G.rlp[tau] - o.y_base, G.mt(tau), &t, 1);
+    }
+}
+
+// op C rounds: 0 leaf U^H, 1..L-lc R^H, L-lc+1 B^H, .. W^H, L+2 leaf Vt^H
+static void emit_C(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& S, const EmitOpts& o) {
+  const int L = G.L, lc = G.lc;
+  if (o.leaf_in)
+    for (int64_t tau = 0; tau < G.nb; ++tau) {
+      if (!o.own.row(L, tau)) continue;
+      const int r = G.r(L, tau);
+      Term t = mk(F.u + G.u_off[tau], (int)G.mt(tau), 1, G.mt(tau), G.rlp[tau] - o.x_base, 1, 1);
+      pb.add(0, 0, S.row_out(G, L, tau), r, &t, 1);
+    }
+  for (int l = L - 1; l >= lc; --l)
+    for (int64_t a = 0; a < (int64_t(1) << l); ++a)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        if (!o.own.row(l, a)) continue;
+        const int64_t i = G.idx(l, a, nu);
+        const int64_t it = G.idx(l + 1, 2 * a, nu >> 1), ib = G.idx(l + 1, 2 * a + 1, nu >> 1);
+        const int rt = G.r(l + 1, it), rb = G.r(l + 1, ib);
+        Term t[2] = {mk(F.r + G.r_off[l][i], rt + rb, 1, rt, S.row_in(G, l + 1, it), 0, 1),
+                     mk(F.r + G.r_off[l][i] + rt, rt + rb, 1, rb, S.row_in(G, l + 1, ib), 0, 1)};
+        pb.add(1 + (L - 1 - l), 0, S.row_out(G, l, i), G.r(l, i), t, 2);
+      }
+  for (int64_t i = 0; i < G.nb; ++i) {
+    const int64_t tau = i >> (L - lc);
+    if (!o.own.row(lc, tau)) continue;
+    const int r = G.r(lc, i), c = G.c(lc, i);
+    Term t = mk(F.b + G.b_off[i], r, 1, r, S.row_in(G, lc, i), 0, 1);
+    pb.add(L - lc + 1, 0, S.col_out(G, lc, i), c, &t, 1);
+  }
+  for (int l = lc; l >= 1; --l)
+    for (int64_t a = 0; a < (int64_t(1) << (l - 1)); ++a)
+      for (int64_t mu = 0; mu < (int64_t(1) << (L - l + 1)); ++mu) {
+        if (!o.own.col(G, l - 1, mu)) continue;
+        const int64_t nu = mu >> 1;
+        const int b = (int)(mu & 1);
+        const int64_t io = G.idx(l - 1, a, mu);
+        const int c1 = G.c(l - 1, G.idx(l - 1, a, 2 * nu));
+        Term t[2];
+        for (int s = 0; s < 2; ++s) {
+          const int64_t i = G.idx(l, 2 * a + s, nu);
+          const int cl = G.c(l, i);
+          t[s] = mk(F.w + G.w_off[l][i] + int64_t(b ? c1 : 0) * cl, cl, 1, cl, S.col_in(G, l, i), 0, 1);
+        }
+        pb.add(L - lc + 2 + (lc - l), 0, S.col_out(G, l - 1, io), G.c(l - 1, io), t, 2);
+      }
+  if (o.leaf_out)
+    for (int64_t nu = 0; nu < G.nb; ++nu) {
+      if (!o.own.col(G, 0, nu)) continue;
+      const int c = G.c(0, nu);
+      Term t = mk(F.vt + G.vt_off[nu], c, 1, c, S.col_in(G, 0, nu), 0, 1);
+      pb.add(L + 2, 1, G.clp[nu] - o.y_base, G.nv(nu), &t, 1);
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// device plan
+// --------------------------------------------------------------------------------------
+struct Plan {
+  std::vector<Round> rounds;
+  void* dev = nullptr;
+  int launches() const {
+    int k = 0;
+    for (auto& r : rounds) k += r.ntasks > 0;
+    return k;
+  }
+};
+
+static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, size_t* bytes) {
+  size_t tot = 0;
+  std::vector<size_t> toff, xoff;
+  for (int r = round_lo; r < round_hi && r < (int)pb.tasks.size(); ++r) {
+    toff.push_back(tot);
+    tot += pb.tasks[r].size() * sizeof(Task);
+    tot = (tot + 255) & ~size_t(255);
+    xoff.push_back(tot);
+    tot += pb.terms[r].size() * sizeof(Term);
+    tot = (tot + 255) & ~size_t(255);
+  }
+  if (tot == 0) return;
+  std::vector<char> host(tot);
+  for (int r = round_lo, q = 0; r < round_hi && r < (int)pb.tasks.size(); ++r, ++q) {
+    if (!pb.tasks[r].empty()) memcpy(host.data() + toff[q], pb.tasks[r].data(), pb.tasks[r].size() * sizeof(Task));
+    if (!pb.terms[r].empty()) memcpy(host.data() + xoff[q], pb.terms[r].data(), pb.terms[r].size() * sizeof(Term));
+  }
+  BF_CK(cudaMalloc(&P.dev, tot));
+  BF_CK(cudaMemcpy(P.dev, host.data(), tot, cudaMemcpyHostToDevice));
+  *bytes += tot;
+  for (int r = round_lo, q = 0; r < round_hi && r < (int)pb.tasks.size(); ++r, ++q) {
+    Round R{};
+    R.tasks = reinterpret_cast<const Task*>((char*)P.dev + toff[q]);
+    R.terms = reinterpret_cast<const Term*>((char*)P.dev + xoff[q]);
+    R.ntasks = (int32_t)pb.tasks[r].size();
+    R.out_kind = pb.okind[r] < 0 ? 0 : pb.okind[r];
+    int mm = 0, mk_ = 0;
+    for (auto& t : pb.tasks[r]) mm = std::max(mm, t.m);
+    for (auto& t : pb.terms[r]) mk_ = std::max(mk_, t.k);
+    R.max_m = mm;
+    R.max_k = mk_;
+    for (auto& t : pb.tasks[r]) {
+      if (pb.okind[r] == 1)
+        R.user_out += t.m;
+      else
+        R.slab_out += t.m;
+      for (int q = 0; q < t.nterm; ++q) {
+        const Term& x = pb.terms[r][t.term0 + q];
+        R.factor_entries += int64_t(t.m) * x.k;
+        if (x.in_kind == 1)
+          R.user_in += x.k;
+        else
+          R.slab_in += x.k;
+      }
+    }
+    if (R.ntasks > 0) P.rounds.push_back(R);
+  }
+}
+
+static void free_plan(Plan& P) {
+  if (P.dev) cudaFree(P.dev);
+  P.dev = nullptr;
+  P.rounds.clear();
+}
+
+static void run_plan(int dtype, const Plan& P, StageArgs a, cudaStream_t st, void* const* ev = nullptr,
+                     int nev = 0) {
+  if (ev) require(nev >= (int)P.rounds.size() + 1, BF_ERR_ARG, "need nrounds + 1 events");
+  for (size_t i = 0; i < P.rounds.size(); ++i) {
+    if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), st));
+    launch_round(dtype, P.rounds[i], a, st);
+  }
+  if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[P.rounds.size()]), st));
+  BF_CK(cudaGetLastError());
+}
+
+static void round_info(int dtype, const Plan& P, int round, bf_round_info_t* info) {
+  require(info != nullptr && round >= 0 && round < (int)P.rounds.size(), BF_ERR_ARG, "round out of range");
+  const Round& r = P.rounds[round];
+  memset(info, 0, sizeof(*info));
+  int id = 0;
+  const char* nm = round_kernel_name(dtype, r, &id);
+  info->kernel = id;
+  info->ntasks = r.ntasks;
+  info->factor_entries = r.factor_entries;
+  info->user_rows_in = r.user_in;
+  info->user_rows_out = r.user_out;
+  info->slab_rows_in = r.slab_in;
+  info->slab_rows_out = r.slab_out;
+  strncpy(info->name, nm, sizeof(info->name) - 1);
+}
+
+}  // namespace bfa
+
+// ======================================================================================
+// handles
+// ======================================================================================
+using namespace bfa;
+
+struct bf_s {
+  int dtype = BF_C128;
+  int device = 0;
+  Geom G;
+  void* pool = nullptr;
+  int64_t* d_rperm = nullptr;
+  int64_t* d_cperm = nullptr;
+  int64_t slab_rows = 0;
+  int64_t factor_entries = 0;
+  size_t device_bytes = 0;
+  Plan plan[2];  // [0] op N, [1] op C/T
+  // distributed
+  bool dist = false;
+  int rank = 0, nranks = 1;
+  Plan pre[2], post[2];
+  int64_t send_rows[2] = {0, 0}, recv_rows[2] = {0, 0};
+  int64_t send_base[2] = {0, 0}, recv_base[2] = {0, 0};  // slab rows
+  std::vector<int64_t> send_cnt[2], recv_cnt[2];         // rows per peer
+  int64_t loc_rows_in[2] = {0, 0}, loc_rows_out[2] = {0, 0};
+  int64_t loc_user_in[2] = {0, 0}, loc_user_out[2] = {0, 0};
+  int64_t* d_lperm_in[2] = {nullptr, nullptr};
+  int64_t* d_lperm_out[2] = {nullptr, nullptr};
+  ~bf_s() {
+    cudaSetDevice(device);
+    for (int k = 0; k < 2; ++k) {
+      free_plan(plan[k]);
+      free_plan(pre[k]);
+      free_plan(post[k]);
+      if (d_lperm_in[k]) cudaFree(d_lperm_in[k]);
+      if (d_lperm_out[k]) cudaFree(d_lperm_out[k]);
+    }
+    if (pool) cudaFree(pool);
+    if (d_rperm) cudaFree(d_rperm);
+    if (d_cperm) cudaFree(d_cperm);
+  }
+};
+
+struct hodbf_s {
+  int dtype = BF_C128;
+  int device = 0;
+  int64_t n = 0;
+  int LH = 0;
+  void* pool = nullptr;
+  int64_t* d_perm = nullptr;
+  int64_t slab_rows = 0;
+  int64_t factor_entries = 0;
+  size_t device_bytes = 0;
+  Plan plan[2];
+  ~hodbf_s() {
+    cudaSetDevice(device);
+    free_plan(plan[0]);
+    free_plan(plan[1]);
+    if (pool) cudaFree(pool);
+    if (d_perm) cudaFree(d_perm);
+  }
+};
+
+namespace bfa {
+
+static int fail(const Err& e) {
+  g_last_error = e.msg;
+  return e.code;
+}
+
+static void check_device(int device) {
+  int cnt = 0;
+  cudaError_t e = cudaGetDeviceCount(&cnt);
+  require(e == cudaSuccess && cnt > 0, BF_ERR_DEVICE, "no CUDA device available (libbfapply has no CPU path)");
+  require(device >= 0 && device < cnt, BF_ERR_DEVICE, "device index out of range");
+  int major = 0;
+  BF_CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  require(major == 10, BF_ERR_DEVICE, "libbfapply is built for sm_100a (B200); device is not compute capability 10.x");
+}
+
+static void* upload(const void* h, size_t bytes, size_t* acct) {
+  if (bytes == 0) return nullptr;
+  void* d = nullptr;
+  BF_CK(cudaMalloc(&d, bytes));
+  BF_CK(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+  *acct += bytes;
+  return d;
+}
+
+// canonical slab allocation for a whole (single-GPU) butterfly: col space 0..lc, row space lc..L
+static Slabs canonical_slabs(const Geom& G, int64_t& cursor) {
+  Slabs S;
+  S.col.assign((size_t)(G.lc + 1) * G.nb, -1);
+  S.row.assign((size_t)(G.L - G.lc + 1) * G.nb, -1);
+  for (int l = 0; l <= G.lc; ++l)
+    for (int64_t i = 0; i < G.nb; ++i) {
+      S.col[(size_t)l * G.nb + i] = cursor;
+      cursor += G.c(l, i);
+    }
+  for (int l = G.lc; l <= G.L; ++l)
+    for (int64_t i = 0; i < G.nb; ++i) {
+      S.row[(size_t)(l - G.lc) * G.nb + i] = cursor;
+      cursor += G.r(l, i);
+    }
+  return S;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+static void validate_apply(int64_t nrhs, const void* X, int64_t ldx, int64_t rows_x, const void* Y,
+                           int64_t ldy, int64_t rows_y, size_t work_bytes, size_t need) {
+  require(nrhs >= 0, BF_ERR_ARG, "nrhs < 0");
+  if (nrhs == 0) return;
+  require(X != nullptr && Y != nullptr, BF_ERR_ARG, "X or Y is NULL");
+  require(X != Y, BF_ERR_ARG, "X and Y must not alias");
+  require(ldx >= std::max<int64_t>(rows_x, 1) && ldy >= std::max<int64_t>(rows_y, 1), BF_ERR_ARG,
+          "leading dimension smaller than the number of rows");
+  require(work_bytes >= need, BF_ERR_ARG, "workspace too small");
+}
+
+}  // namespace bfa
+
+// ======================================================================================
+// C ABI
+// ======================================================================================
+extern "C" {
+
+const char* bf_status_string(int s) {
+  switch (s) {
+    case BF_OK: return "BF_OK";
+    case BF_ERR_ARG: return "BF_ERR_ARG";
+    case BF_ERR_SHAPE: return "BF_ERR_SHAPE";
+    case BF_ERR_RANK: return "BF_ERR_RANK";
+    case BF_ERR_PERM: return "BF_ERR_PERM";
+    case BF_ERR_CUDA: return "BF_ERR_CUDA";
+    case BF_ERR_OOM: return "BF_ERR_OOM";
+    case BF_ERR_NCCL: return "BF_ERR_NCCL";
+    case BF_ERR_DEVICE: return "BF_ERR_DEVICE";
+    default: return "BF_ERR_UNKNOWN";
+  }
+}
+
+const char* bf_last_error(void) { return bfa::g_last_error.c_str(); }
+
+const char* bf_version(void) { return "bfapply 0.1 sm_100a"; }
+
+int bf_create(const bf_desc* d, int device, bf_handle* out) {
+  if (!d || !out) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  *out = nullptr;
+  try {
+    Geom G = make_geom(*d);
+    check_perm(d->row_perm, d->m, "row_perm");
+    check_perm(d->col_perm, d->n, "col_perm");
+    check_device(device);
+    DeviceGuard dg(device);
+    std::unique_ptr<bf_s> h(new bf_s());
+    h->dtype = d->dtype;
+    h->device = device;
+    const size_t cs = csize(d->dtype);
+    const int64_t tot = G.len_U + G.len_R + G.len_B + G.len_W + G.len_Vt;
+    h->factor_entries = tot;
+    FBase F;
+    F.u = 0;
+    F.r = G.len_U;
+    F.b = F.r + G.len_R;
+    F.w = F.b + G.len_B;
+    F.vt = F.w + G.len_W;
+    if (tot > 0) {
+      BF_CK(cudaMalloc(&h->pool, (size_t)tot * cs));
+      h->device_bytes += (size_t)tot * cs;
+      char* p = static_cast<char*>(h->pool);
+      if (G.len_U) BF_CK(cudaMemcpy(p + F.u * cs, d->U, G.len_U * cs, cudaMemcpyHostToDevice));
+      if (G.len_R) BF_CK(cudaMemcpy(p + F.r * cs, d->R, G.len_R * cs, cudaMemcpyHostToDevice));
+      if (G.len_B) BF_CK(cudaMemcpy(p + F.b * cs, d->B, G.len_B * cs, cudaMemcpyHostToDevice));
+      if (G.len_W) BF_CK(cudaMemcpy(p + F.w * cs, d->W, G.len_W * cs, cudaMemcpyHostToDevice));
+      if (G.len_Vt) BF_CK(cudaMemcpy(p + F.vt * cs, d->Vt, G.len_Vt * cs, cudaMemcpyHostToDevice));
+    }
+    if (d->row_perm) h->d_rperm = (int64_t*)upload(d->row_perm, d->m * 8, &h->device_bytes);
+    if (d->col_perm) h->d_cperm = (int64_t*)upload(d->col_perm, d->n * 8, &h->device_bytes);
+    int64_t cursor = 0;
+    Slabs S = canonical_slabs(G, cursor);
+    h->slab_rows = cursor;
+    for (int k = 0; k < 2; ++k) {
+      PlanBuilder pb;
+      EmitOpts o;
+      if (k == 0)
+        emit_N(pb, G, F, S, o);
+      else
+        emit_C(pb, G, F, S, o);
+      upload_plan(h->plan[k], pb, 0, (int)pb.tasks.size(), &h->device_bytes);
+    }
+    h->G = std::move(G);
+    *out = h.release();
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    return fail(Err{BF_ERR_OOM, "host allocation failed"});
+  }
+}
+
+int bf_destroy(bf_handle h) {
+  delete h;
+  return BF_OK;
+}
+
+int bf_info(bf_handle h, bf_info_t* info) {
+  if (!h || !info) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  info->factor_entries = h->factor_entries;
+  info->device_bytes = (int64_t)h->device_bytes;
+  if (h->dist) {
+    info->launches_n = h->pre[0].launches() + h->post[0].launches();
+    info->launches_c = h->pre[1].launches() + h->post[1].launches();
+  } else {
+    info->launches_n = h->plan[0].launches();
+    info->launches_c = h->plan[1].launches();
+  }
+  info->rows_in = h->G.n;
+  info->rows_out = h->G.m;
+  return BF_OK;
+}
+
+int bf_workspace_size(bf_handle h, int64_t nrhs, size_t* bytes) {
+  if (!h || !bytes || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
+  *bytes = align256((size_t)h->slab_rows * (size_t)nrhs * csize(h->dtype));
+  return BF_OK;
+}
+
+int bf_apply_op_events(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                       void* work, size_t work_bytes, bf_stream_t stream, void* const* events, int32_t nevents) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    require(op == BF_OP_N || op == BF_OP_C || op == BF_OP_T, BF_ERR_ARG, "bad op");
+    require(!h->dist, BF_ERR_ARG, "distributed handle: use bf_dist_apply_pre/post");
+    const bool fwd = op == BF_OP_N;
+    const int64_t rx = fwd ? h->G.n : h->G.m, ry = fwd ? h->G.m : h->G.n;
+    size_t need = 0;
+    bf_workspace_size(h, nrhs, &need);
+    validate_apply(nrhs, X, ldx, rx, Y, ldy, ry, work_bytes, need);
+    if (nrhs == 0 || ry == 0) return BF_OK;
+    require(need == 0 || work != nullptr, BF_ERR_ARG, "workspace is NULL");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (rx == 0 || h->plan[fwd ? 0 : 1].rounds.empty()) {
+      // K has no columns (or no entries): Y = 0
+      for (int64_t j = 0; j < nrhs; ++j)
+        BF_CK(cudaMemsetAsync((char*)Y + (size_t)j * ldy * csize(h->dtype), 0, (size_t)ry * csize(h->dtype), st));
+    }
+    StageArgs a{};
+    a.pool = h->pool;
+    a.X = X;
+    a.ldx = ldx;
+    a.xperm = fwd ? h->d_cperm : h->d_rperm;
+    a.S = work;
+    a.ldS = nrhs;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.yperm = fwd ? h->d_rperm : h->d_cperm;
+    a.conj_flip = (op == BF_OP_T) ? 1 : 0;
+    a.nrhs = (int32_t)nrhs;
+    require(nrhs <= (int64_t)65535 * 32, BF_ERR_ARG, "nrhs too large for one launch");
+    run_plan(h->dtype, h->plan[fwd ? 0 : 1], a, st, events, nevents);
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+int bf_apply_op(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                void* work, size_t work_bytes, bf_stream_t stream) {
+  return bf_apply_op_events(h, op, nrhs, X, ldx, Y, ldy, work, work_bytes, stream, nullptr, 0);
+}
+
+int bf_rounds(bf_handle h, int op, int32_t* n) {
+  if (!h || !n) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  const int k = op == BF_OP_N ? 0 : 1;
+  *n = h->dist ? (int32_t)(h->pre[k].rounds.size() + h->post[k].rounds.size()) : (int32_t)h->plan[k].rounds.size();
+  return BF_OK;
+}
+
+int bf_round_info(bf_handle h, int op, int32_t round, bf_round_info_t* info) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    const int k = op == BF_OP_N ? 0 : 1;
+    if (h->dist) {
+      const int np = (int)h->pre[k].rounds.size();
+      if (round < np)
+        round_info(h->dtype, h->pre[k], round, info);
+      else
+        round_info(h->dtype, h->post[k], round - np, info);
+    } else {
+      round_info(h->dtype, h->plan[k], round, info);
+    }
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+int bf_apply(bf_handle h, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy, void* work,
+             size_t work_bytes, bf_stream_t stream) {
+  return bf_apply_op(h, BF_OP_N, nrhs, X, ldx, Y, ldy, work, work_bytes, stream);
+}
+
+int bf_apply_adj(bf_handle h, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy, void* work,
+                 size_t work_bytes, bf_stream_t stream) {
+  return bf_apply_op(h, BF_OP_C, nrhs, X, ldx, Y, ldy, work, work_bytes, stream);
+}
+
+int bf_workspace_size_host(bf_handle h, int op, int64_t nrhs, size_t* bytes) {
+  if (!h || !bytes || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
+  const bool fwd = op == BF_OP_N;
+  const int64_t rx = fwd ? h->G.n : h->G.m, ry = fwd ? h->G.m : h->G.n;
+  size_t s = 0;
+  bf_workspace_size(h, nrhs, &s);
+  const size_t cs = csize(h->dtype);
+  *bytes = s + align256((size_t)rx * nrhs * cs) + align256((size_t)ry * nrhs * cs);
+  return BF_OK;
+}
+
+int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx, void* Yh, int64_t ldy,
+                  void* work, size_t work_bytes, bf_stream_t stream) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    const bool fwd = op == BF_OP_N;
+    const int64_t rx = fwd ? h->G.n : h->G.m, ry = fwd ? h->G.m : h->G.n;
+    size_t need = 0, s = 0;
+    bf_workspace_size_host(h, op, nrhs, &need);
+    bf_workspace_size(h, nrhs, &s);
+    validate_apply(nrhs, Xh, ldx, rx, Yh, ldy, ry, work_bytes, need);
+    if (nrhs == 0) return BF_OK;
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t cs = csize(h->dtype);
+    char* dX = static_cast<char*>(work) + s;
+    char* dY = dX + align256((size_t)rx * nrhs * cs);
+    // one copy per call when the host block is dense, else one per column
+    if (ldx == rx) {
+      BF_CK(cudaMemcpyAsync(dX, Xh, (size_t)rx * nrhs * cs, cudaMemcpyHostToDevice, st));
+    } else {
+      BF_CK(cudaMemcpy2DAsync(dX, rx * cs, Xh, ldx * cs, rx * cs, nrhs, cudaMemcpyHostToDevice, st));
+    }
+    int rc = bf_apply_op(h, op, nrhs, dX, std::max<int64_t>(rx, 1), dY, std::max<int64_t>(ry, 1), work, s, stream);
+    if (rc != BF_OK) return rc;
+    if (ldy == ry) {
+      BF_CK(cudaMemcpyAsync(Yh, dY, (size_t)ry * nrhs * cs, cudaMemcpyDeviceToHost, st));
+    } else {
+      BF_CK(cudaMemcpy2DAsync(Yh, ldy * cs, dY, ry * cs, ry * cs, nrhs, cudaMemcpyDeviceToHost, st));
+    }
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// HOD-BF
+// --------------------------------------------------------------------------------------
+int hodbf_create(const hodbf_desc* d, int device, hodbf_handle* out) {
+  if (!d || !out) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  *out = nullptr;
+  try {
+    require(d->dtype == BF_C64 || d->dtype == BF_C128, BF_ERR_ARG, "bad dtype");
+    require(d->LH >= 0 && d->LH <= 20, BF_ERR_SHAPE, "LH out of range [0, 20]");
+    const int LH = d->LH;
+    const int64_t nleaf = int64_t(1) << LH;
+    check_leafptr(d->leaf_ptr, nleaf, d->n, "leaf_ptr");
+    check_perm(d->perm, d->n, "perm");
+    const int64_t* lp = d->leaf_ptr;
+    int64_t lenD = 0;
+    for (int64_t t = 0; t < nleaf; ++t) lenD += (lp[t + 1] - lp[t]) * (lp[t + 1] - lp[t]);
+    require(d->len_D == lenD && (lenD == 0 || d->D), BF_ERR_SHAPE, "len_D does not match the leaf sizes");
+    const int64_t nbf = 2 * nleaf - 2;
+    require(nbf == 0 || d->offdiag, BF_ERR_ARG, "offdiag is NULL");
+    // geometry of every off-diagonal butterfly, checked against the HOD-BF tree
+    std::vector<Geom> G(nbf);
+    for (int l = 1; l <= LH; ++l)
+      for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau) {
+        const int64_t k = (int64_t(1) << l) - 2 + tau;
+        const bf_desc& b = d->offdiag[k];
+        require(b.dtype == d->dtype, BF_ERR_ARG, "offdiag dtype differs");
+        require(b.L == LH - l, BF_ERR_SHAPE, "offdiag butterfly must have LH - l levels");
+        require(b.row_perm == nullptr && b.col_perm == nullptr, BF_ERR_PERM, "offdiag perms must be NULL (tree-local)");
+        G[k] = make_geom(b);
+        const int64_t w = int64_t(1) << (LH - l);
+        const int64_t sib = tau ^ 1;
+        for (int64_t q = 0; q <= w; ++q) {
+          require(G[k].rlp[q] == lp[tau * w + q] - lp[tau * w], BF_ERR_SHAPE, "offdiag row leaves differ from T_H");
+          require(G[k].clp[q] == lp[sib * w + q] - lp[sib * w], BF_ERR_SHAPE, "offdiag column leaves differ from T_H");
+        }
+      }
+    check_device(device);
+    DeviceGuard dg(device);
+    std::unique_ptr<hodbf_s> h(new hodbf_s());
+    h->dtype = d->dtype;
+    h->device = device;
+    h->n = d->n;
+    h->LH = LH;
+    const size_t cs = csize(d->dtype);
+    auto bf_of_row_leaf = [&](int l, int64_t t, int64_t* k, int64_t* loc) {  // butterfly whose row tree holds t
+      const int64_t sig = t >> (LH - l);
+      *k = (int64_t(1) << l) - 2 + sig;
+      *loc = t - (sig << (LH - l));
+    };
+    auto bf_of_col_leaf = [&](int l, int64_t t, int64_t* k, int64_t* loc) {  // column tree holds t
+      const int64_t sig = t >> (LH - l);
+      *k = (int64_t(1) << l) - 2 + (sig ^ 1);
+      *loc = t - (sig << (LH - l));
+    };
+    // ---- pool layout: per leaf M_t = [D_t | U^(1)_t .. U^(LH)_t], per leaf stacked Vt, then R/B/W per bf
+    std::vector<int64_t> M_off(nleaf), SV_off(nleaf), sumr(nleaf, 0), sumc(nleaf, 0);
+    int64_t o = 0;
+    for (int64_t t = 0; t < nleaf; ++t) {
+      const int64_t mt = lp[t + 1] - lp[t];
+      for (int l = 1; l <= LH; ++l) {
+        int64_t k, loc;
+        bf_of_row_leaf(l, t, &k, &loc);
+        sumr[t] += G[k].r(G[k].L, loc);
+        bf_of_col_leaf(l, t, &k, &loc);
+        sumc[t] += G[k].c(0, loc);
+      }
+      M_off[t] = o;
+      o += mt * (mt + sumr[t]);
+    }
+    for (int64_t t = 0; t < nleaf; ++t) {
+      SV_off[t] = o;
+      o += sumc[t] * (lp[t + 1] - lp[t]);
+    }
+    std::vector<FBase> F(nbf);
+    int64_t entries = lenD;
+    for (int64_t k = 0; k < nbf; ++k) {
+      F[k].r = o;
+      o += G[k].len_R;
+      F[k].b = o;
+      o += G[k].len_B;
+      F[k].w = o;
+      o += G[k].len_W;
+      entries += G[k].len_U + G[k].len_R + G[k].len_B + G[k].len_W + G[k].len_Vt;
+    }
+    const int64_t pool_len = o;
+    h->factor_entries = entries;
+    std::vector<char> host((size_t)pool_len * cs);
+    char* hp = host.data();
+    const char* Dsrc = static_cast<const char*>(d->D);
+    int64_t doff = 0;
+    for (int64_t t = 0; t < nleaf; ++t) {
+      const int64_t mt = lp[t + 1] - lp[t];
+      char* dst = hp + M_off[t] * cs;
+      if (mt) memcpy(dst, Dsrc + doff * cs, (size_t)(mt * mt) * cs);
+      doff += mt * mt;
+      int64_t col = mt;
+      int64_t row = 0;
+      for (int l = 1; l <= LH; ++l) {
+        int64_t k, loc;
+        bf_of_row_leaf(l, t, &k, &loc);
+        const int r = G[k].r(G[k].L, loc);
+        const char* U = static_cast<const char*>(d->offdiag[k].U) + G[k].u_off[loc] * cs;
+        if (mt * r) memcpy(dst + col * mt * cs, U, (size_t)(mt * r) * cs);
+        col += r;
+        // stacked Vt: rows [row, row + c) of the (sumc x mt) column-major matrix
+        bf_of_col_leaf(l, t, &k, &loc);
+        const int c = G[k].c(0, loc);
+        const char* Vt = static_cast<const char*>(d->offdiag[k].Vt) + G[k].vt_off[loc] * cs;
+        char* sv = hp + SV_off[t] * cs;
+        for (int64_t j = 0; j < mt; ++j)
+          if (c) memcpy(sv + (j * sumc[t] + row) * cs, Vt + j * c * cs, (size_t)c * cs);
+        row += c;
+      }
+    }
+    for (int64_t k = 0; k < nbf; ++k) {
+      const bf_desc& b = d->offdiag[k];
+      if (G[k].len_R) memcpy(hp + F[k].r * cs, b.R, (size_t)G[k].len_R * cs);
+      if (G[k].len_B) memcpy(hp + F[k].b * cs, b.B, (size_t)G[k].len_B * cs);
+      if (G[k].len_W) memcpy(hp + F[k].w * cs, b.W, (size_t)G[k].len_W * cs);
+    }
+    if (pool_len) h->pool = upload(hp, (size_t)pool_len * cs, &h->device_bytes);
+    if (d->perm) h->d_perm = (int64_t*)upload(d->perm, d->n * 8, &h->device_bytes);
+    // ---- slab space: per leaf the z^0 group and the y^L group, then each bf's inner levels
+    std::vector<Slabs> S(nbf);
+    for (int64_t k = 0; k < nbf; ++k) {
+      S[k].col.assign((size_t)(G[k].lc + 1) * G[k].nb, -1);
+      S[k].row.assign((size_t)(G[k].L - G[k].lc + 1) * G[k].nb, -1);
+    }
+    std::vector<int64_t> zgrp(nleaf), ygrp(nleaf);
+    int64_t cur = 0;
+    for (int64_t t = 0; t < nleaf; ++t) {
+      zgrp[t] = cur;
+      for (int l = 1; l <= LH; ++l) {
+        int64_t k, loc;
+        bf_of_col_leaf(l, t, &k, &loc);
+        S[k].col[loc] = cur;
+        cur += G[k].c(0, loc);
+      }
+      ygrp[t] = cur;
+      for (int l = 1; l <= LH; ++l) {
+        int64_t k, loc;
+        bf_of_row_leaf(l, t, &k, &loc);
+        S[k].row[(size_t)(G[k].L - G[k].lc) * G[k].nb + loc] = cur;
+        cur += G[k].r(G[k].L, loc);
+      }
+    }
+    for (int64_t k = 0; k < nbf; ++k) {
+      const Geom& g = G[k];
+      for (int l = 1; l <= g.lc; ++l)
+        for (int64_t i = 0; i < g.nb; ++i) {
+          S[k].col[(size_t)l * g.nb + i] = cur;
+          cur += g.c(l, i);
+        }
+      for (int l = g.lc; l < g.L; ++l)
+        for (int64_t i = 0; i < g.nb; ++i) {
+          S[k].row[(size_t)(l - g.lc) * g.nb + i] = cur;
+          cur += g.r(l, i);
+        }
+    }
+    h->slab_rows = cur;
+    // ---- plans
+    for (int op = 0; op < 2; ++op) {
+      PlanBuilder pb;
+      for (int64_t t = 0; t < nleaf; ++t) {
+        const int64_t mt = lp[t + 1] - lp[t];
+        if (op == 0) {
+          Term tm = mk(SV_off[t], 1, (int)std::max<int64_t>(sumc[t], 1), mt, lp[t], 1, 0);
+          pb.add(0, 0, zgrp[t], sumc[t], &tm, 1);
+        } else {
+          Term tm = mk(M_off[t] + mt * mt, (int)std::max<int64_t>(mt, 1), 1, mt, lp[t], 1, 1);
+          pb.add(0, 0, ygrp[t], sumr[t], &tm, 1);
+        }
+      }
+      for (int64_t k = 0; k < nbf; ++k) {
+        EmitOpts eo;
+        eo.leaf_in = eo.leaf_out = false;
+        if (op == 0)
+          emit_N(pb, G[k], F[k], S[k], eo);
+        else
+          emit_C(pb, G[k], F[k], S[k], eo);
+      }
+      for (int64_t t = 0; t < nleaf; ++t) {
+        const int64_t mt = lp[t + 1] - lp[t];
+        Term tm[2];
+        if (op == 0) {
+          tm[0] = mk(M_off[t], 1, (int)std::max<int64_t>(mt, 1), mt, lp[t], 1, 0);
+          tm[1] = mk(M_off[t] + mt * mt, 1, (int)std::max<int64_t>(mt, 1), sumr[t], ygrp[t], 0, 0);
+        } else {
+          tm[0] = mk(M_off[t], (int)std::max<int64_t>(mt, 1), 1, mt, lp[t], 1, 1);
+          tm[1] = mk(SV_off[t], (int)std::max<int64_t>(sumc[t], 1), 1, sumc[t], zgrp[t], 0, 1);
+        }
+        pb.add(LH + 1, 1, lp[t], mt, tm, 2);
+      }
+      upload_plan(h->plan[op], pb, 0, (int)pb.tasks.size(), &h->device_bytes);
+    }
+    *out = h.release();
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    return fail(Err{BF_ERR_OOM, "host allocation failed"});
+  }
+}
+
+int hodbf_destroy(hodbf_handle h) {
+  delete h;
+  return BF_OK;
+}
+
+int hodbf_info(hodbf_handle h, bf_info_t* info) {
+  if (!h || !info) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  info->factor_entries = h->factor_entries;
+  info->device_bytes = (int64_t)h->device_bytes;
+  info->launches_n = h->plan[0].launches();
+  info->launches_c = h->plan[1].launches();
+  info->rows_in = h->n;
+  info->rows_out = h->n;
+  return BF_OK;
+}
+
+int hodbf_workspace_size(hodbf_handle h, int64_t nrhs, size_t* bytes) {
+  if (!h || !bytes || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
+  *bytes = align256((size_t)h->slab_rows * (size_t)nrhs * csize(h->dtype));
+  return BF_OK;
+}
+
+int hodbf_rounds(hodbf_handle h, int op, int32_t* n) {
+  if (!h || !n) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  *n = (int32_t)h->plan[op == BF_OP_N ? 0 : 1].rounds.size();
+  return BF_OK;
+}
+
+int hodbf_round_info(hodbf_handle h, int op, int32_t round, bf_round_info_t* info) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    round_info(h->dtype, h->plan[op == BF_OP_N ? 0 : 1], round, info);
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+int hodbf_apply(hodbf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                void* work, size_t work_bytes, bf_stream_t stream) {
+  return hodbf_apply_events(h, op, nrhs, X, ldx, Y, ldy, work, work_bytes, stream, nullptr, 0);
+}
+
+int hodbf_apply_events(hodbf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                       void* work, size_t work_bytes, bf_stream_t stream, void* const* events, int32_t nevents) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    require(op == BF_OP_N || op == BF_OP_C || op == BF_OP_T, BF_ERR_ARG, "bad op");
+    size_t need = 0;
+    hodbf_workspace_size(h, nrhs, &need);
+    validate_apply(nrhs, X, ldx, h->n, Y, ldy, h->n, work_bytes, need);
+    if (nrhs == 0 || h->n == 0) return BF_OK;
+    require(nrhs <= (int64_t)65535 * 32, BF_ERR_ARG, "nrhs too large for one launch");
+    DeviceGuard dg(h->device);
+    StageArgs a{};
+    a.pool = h->pool;
+    a.X = X;
+    a.ldx = ldx;
+    a.xperm = h->d_perm;
+    a.S = work;
+    a.ldS = nrhs;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.yperm = h->d_perm;
+    a.conj_flip = op == BF_OP_T ? 1 : 0;
+    a.nrhs = (int32_t)nrhs;
+    run_plan(h->dtype, h->plan[op == BF_OP_N ? 0 : 1], a, static_cast<cudaStream_t>(stream), events, nevents);
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+int hodbf_workspace_size_host(hodbf_handle h, int64_t nrhs, size_t* bytes) {
+  if (!h || !bytes || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
+  size_t s = 0;
+  hodbf_workspace_size(h, nrhs, &s);
+  *bytes = s + 2 * align256((size_t)h->n * nrhs * csize(h->dtype));
+  return BF_OK;
+}
+
+int hodbf_apply_host(hodbf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx, void* Yh, int64_t ldy,
+                     void* work, size_t work_bytes, bf_stream_t stream) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    size_t need = 0, s = 0;
+    hodbf_workspace_size_host(h, nrhs, &need);
+    hodbf_workspace_size(h, nrhs, &s);
+    validate_apply(nrhs, Xh, ldx, h->n, Yh, ldy, h->n, work_bytes, need);
+    if (nrhs == 0 || h->n == 0) return BF_OK;
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t cs = csize(h->dtype);
+    char* dX = static_cast<char*>(work) + s;
+    char* dY = dX + align256((size_t)h->n * nrhs * cs);
+    BF_CK(cudaMemcpy2DAsync(dX, h->n * cs, Xh, ldx * cs, h->n * cs, nrhs, cudaMemcpyHostToDevice, st));
+    int rc = hodbf_apply(h, op, nrhs, dX, h->n, dY, h->n, work, s, stream);
+    if (rc != BF_OK) return rc;
+    BF_CK(cudaMemcpy2DAsync(Yh, ldy * cs, dY, h->n * cs, h->n * cs, nrhs, cudaMemcpyDeviceToHost, st));
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+}  // extern "C"
+
+// ======================================================================================
+// distributed butterfly: column subtrees -> all-to-all -> row subtrees
+// ======================================================================================
+namespace bfa {
+
+// Copy the blocks a rank touches into a compact local pool; remap the block offsets of a
+// private Geom copy (untouched blocks keep offset -1).
+static void local_pool(const bf_desc& d, Geom& G, const Own& own, std::vector<char>& host, FBase& F,
+                       size_t cs) {
+  const int L = G.L, lc = G.lc;
+  auto take = [&](const void* src, int64_t off, int64_t len) {
+    const int64_t at = (int64_t)(host.size() / cs);
+    host.resize(host.size() + (size_t)len * cs);
+    memcpy(host.data() + (size_t)at * cs, static_cast<const char*>(src) + (size_t)off * cs, (size_t)len * cs);
+    return at;
+  };
+  F = FBase{};
+  for (int64_t tau = 0; tau < G.nb; ++tau)
+    G.u_off[tau] = own.row(L, tau) ? take(d.U, G.u_off[tau], G.mt(tau) * G.r(L, tau)) : -1;
+  for (int l = lc; l < L; ++l)
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        const int64_t i = G.idx(l, tau, nu);
+        G.r_off[l][i] = own.row(l, tau) ? take(d.R, G.r_off[l][i], int64_t(G.R_rows(l, tau, nu)) * G.r(l, i)) : -1;
+      }
+  for (int64_t i = 0; i < G.nb; ++i) {
+    const int64_t tau = i >> (L - lc), nu = i & ((int64_t(1) << (L - lc)) - 1);
+    G.b_off[i] = (own.row(lc, tau) || own.col(G, lc, nu)) ? take(d.B, G.b_off[i], int64_t(G.r(lc, i)) * G.c(lc, i)) : -1;
+  }
+  for (int l = 1; l <= lc; ++l)
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        const int64_t i = G.idx(l, tau, nu);
+        G.w_off[l][i] = own.col(G, l, nu) ? take(d.W, G.w_off[l][i], int64_t(G.c(l, i)) * G.W_cols(l, tau, nu)) : -1;
+      }
+  for (int64_t nu = 0; nu < G.nb; ++nu)
+    G.vt_off[nu] = own.col(G, 0, nu) ? take(d.Vt, G.vt_off[nu], int64_t(G.c(0, nu)) * G.nv(nu)) : -1;
+}
+
+// contiguous user range of tree positions [a, b) under perm (NULL = identity)
+static int64_t user_range(const int64_t* perm, int64_t a, int64_t b, std::vector<int64_t>& lperm) {
+  lperm.resize((size_t)(b - a));
+  if (!perm) {
+    for (int64_t q = 0; q < b - a; ++q) lperm[q] = q;
+    return a;
+  }
+  int64_t lo = INT64_MAX, hi = -1;
+  for (int64_t q = a; q < b; ++q) {
+    lo = std::min(lo, perm[q]);
+    hi = std::max(hi, perm[q]);
+  }
+  require(b == a || hi - lo + 1 == b - a, BF_ERR_PERM, "a rank's subtree does not map to a contiguous user range");
+  for (int64_t q = a; q < b; ++q) lperm[q - a] = perm[q] - lo;
+  return b == a ? 0 : lo;
+}
+
+}  // namespace bfa
+
+extern "C" {
+
+int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle* out) {
+  if (!d || !out) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  *out = nullptr;
+  try {
+    require(nranks >= 1 && (nranks & (nranks - 1)) == 0, BF_ERR_NCCL, "nranks must be a power of two");
+    require(rank >= 0 && rank < nranks, BF_ERR_ARG, "rank out of range");
+    Geom G = make_geom(*d);
+    int p = 0;
+    while ((1 << p) < nranks) ++p;
+    require(p <= G.lc && p <= G.L - G.lc, BF_ERR_NCCL, "need log2(nranks) <= min(lc, L - lc)");
+    check_perm(d->row_perm, d->m, "row_perm");
+    check_perm(d->col_perm, d->n, "col_perm");
+    check_device(device);
+    DeviceGuard dg(device);
+    std::unique_ptr<bf_s> h(new bf_s());
+    h->dtype = d->dtype;
+    h->device = device;
+    h->dist = true;
+    h->rank = rank;
+    h->nranks = nranks;
+    const size_t cs = csize(d->dtype);
+    Own own;
+    own.p = p;
+    own.g = rank;
+    std::vector<char> host;
+    FBase F;
+    local_pool(*d, G, own, host, F, cs);
+    h->factor_entries = (int64_t)(host.size() / cs);
+    if (!host.empty()) h->pool = upload(host.data(), host.size(), &h->device_bytes);
+    const int L = G.L, lc = G.lc;
+    const int64_t P = nranks, g = rank;
+    // local row ranges (tree positions) and local perms
+    const int64_t cs0 = G.clp[g << (L - p)], cs1 = G.clp[(g + 1) << (L - p)];
+    const int64_t rs0 = G.rlp[g << (L - p)], rs1 = G.rlp[(g + 1) << (L - p)];
+    std::vector<int64_t> lpc, lpr;
+    const int64_t uc = user_range(d->col_perm, cs0, cs1, lpc);
+    const int64_t ur = user_range(d->row_perm, rs0, rs1, lpr);
+    int64_t* dpc = lpc.empty() ? nullptr : (int64_t*)upload(lpc.data(), lpc.size() * 8, &h->device_bytes);
+    int64_t* dpr = lpr.empty() ? nullptr : (int64_t*)upload(lpr.data(), lpr.size() * 8, &h->device_bytes);
+    // op N: in = column subtree, out = row subtree; op C the reverse.  One perm copy each.
+    h->d_lperm_in[0] = dpc;
+    h->d_lperm_out[0] = dpr;
+    h->loc_rows_in[0] = cs1 - cs0;
+    h->loc_rows_out[0] = rs1 - rs0;
+    h->loc_user_in[0] = uc;
+    h->loc_user_out[0] = ur;
+    h->loc_rows_in[1] = rs1 - rs0;
+    h->loc_rows_out[1] = cs1 - cs0;
+    h->loc_user_in[1] = ur;
+    h->loc_user_out[1] = uc;
+    int64_t max_rows = 0;
+    for (int op = 0; op < 2; ++op) {
+      Slabs S;
+      S.col.assign((size_t)(lc + 1) * G.nb, -1);
+      S.row.assign((size_t)(L - lc + 1) * G.nb, -1);
+      S.xspace = op == 0 ? 1 : 2;
+      S.xout.assign(G.nb, -1);
+      S.xin.assign(G.nb, -1);
+      int64_t cur = 0;
+      for (int l = 0; l <= lc; ++l) {
+        if (op == 1 && l == lc) break;
+        for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+          for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu)
+            if (own.col(G, l, nu)) {
+              const int64_t i = G.idx(l, tau, nu);
+              S.col[(size_t)l * G.nb + i] = cur;
+              cur += G.c(l, i);
+            }
+      }
+      for (int l = lc; l <= L; ++l) {
+        if (op == 0 && l == lc) continue;
+        for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+          if (own.row(l, tau))
+            for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+              const int64_t i = G.idx(l, tau, nu);
+              S.row[(size_t)(l - lc) * G.nb + i] = cur;
+              cur += G.r(l, i);
+            }
+      }
+      // exchange regions at the centre level: sender groups by destination, receiver by source
+      const int64_t wt = int64_t(1) << (lc - p), wn = int64_t(1) << (L - lc - p);
+      auto sz = [&](int64_t i) { return op == 0 ? G.r(lc, i) : G.c(lc, i); };
+      h->send_base[op] = cur;
+      h->send_cnt[op].assign(P, 0);
+      h->recv_cnt[op].assign(P, 0);
+      for (int64_t q = 0; q < P; ++q) {
+        // op N: sender owns nu (col subtree g), destination q owns tau
+        // op C: sender owns tau (row subtree g), destination q owns nu
+        const int64_t t0 = (op == 0 ? q : g) * wt, n0 = (op == 0 ? g : q) * wn;
+        for (int64_t tau = t0; tau < t0 + wt; ++tau)
+          for (int64_t nu = n0; nu < n0 + wn; ++nu) {
+            const int64_t i = G.idx(lc, tau, nu);
+            S.xout[i] = cur;
+            cur += sz(i);
+            h->send_cnt[op][q] += sz(i);
+          }
+      }
+      h->send_rows[op] = cur - h->send_base[op];
+      h->recv_base[op] = cur;
+      for (int64_t q = 0; q < P; ++q) {
+        const int64_t t0 = (op == 0 ? g : q) * wt, n0 = (op == 0 ? q : g) * wn;
+        for (int64_t tau = t0; tau < t0 + wt; ++tau)
+          for (int64_t nu = n0; nu < n0 + wn; ++nu) {
+            const int64_t i = G.idx(lc, tau, nu);
+            S.xin[i] = cur;
+            cur += sz(i);
+            h->recv_cnt[op][q] += sz(i);
+          }
+      }
+      h->recv_rows[op] = cur - h->recv_base[op];
+      max_rows = std::max(max_rows, cur);
+      PlanBuilder pb;
+      EmitOpts o;
+      o.own = own;
+      if (op == 0) {
+        o.x_base = cs0;
+        o.y_base = rs0;
+        emit_N(pb, G, F, S, o);
+        upload_plan(h->pre[0], pb, 0, lc + 2, &h->device_bytes);
+        upload_plan(h->post[0], pb, lc + 2, L + 3, &h->device_bytes);
+      } else {
+        o.x_base = rs0;
+        o.y_base = cs0;
+        emit_C(pb, G, F, S, o);
+        upload_plan(h->pre[1], pb, 0, L - lc + 2, &h->device_bytes);
+        upload_plan(h->post[1], pb, L - lc + 2, L + 3, &h->device_bytes);
+      }
+    }
+    h->slab_rows = max_rows;
+    h->G = std::move(G);
+    *out = h.release();
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    return fail(Err{BF_ERR_OOM, "host allocation failed"});
+  }
+}
+
+int bf_dist_layout(bf_handle h, int op, int64_t nrhs, size_t* work_bytes, size_t* send_off, size_t* recv_off,
+                   int64_t* send_counts, int64_t* recv_counts) {
+  if (!h || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
+  if (!h->dist) return fail(Err{BF_ERR_ARG, "not a distributed handle"});
+  const int k = op == BF_OP_N ? 0 : 1;
+  const size_t row_bytes = (size_t)nrhs * csize(h->dtype);
+  if (work_bytes) *work_bytes = align256((size_t)h->slab_rows * row_bytes);
+  if (send_off) *send_off = (size_t)h->send_base[k] * row_bytes;
+  if (recv_off) *recv_off = (size_t)h->recv_base[k] * row_bytes;
+  for (int q = 0; q < h->nranks; ++q) {
+    if (send_counts) send_counts[q] = h->send_cnt[k][q] * nrhs;
+    if (recv_counts) recv_counts[q] = h->recv_cnt[k][q] * nrhs;
+  }
+  return BF_OK;
+}
+
+int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out, int64_t* user_off_in,
+                       int64_t* user_off_out) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  if (!h->dist) return fail(Err{BF_ERR_ARG, "not a distributed handle"});
+  const int k = op == BF_OP_N ? 0 : 1;
+  if (rows_in) *rows_in = h->loc_rows_in[k];
+  if (rows_out) *rows_out = h->loc_rows_out[k];
+  if (user_off_in) *user_off_in = h->loc_user_in[k];
+  if (user_off_out) *user_off_out = h->loc_user_out[k];
+  return BF_OK;
+}
+
+static int dist_run(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                    void* work, size_t work_bytes, bf_stream_t stream, bool pre) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    require(h->dist, BF_ERR_ARG, "not a distributed handle");
+    require(op == BF_OP_N || op == BF_OP_C || op == BF_OP_T, BF_ERR_ARG, "bad op");
+    require(nrhs >= 0 && nrhs <= (int64_t)65535 * 32, BF_ERR_ARG, "bad nrhs");
+    const int k = op == BF_OP_N ? 0 : 1;
+    size_t need = 0;
+    bf_dist_layout(h, op, nrhs, &need, nullptr, nullptr, nullptr, nullptr);
+    require(work_bytes >= need && (need == 0 || work), BF_ERR_ARG, "workspace too small");
+    if (nrhs == 0) return BF_OK;
+    if (pre)
+      require(X && ldx >= std::max<int64_t>(h->loc_rows_in[k], 1), BF_ERR_ARG, "bad X_loc / ldx");
+    else
+      require(Y && ldy >= std::max<int64_t>(h->loc_rows_out[k], 1), BF_ERR_ARG, "bad Y_loc / ldy");
+    DeviceGuard dg(h->device);
+    StageArgs a{};
+    a.pool = h->pool;
+    a.X = X;
+    a.ldx = ldx;
+    a.xperm = h->d_lperm_in[k];
+    a.S = work;
+    a.ldS = nrhs;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.yperm = h->d_lperm_out[k];
+    a.conj_flip = op == BF_OP_T ? 1 : 0;
+    a.nrhs = (int32_t)nrhs;
+    run_plan(h->dtype, pre ? h->pre[k] : h->post[k], a, static_cast<cudaStream_t>(stream));
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+int bf_dist_apply_pre(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx, void* work,
+                      size_t work_bytes, bf_stream_t stream) {
+  return dist_run(h, op, nrhs, X_loc, ldx, nullptr, 0, work, work_bytes, stream, true);
+}
+
+int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy, void* work, size_t work_bytes,
+                       bf_stream_t stream) {
+  return dist_run(h, op, nrhs, nullptr, 0, Y_loc, ldy, work, work_bytes, stream, false);
+}
+
+}  // extern "C"

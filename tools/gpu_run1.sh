@@ -1,0 +1,12 @@
+#!/bin/bash
+# first GPU call: peaks, parity tests, bench, launch list
+set -x
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+nvidia-smi > gpurun_out/nvsmi.txt 2>&1
+timeout 120 ./tools/peaks > gpurun_out/peaks.json 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q -k "not cfg3" > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo "bench exit $?" >> gpurun_out/bench.err
+timeout 600 python bench.py --steps 10 --warmup 3 --dtype c64 --no-cpu-baseline > gpurun_out/bench_c64.json 2> gpurun_out/bench_c64.err
