@@ -14,6 +14,7 @@
 // owns rank x nrhs entries (nrhs fastest), so no stage ever overwrites another stage's
 // data and no atomics are needed (each output slab is written by exactly one task).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -21,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fast.cuh"
 
 namespace bfa {
 
@@ -363,6 +365,204 @@ static void emit_C(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
 }
 
 // --------------------------------------------------------------------------------------
+// fused window-pass plan (fast.cuh) for uniform rank-16 butterflies
+// --------------------------------------------------------------------------------------
+struct FastPlan {
+  std::vector<FastPass> passes;
+  void* F = nullptr;
+  int64_t entries = 0;
+};
+
+static bool fast_eligible(const Geom& G) {
+  if (G.L < 1) return false;
+  for (int32_t v : G.rr)
+    if (v != FAST_RANK) return false;
+  for (int32_t v : G.rc)
+    if (v != FAST_RANK) return false;
+  const int64_t lr = G.mt(0), lcn = G.nv(0);
+  if (lr <= 0 || lcn <= 0 || lr % 16 || lcn % 16) return false;
+  for (int64_t i = 0; i < G.nb; ++i)
+    if (G.mt(i) != lr || G.nv(i) != lcn) return false;
+  return true;
+}
+
+template <typename CT>
+struct HostFactors {
+  const CT *U, *R, *B, *W, *Vt;
+};
+
+template <typename CT>
+static inline CT cj(CT v, bool c) {
+  if (c) v.y = -v.y;
+  return v;
+}
+
+// write an M x K operand in MMA fragment order [mg][ki][mi][lane] (lane = 4g + t <-> row 16mg+8mi+g, col 4ki+t)
+template <typename CT, typename Fn>
+static void fill_frag(CT* dst, int M, int K, Fn A) {
+  const int nk = K / 4;
+  for (int mg = 0; mg < M / 16; ++mg)
+    for (int ki = 0; ki < nk; ++ki)
+      for (int mi = 0; mi < 2; ++mi)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int g = lane >> 2, t = lane & 3;
+          dst[((mg * nk + ki) * 2 + mi) * 32 + lane] = A(16 * mg + 8 * mi + g, 4 * ki + t);
+        }
+}
+
+// op 0 = N (forward), 1 = C (adjoint; conjugate-transposed factor views)
+template <typename CT>
+static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, int opk, size_t* acct) {
+  const int L = G.L, lc = G.lc;
+  const int np = (L + FAST_DMAX - 1) / FAST_DMAX;
+  std::vector<int> lv(np + 1, 0);
+  for (int p = 0; p < np; ++p) lv[p + 1] = lv[p] + L / np + (p < L % np ? 1 : 0);
+  const int lr = (int)G.mt(0), lcn = (int)G.nv(0);
+  const bool adj = opk == 1;
+  std::vector<FastPass> passes;
+  int64_t total = 0;
+  for (int k = 0; k < np; ++k) {
+    const int p = adj ? np - 1 - k : k;
+    FastPass P{};
+    P.L = L;
+    P.l0 = lv[p];
+    P.d = lv[p + 1] - lv[p];
+    const int l0 = P.l0, l1 = lv[p + 1], d = P.d;
+    P.bbits = L - l1;
+    P.nwin = int64_t(1) << (L - d);
+    const bool hasB = (l0 <= lc && lc < l1) || (lc == L && p == np - 1);
+    std::vector<FastOp> ops;
+    auto add = [&](int kind, int s, int leaf) {
+      FastOp o{};
+      o.kind = kind;
+      o.s = s;
+      o.leaf = leaf;
+      ops.push_back(o);
+    };
+    if (!adj) {
+      if (p == 0) add(FK_LEAF_IN, 0, lcn);
+      for (int l = l0 + 1; l <= l1 && l <= lc; ++l) add(FK_PAIR_DOWN, l - 1 - l0, 0);  // W_l
+      if (hasB) add(FK_DIAG, lc - l0, 0);
+      for (int l = std::max(l0, lc); l < l1; ++l) add(FK_PAIR_DOWN, l - l0, 0);      // R_l
+      if (p == np - 1) add(FK_LEAF_OUT, d, lr);
+      P.in_s = p == 0 ? -1 : 0;
+      P.out_s = p == np - 1 ? -1 : d;
+    } else {
+      if (p == np - 1) add(FK_LEAF_IN, d, lr);                                       // U^H
+      for (int l = l1 - 1; l >= l0 && l >= lc; --l) add(FK_PAIR_UP, l - l0, 0);        // R^H_l
+      if (hasB) add(FK_DIAG, lc - l0, 0);                                              // B^H
+      for (int l = std::min(l1, lc); l >= l0 + 1; --l) add(FK_PAIR_UP, l - 1 - l0, 0); // W^H_l
+      if (p == 0) add(FK_LEAF_OUT, 0, lcn);                                            // Vt^H
+      P.in_s = p == np - 1 ? -1 : d;
+      P.out_s = p == 0 ? -1 : 0;
+    }
+    require((int)ops.size() <= FAST_MAXOPS, BF_ERR_ARG, "internal: too many ops in a pass");
+    P.nops = (int)ops.size();
+    int64_t off = 0;
+    const int nslot = 1 << d;
+    for (int q = 0; q < P.nops; ++q) {
+      ops[q].off = off;
+      off += nslot * fast_slot_size(ops[q]);
+      P.ops[q] = ops[q];
+    }
+    P.win_size = off;
+    P.fbase = total;
+    P.factor_entries = off * P.nwin;
+    total += off * P.nwin;
+    for (int q = 0; q < P.nops; ++q) {
+      if (ops[q].kind == FK_LEAF_IN) P.user_in = (adj ? G.m : G.n);
+      if (ops[q].kind == FK_LEAF_OUT) P.user_out = (adj ? G.n : G.m);
+    }
+    passes.push_back(P);
+  }
+  std::vector<CT> host((size_t)total);
+  for (const FastPass& P : passes) {
+    const int d = P.d, nslot = 1 << d;
+    for (int64_t w = 0; w < P.nwin; ++w) {
+      const int64_t a = w >> P.bbits, b = w & ((int64_t(1) << P.bbits) - 1);
+      for (int q = 0; q < P.nops; ++q) {
+        const FastOp& op = P.ops[q];
+        for (int o = 0; o < nslot; ++o) {
+          CT* dst = host.data() + P.fbase + w * P.win_size + op.off + o * fast_slot_size(op);
+          // block (tau, nu) of slot o at window level s
+          auto blk = [&](int s, int64_t& tau, int64_t& nu) {
+            const int ds = d - s;
+            tau = (a << s) + (o >> ds);
+            nu = (b << ds) + (o & ((1 << ds) - 1));
+          };
+          int64_t tau, nu;
+          if (op.kind == FK_LEAF_IN) {
+            blk(op.s, tau, nu);
+            if (!adj) {
+              const CT* V = H.Vt + G.vt_off[nu];
+              fill_frag(dst, 16, lcn, [&](int i, int k) { return V[i + k * 16]; });
+            } else {
+              const CT* U = H.U + G.u_off[tau];
+              fill_frag(dst, 16, lr, [&](int i, int k) { return cj(U[k + (int64_t)i * lr], true); });
+            }
+          } else if (op.kind == FK_LEAF_OUT) {
+            blk(op.s, tau, nu);
+            if (!adj) {
+              const CT* U = H.U + G.u_off[tau];
+              fill_frag(dst, lr, 16, [&](int i, int k) { return U[i + (int64_t)k * lr]; });
+            } else {
+              const CT* V = H.Vt + G.vt_off[nu];
+              fill_frag(dst, lcn, 16, [&](int i, int k) { return cj(V[k + i * 16], true); });
+            }
+          } else if (op.kind == FK_DIAG) {
+            blk(op.s, tau, nu);
+            const CT* Bb = H.B + G.b_off[G.idx(lc, tau, nu)];
+            fill_frag(dst, 16, 16, [&](int i, int k) { return adj ? cj(Bb[k + i * 16], true) : Bb[i + k * 16]; });
+          } else if (op.kind == FK_PAIR_DOWN) {
+            blk(op.s + 1, tau, nu);  // output block at level l0 + s + 1
+            const int l = P.l0 + op.s + 1;
+            if (l <= lc) {  // W_l
+              const CT* Wb = H.W + G.w_off[l][G.idx(l, tau, nu)];
+              fill_frag(dst, 16, 32, [&](int i, int k) { return Wb[i + k * 16]; });
+            } else {  // R_{l-1}, gather form
+              const int lr_ = l - 1;
+              const int part = (int)(tau & 1);
+              const CT* R0 = H.R + G.r_off[lr_][G.idx(lr_, tau >> 1, 2 * nu)];
+              const CT* R1 = H.R + G.r_off[lr_][G.idx(lr_, tau >> 1, 2 * nu + 1)];
+              fill_frag(dst, 16, 32, [&](int i, int k) {
+                const CT* Rs = k < 16 ? R0 : R1;
+                return Rs[(part * 16 + i) + (k & 15) * 32];
+              });
+            }
+          } else {  // FK_PAIR_UP: output block at level l = l0 + s
+            blk(op.s, tau, nu);
+            const int l = P.l0 + op.s;
+            if (l >= lc) {  // R^H_l: inputs (2tau + p, nu >> 1)
+              const CT* Rb = H.R + G.r_off[l][G.idx(l, tau, nu)];
+              fill_frag(dst, 16, 32, [&](int i, int k) {
+                const int pp = k >> 4;
+                return cj(Rb[(pp * 16 + (k & 15)) + i * 32], true);
+              });
+            } else {  // W^H_{l+1}: inputs (2tau + p, nu >> 1) at level l + 1, column part nu & 1
+              const int lw = l + 1;
+              const CT* W0 = H.W + G.w_off[lw][G.idx(lw, 2 * tau, nu >> 1)];
+              const CT* W1 = H.W + G.w_off[lw][G.idx(lw, 2 * tau + 1, nu >> 1)];
+              const int cp = (int)(nu & 1);
+              fill_frag(dst, 16, 32, [&](int i, int k) {
+                const CT* Ws = k < 16 ? W0 : W1;
+                return cj(Ws[(k & 15) + (cp * 16 + i) * 16], true);
+              });
+            }
+          }
+        }
+      }
+    }
+  }
+  FP.passes = std::move(passes);
+  FP.entries = total;
+  if (total) {
+    BF_CK(cudaMalloc(&FP.F, (size_t)total * sizeof(CT)));
+    BF_CK(cudaMemcpy(FP.F, host.data(), (size_t)total * sizeof(CT), cudaMemcpyHostToDevice));
+    *acct += (size_t)total * sizeof(CT);
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // device plan
 // --------------------------------------------------------------------------------------
 struct Plan {
@@ -475,6 +675,8 @@ struct bf_s {
   int64_t factor_entries = 0;
   size_t device_bytes = 0;
   Plan plan[2];  // [0] op N, [1] op C/T
+  bool use_fast = false;
+  FastPlan fast[2];
   // distributed
   bool dist = false;
   int rank = 0, nranks = 1;
@@ -495,6 +697,8 @@ struct bf_s {
       if (d_lperm_in[k]) cudaFree(d_lperm_in[k]);
       if (d_lperm_out[k]) cudaFree(d_lperm_out[k]);
     }
+    for (int k = 0; k < 2; ++k)
+      if (fast[k].F) cudaFree(fast[k].F);
     if (pool) cudaFree(pool);
     if (d_rperm) cudaFree(d_rperm);
     if (d_cperm) cudaFree(d_cperm);
@@ -649,6 +853,13 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
         emit_C(pb, G, F, S, o);
       upload_plan(h->plan[k], pb, 0, (int)pb.tasks.size(), &h->device_bytes);
     }
+    if (fast_eligible(G) && d->dtype == BF_C128 && !getenv("BF_DISABLE_FAST")) {
+      HostFactors<double2> HF{static_cast<const double2*>(d->U), static_cast<const double2*>(d->R),
+                              static_cast<const double2*>(d->B), static_cast<const double2*>(d->W),
+                              static_cast<const double2*>(d->Vt)};
+      for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
+      h->use_fast = true;
+    }
     h->G = std::move(G);
     *out = h.release();
     return BF_OK;
@@ -671,6 +882,9 @@ int bf_info(bf_handle h, bf_info_t* info) {
   if (h->dist) {
     info->launches_n = h->pre[0].launches() + h->post[0].launches();
     info->launches_c = h->pre[1].launches() + h->post[1].launches();
+  } else if (h->use_fast) {
+    info->launches_n = (int32_t)h->fast[0].passes.size();
+    info->launches_c = (int32_t)h->fast[1].passes.size();
   } else {
     info->launches_n = h->plan[0].launches();
     info->launches_c = h->plan[1].launches();
@@ -680,10 +894,48 @@ int bf_info(bf_handle h, bf_info_t* info) {
   return BF_OK;
 }
 
+static size_t fast_ws(bf_handle h, int64_t nrhs) {
+  if (!h->use_fast) return 0;
+  const size_t tiles = (size_t)((nrhs + FAST_NB - 1) / FAST_NB);
+  return 2 * align256((size_t)h->G.nb * tiles * FAST_SLAB * csize(h->dtype));
+}
+
 int bf_workspace_size(bf_handle h, int64_t nrhs, size_t* bytes) {
   if (!h || !bytes || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
-  *bytes = align256((size_t)h->slab_rows * (size_t)nrhs * csize(h->dtype));
+  if (h->use_fast && !h->dist)
+    *bytes = fast_ws(h, nrhs);
+  else
+    *bytes = align256((size_t)h->slab_rows * (size_t)nrhs * csize(h->dtype));
   return BF_OK;
+}
+
+static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                     void* work, cudaStream_t st, void* const* ev, int nev) {
+  const FastPlan& FP = h->fast[k];
+  if (ev) require(nev >= (int)FP.passes.size() + 1, BF_ERR_ARG, "need nrounds + 1 events");
+  const size_t half = fast_ws(h, nrhs) / 2;
+  char* buf[2] = {static_cast<char*>(work), static_cast<char*>(work) + half};
+  const bool fwd = k == 0;
+  for (size_t i = 0; i < FP.passes.size(); ++i) {
+    FastArgs a{};
+    a.p = FP.passes[i];
+    a.F = FP.F;
+    a.X = X;
+    a.ldx = ldx;
+    a.xperm = fwd ? h->d_cperm : h->d_rperm;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.yperm = fwd ? h->d_rperm : h->d_cperm;
+    a.Sin = buf[i % 2];
+    a.Sout = buf[(i + 1) % 2];
+    a.nlev = h->G.nb;
+    a.nrhs = (int32_t)nrhs;
+    a.conj_io = op == BF_OP_T ? 1 : 0;
+    if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), st));
+    launch_fast_pass(h->dtype, a, st);
+  }
+  if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[FP.passes.size()]), st));
+  BF_CK(cudaGetLastError());
 }
 
 int bf_apply_op_events(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
@@ -719,6 +971,10 @@ int bf_apply_op_events(bf_handle h, int op, int64_t nrhs, const void* X, int64_t
     a.conj_flip = (op == BF_OP_T) ? 1 : 0;
     a.nrhs = (int32_t)nrhs;
     require(nrhs <= (int64_t)65535 * 32, BF_ERR_ARG, "nrhs too large for one launch");
+    if (h->use_fast) {
+      run_fast(h, fwd ? 0 : 1, op, nrhs, X, ldx, Y, ldy, work, st, events, nevents);
+      return BF_OK;
+    }
     run_plan(h->dtype, h->plan[fwd ? 0 : 1], a, st, events, nevents);
     return BF_OK;
   } catch (const Err& e) {
@@ -734,7 +990,10 @@ int bf_apply_op(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, v
 int bf_rounds(bf_handle h, int op, int32_t* n) {
   if (!h || !n) return fail(Err{BF_ERR_ARG, "NULL argument"});
   const int k = op == BF_OP_N ? 0 : 1;
-  *n = h->dist ? (int32_t)(h->pre[k].rounds.size() + h->post[k].rounds.size()) : (int32_t)h->plan[k].rounds.size();
+  if (h->use_fast && !h->dist)
+    *n = (int32_t)h->fast[k].passes.size();
+  else
+    *n = h->dist ? (int32_t)(h->pre[k].rounds.size() + h->post[k].rounds.size()) : (int32_t)h->plan[k].rounds.size();
   return BF_OK;
 }
 
@@ -742,6 +1001,20 @@ int bf_round_info(bf_handle h, int op, int32_t round, bf_round_info_t* info) {
   if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
   try {
     const int k = op == BF_OP_N ? 0 : 1;
+    if (h->use_fast && !h->dist) {
+      require(info && round >= 0 && round < (int)h->fast[k].passes.size(), BF_ERR_ARG, "round out of range");
+      const FastPass& P = h->fast[k].passes[round];
+      memset(info, 0, sizeof(*info));
+      info->kernel = 10;
+      info->ntasks = (int32_t)P.nwin;
+      info->factor_entries = P.factor_entries;
+      info->user_rows_in = P.user_in;
+      info->user_rows_out = P.user_out;
+      info->slab_rows_in = P.in_s >= 0 ? h->G.nb * FAST_RANK : 0;
+      info->slab_rows_out = P.out_s >= 0 ? h->G.nb * FAST_RANK : 0;
+      strncpy(info->name, fast_kernel_name(h->dtype), sizeof(info->name) - 1);
+      return BF_OK;
+    }
     if (h->dist) {
       const int np = (int)h->pre[k].rounds.size();
       if (round < np)

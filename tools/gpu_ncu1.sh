@@ -1,0 +1,9 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+$CMD > gpurun_out/ncu_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_generic.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+$CMD > gpurun_out/ncu_plain2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_stage_generic -s 40 -c 2 -o gpurun_out/prof_generic $CMD > gpurun_out/ncu_full.log 2>&1
+echo done

@@ -1,0 +1,7 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_fast.py -x -q > gpurun_out/pytest_fast.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_fast.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_fast.json 2> gpurun_out/bench_fast.err
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --op C > gpurun_out/bench_fast_C.json 2>> gpurun_out/bench_fast.err
