@@ -20,8 +20,10 @@ constexpr int FAST_NB = 32;        // right-hand sides per CTA (slab columns)
 constexpr int FAST_DMAX = 3;       // window levels per pass
 constexpr int FAST_MAXOPS = 8;
 constexpr int FAST_SLAB = FAST_RANK * FAST_NB;  // complex entries per slab (512)
-constexpr int FAST_THREADS = 512;  // 16 warps: two per window slot (column halves)
-constexpr int FAST_OPBUF = (1 << FAST_DMAX) * 2 * FAST_RANK * FAST_RANK;  // complex entries of one op's ring buffer
+constexpr int FAST_NCONS = 8;                       // consumer warps (one per window slot; 17 warps would cap registers at 96)
+constexpr int FAST_THREADS = (FAST_NCONS + 1) * 32;  // + one producer warp
+constexpr int FAST_CHUNK = 16384;                    // bytes per factor-ring chunk
+constexpr int FAST_NBUF = 6;                         // factor-ring depth
 
 struct FastOp {
   int32_t kind;
@@ -58,6 +60,7 @@ struct FastArgs {
 };
 
 void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st);
+size_t fast_smem_bytes(int dtype);
 const char* fast_kernel_name(int dtype);
 
 // per-slot complex entries of an op's factor data

@@ -14,6 +14,7 @@
 // owns rank x nrhs entries (nrhs fastest), so no stage ever overwrites another stage's
 // data and no atomics are needed (each output slab is written by exactly one task).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -373,14 +374,17 @@ struct FastPlan {
   int64_t entries = 0;
 };
 
-static bool fast_eligible(const Geom& G) {
+static bool fast_eligible(const Geom& G, int dtype) {
   if (G.L < 1) return false;
+  // a leaf operand slot (16 x leaf complex) must fit one factor-ring chunk
+  const int64_t maxleaf = FAST_CHUNK / (FAST_RANK * (dtype == BF_C128 ? 16 : 8));
   for (int32_t v : G.rr)
     if (v != FAST_RANK) return false;
   for (int32_t v : G.rc)
     if (v != FAST_RANK) return false;
   const int64_t lr = G.mt(0), lcn = G.nv(0);
-  if (lr <= 0 || lcn <= 0 || lr % 16 || lcn % 16) return false;
+  if (lr <= 0 || lcn <= 0 || lr % 16 || lcn % 16 || lr > maxleaf || lcn > maxleaf) return false;
+  if ((lr & (lr - 1)) || (lcn & (lcn - 1))) return false;  // slot sizes must divide the chunk
   for (int64_t i = 0; i < G.nb; ++i)
     if (G.mt(i) != lr || G.nv(i) != lcn) return false;
   return true;
@@ -397,17 +401,34 @@ static inline CT cj(CT v, bool c) {
   return v;
 }
 
-// write an M x K operand in MMA fragment order [mg][ki][mi][lane] (lane = 4g + t <-> row 16mg+8mi+g, col 4ki+t)
+// write an M x K operand in the MMA fragment order the fast kernel consumes.
+// complex128 (mma m8n8k4): [mg][ki][mi][lane], lane = 4g + t <-> (row 16mg + 8mi + g, col 4ki + t)
+// complex64 (mma m16n8k8): [mg][ki][lane][e], e: (g, t), (g+8, t), (g, t+4), (g+8, t+4) of the
+//                          16 x 8 block at rows 16mg, cols 8ki
 template <typename CT, typename Fn>
 static void fill_frag(CT* dst, int M, int K, Fn A) {
-  const int nk = K / 4;
-  for (int mg = 0; mg < M / 16; ++mg)
-    for (int ki = 0; ki < nk; ++ki)
-      for (int mi = 0; mi < 2; ++mi)
+  if (sizeof(CT) == 16) {
+    const int nk = K / 4;
+    for (int mg = 0; mg < M / 16; ++mg)
+      for (int ki = 0; ki < nk; ++ki)
+        for (int mi = 0; mi < 2; ++mi)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int g = lane >> 2, t = lane & 3;
+            dst[((mg * nk + ki) * 2 + mi) * 32 + lane] = A(16 * mg + 8 * mi + g, 4 * ki + t);
+          }
+  } else {
+    const int nk = K / 8;
+    for (int mg = 0; mg < M / 16; ++mg)
+      for (int ki = 0; ki < nk; ++ki)
         for (int lane = 0; lane < 32; ++lane) {
           const int g = lane >> 2, t = lane & 3;
-          dst[((mg * nk + ki) * 2 + mi) * 32 + lane] = A(16 * mg + 8 * mi + g, 4 * ki + t);
+          CT* d = dst + ((mg * nk + ki) * 32 + lane) * 4;
+          d[0] = A(16 * mg + g, 8 * ki + t);
+          d[1] = A(16 * mg + g + 8, 8 * ki + t);
+          d[2] = A(16 * mg + g, 8 * ki + t + 4);
+          d[3] = A(16 * mg + g + 8, 8 * ki + t + 4);
         }
+  }
 }
 
 // op 0 = N (forward), 1 = C (adjoint; conjugate-transposed factor views)
@@ -853,11 +874,18 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
         emit_C(pb, G, F, S, o);
       upload_plan(h->plan[k], pb, 0, (int)pb.tasks.size(), &h->device_bytes);
     }
-    if (fast_eligible(G) && d->dtype == BF_C128 && !getenv("BF_DISABLE_FAST")) {
-      HostFactors<double2> HF{static_cast<const double2*>(d->U), static_cast<const double2*>(d->R),
-                              static_cast<const double2*>(d->B), static_cast<const double2*>(d->W),
-                              static_cast<const double2*>(d->Vt)};
-      for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
+    if (fast_eligible(G, d->dtype) && !getenv("BF_DISABLE_FAST")) {
+      if (d->dtype == BF_C128) {
+        HostFactors<double2> HF{static_cast<const double2*>(d->U), static_cast<const double2*>(d->R),
+                                static_cast<const double2*>(d->B), static_cast<const double2*>(d->W),
+                                static_cast<const double2*>(d->Vt)};
+        for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
+      } else {
+        HostFactors<float2> HF{static_cast<const float2*>(d->U), static_cast<const float2*>(d->R),
+                               static_cast<const float2*>(d->B), static_cast<const float2*>(d->W),
+                               static_cast<const float2*>(d->Vt)};
+        for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
+      }
       h->use_fast = true;
     }
     h->G = std::move(G);
@@ -933,6 +961,12 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
     a.conj_io = op == BF_OP_T ? 1 : 0;
     if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), st));
     launch_fast_pass(h->dtype, a, st);
+    if (getenv("BF_DEBUG_SYNC")) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      fprintf(stderr, "bfapply debug: pass %zu (d=%d l0=%d nops=%d nwin=%lld) -> %s\n", i, a.p.d, a.p.l0, a.p.nops,
+              (long long)a.p.nwin, cudaGetErrorString(e));
+      BF_CK(e);
+    }
   }
   if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[FP.passes.size()]), st));
   BF_CK(cudaGetLastError());
