@@ -22,6 +22,13 @@
 
 #include "fast.cuh"
 
+#ifndef BF_C128_3M
+#define BF_C128_3M 1
+#endif
+#ifndef BF_USE_RING
+#define BF_USE_RING 1
+#endif
+
 namespace bfa {
 
 // ---- mbarrier / bulk-copy (TMA 1-D) helpers --------------------------------------------
@@ -73,7 +80,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int ta
 // ring op has at most FAST_NBUF chunks, so a consumer never waits on a ring phase more than one
 // ahead of the barrier (an mbarrier parity wait aliases beyond that).  Leaf ops read their
 // operand directly with coalesced loads.
-__device__ __forceinline__ bool ring_op(int kind) { return kind != FK_LEAF_IN && kind != FK_LEAF_OUT; }
+__device__ __forceinline__ bool ring_op(int kind) { return BF_USE_RING && kind != FK_LEAF_IN && kind != FK_LEAF_OUT; }
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(FAST_NCONS * 32) : "memory"); }
 
@@ -135,6 +142,8 @@ struct PolC128 {
 #pragma unroll
           for (int ni = 0; ni < NT; ++ni) p[q][mi][ni][0] = p[q][mi][ni][1] = 0.0;
     }
+#if BF_C128_3M
+    // 3M: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)
     __device__ __forceinline__ void step(const AFrag& a, const BFrag (&b)[NT]) {
       double bs[NT];
 #pragma unroll
@@ -150,6 +159,23 @@ struct PolC128 {
         }
       }
     }
+#else
+    // 4M without in-loop FP64 adds: P1 = Ar Br, P2 = Ai Bi, P3 = Ar Bi + Ai Br.  On B200 the
+    // DADDs that 3M needs share the FP64 pipe with DMMA and stall its issue stream (ncu:
+    // math-pipe-throttle at the DADDs, DMMA pipe ~50% active), so 4 DMMAs per complex
+    // product run faster than 3 DMMAs + 2 dependent DADDs.
+    __device__ __forceinline__ void step(const AFrag& a, const BFrag (&b)[NT]) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) {
+          mma(p[0][mi][ni][0], p[0][mi][ni][1], a.v[mi].x, b[ni].v.x);
+          mma(p[1][mi][ni][0], p[1][mi][ni][1], a.v[mi].y, b[ni].v.y);
+          mma(p[2][mi][ni][0], p[2][mi][ni][1], a.v[mi].x, b[ni].v.y);
+          mma(p[2][mi][ni][0], p[2][mi][ni][1], a.v[mi].y, b[ni].v.x);
+        }
+    }
+#endif
     // visit every output element: f(row, col_in_warp_tile, value); rows 0..15, cols 0..8NT-1
     template <typename Fn>
     __device__ __forceinline__ void each(int g, int t, Fn f) const {
@@ -160,7 +186,11 @@ struct PolC128 {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double p1 = p[0][mi][ni][e], p2 = p[1][mi][ni][e], p3 = p[2][mi][ni][e];
+#if BF_C128_3M
             f(8 * mi + g, 8 * ni + 2 * t + e, make_double2(p1 - p2, p3 - p1 - p2));
+#else
+            f(8 * mi + g, 8 * ni + 2 * t + e, make_double2(p1 - p2, p3));
+#endif
           }
     }
   };
@@ -469,7 +499,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
               for (int ki = 0; ki < KPS; ++ki) {
                 typename Pol::AFrag af;
                 typename Pol::BFrag bf[NT];
-                Pol::load_a(af, Aslot + (sidx * KPS + ki) * Pol::A_KSTEP, lane);
+                if (inring)
+                  Pol::load_a(af, Aslot + (sidx * KPS + ki) * Pol::A_KSTEP, lane);
+                else
+                  Pol::load_a_g(af, Aslot + (sidx * KPS + ki) * Pol::A_KSTEP, lane);
 #pragma unroll
                 for (int ni = 0; ni < NT; ++ni) Pol::load_b(bf[ni], sl, ki * Pol::KS, 8 * NT * h + 8 * ni, g, t);
                 acc.step(af, bf);
