@@ -164,12 +164,21 @@ int hodbf_apply_host(hodbf_handle h, int op, int64_t nrhs, const void* X_host, i
  *   the caller exchanges send -> recv with an all-to-all (NCCL) using bf_dist_layout;
  *   bf_dist_apply_post reads the recv region and writes Y_loc.
  * `desc` is the FULL descriptor (every rank passes the same); only the rank's blocks are
- * uploaded.  nranks = 1 runs the same path with a self exchange. */
+ * uploaded.  nranks = 1 runs the same path with a self exchange.
+ * device < 0 builds a HOST-ONLY plan: layouts, local rows and the exchange block maps can be
+ * queried (multi-process CPU tests of the exchange logic), nothing is uploaded, and
+ * bf_dist_apply_pre / _post return BF_ERR_DEVICE. */
 int bf_dist_create(const bf_desc* desc, int rank, int nranks, int device, bf_handle* out);
 /* Workspace bytes, and the send/recv regions: byte offsets into work plus per-peer
  * ELEMENT counts (complex entries) -- arrays of length nranks.  Op selects N or C/T. */
 int bf_dist_layout(bf_handle h, int op, int64_t nrhs, size_t* work_bytes, size_t* send_off,
                    size_t* recv_off, int64_t* send_counts, int64_t* recv_counts);
+/* The centre blocks (canonical index tau * 2^(L-lc) + nu at level lc) in the
+ * order their slabs occupy the send and the recv region (grouped by peer, peers ascending).
+ * Each block occupies rank x nrhs elements (op N: r^lc, op C / T: c^lc).  Pass NULL arrays to
+ * query only the counts. */
+int bf_dist_exchange_blocks(bf_handle h, int op, int64_t* n_send, int64_t* send_blocks, int64_t* n_recv,
+                            int64_t* recv_blocks);
 int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out,
                        int64_t* user_off_in, int64_t* user_off_out);
 int bf_dist_apply_pre(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx,

@@ -28,6 +28,9 @@
 namespace bfa {
 
 thread_local std::string g_last_error;
+// Set while bf_dist_create builds a host-only plan (device < 0): layouts and exchange maps
+// are computed, nothing is uploaded, and every apply on the handle fails with BF_ERR_DEVICE.
+thread_local bool g_host_only = false;
 
 struct Err {
   int code;
@@ -49,6 +52,7 @@ static void require(bool ok, int code, const std::string& msg) {
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
+    if (dev < 0) return;  // host-only plan: no device is touched
     cudaGetDevice(&prev);
     if (prev != dev) BF_CK(cudaSetDevice(dev));
   }
@@ -609,13 +613,16 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
   }
   if (tot == 0) return;
   std::vector<char> host(tot);
+  if (g_host_only) tot = 0;
   for (int r = round_lo, q = 0; r < round_hi && r < (int)pb.tasks.size(); ++r, ++q) {
     if (!pb.tasks[r].empty()) memcpy(host.data() + toff[q], pb.tasks[r].data(), pb.tasks[r].size() * sizeof(Task));
     if (!pb.terms[r].empty()) memcpy(host.data() + xoff[q], pb.terms[r].data(), pb.terms[r].size() * sizeof(Term));
   }
-  BF_CK(cudaMalloc(&P.dev, tot));
-  BF_CK(cudaMemcpy(P.dev, host.data(), tot, cudaMemcpyHostToDevice));
-  *bytes += tot;
+  if (tot) {
+    BF_CK(cudaMalloc(&P.dev, tot));
+    BF_CK(cudaMemcpy(P.dev, host.data(), tot, cudaMemcpyHostToDevice));
+    *bytes += tot;
+  }
   for (int r = round_lo, q = 0; r < round_hi && r < (int)pb.tasks.size(); ++r, ++q) {
     Round R{};
     R.tasks = reinterpret_cast<const Task*>((char*)P.dev + toff[q]);
@@ -705,19 +712,22 @@ struct bf_s {
   int64_t send_rows[2] = {0, 0}, recv_rows[2] = {0, 0};
   int64_t send_base[2] = {0, 0}, recv_base[2] = {0, 0};  // slab rows
   std::vector<int64_t> send_cnt[2], recv_cnt[2];         // rows per peer
+  std::vector<int64_t> send_blk[2], recv_blk[2];         // centre blocks in exchange-region order
+  bool host_only = false;
   int64_t loc_rows_in[2] = {0, 0}, loc_rows_out[2] = {0, 0};
   int64_t loc_user_in[2] = {0, 0}, loc_user_out[2] = {0, 0};
   int64_t* d_lperm_in[2] = {nullptr, nullptr};
   int64_t* d_lperm_out[2] = {nullptr, nullptr};
   ~bf_s() {
+    if (host_only) return;
     cudaSetDevice(device);
     for (int k = 0; k < 2; ++k) {
       free_plan(plan[k]);
       free_plan(pre[k]);
       free_plan(post[k]);
-      if (d_lperm_in[k]) cudaFree(d_lperm_in[k]);
-      if (d_lperm_out[k]) cudaFree(d_lperm_out[k]);
     }
+    if (d_lperm_in[0]) cudaFree(d_lperm_in[0]);  // [1] aliases [0] with in / out swapped
+    if (d_lperm_out[0]) cudaFree(d_lperm_out[0]);
     for (int k = 0; k < 2; ++k)
       if (fast[k].F) cudaFree(fast[k].F);
     if (pool) cudaFree(pool);
@@ -764,7 +774,7 @@ static void check_device(int device) {
 }
 
 static void* upload(const void* h, size_t bytes, size_t* acct) {
-  if (bytes == 0) return nullptr;
+  if (bytes == 0 || g_host_only) return nullptr;
   void* d = nullptr;
   BF_CK(cudaMalloc(&d, bytes));
   BF_CK(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
@@ -1503,11 +1513,17 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
     require(p <= G.lc && p <= G.L - G.lc, BF_ERR_NCCL, "need log2(nranks) <= min(lc, L - lc)");
     check_perm(d->row_perm, d->m, "row_perm");
     check_perm(d->col_perm, d->n, "col_perm");
-    check_device(device);
-    DeviceGuard dg(device);
+    const bool host_only = device < 0;
+    struct HostOnly {
+      explicit HostOnly(bool on) { g_host_only = on; }
+      ~HostOnly() { g_host_only = false; }
+    } ho(host_only);
+    if (!host_only) check_device(device);
+    DeviceGuard dg(host_only ? -1 : device);
     std::unique_ptr<bf_s> h(new bf_s());
     h->dtype = d->dtype;
     h->device = device;
+    h->host_only = host_only;
     h->dist = true;
     h->rank = rank;
     h->nranks = nranks;
@@ -1531,8 +1547,10 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
     int64_t* dpc = lpc.empty() ? nullptr : (int64_t*)upload(lpc.data(), lpc.size() * 8, &h->device_bytes);
     int64_t* dpr = lpr.empty() ? nullptr : (int64_t*)upload(lpr.data(), lpr.size() * 8, &h->device_bytes);
     // op N: in = column subtree, out = row subtree; op C the reverse.  One perm copy each.
-    h->d_lperm_in[0] = dpc;
+    h->d_lperm_in[0] = dpc;   // owned; the op-C entries alias them
     h->d_lperm_out[0] = dpr;
+    h->d_lperm_in[1] = dpr;
+    h->d_lperm_out[1] = dpc;
     h->loc_rows_in[0] = cs1 - cs0;
     h->loc_rows_out[0] = rs1 - rs0;
     h->loc_user_in[0] = uc;
@@ -1586,6 +1604,7 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
             S.xout[i] = cur;
             cur += sz(i);
             h->send_cnt[op][q] += sz(i);
+            h->send_blk[op].push_back(i);
           }
       }
       h->send_rows[op] = cur - h->send_base[op];
@@ -1598,6 +1617,7 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
             S.xin[i] = cur;
             cur += sz(i);
             h->recv_cnt[op][q] += sz(i);
+            h->recv_blk[op].push_back(i);
           }
       }
       h->recv_rows[op] = cur - h->recv_base[op];
@@ -1646,6 +1666,18 @@ int bf_dist_layout(bf_handle h, int op, int64_t nrhs, size_t* work_bytes, size_t
   return BF_OK;
 }
 
+int bf_dist_exchange_blocks(bf_handle h, int op, int64_t* n_send, int64_t* send_blocks, int64_t* n_recv,
+                            int64_t* recv_blocks) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  if (!h->dist) return fail(Err{BF_ERR_ARG, "not a distributed handle"});
+  const int k = op == BF_OP_N ? 0 : 1;
+  if (n_send) *n_send = (int64_t)h->send_blk[k].size();
+  if (n_recv) *n_recv = (int64_t)h->recv_blk[k].size();
+  if (send_blocks) std::copy(h->send_blk[k].begin(), h->send_blk[k].end(), send_blocks);
+  if (recv_blocks) std::copy(h->recv_blk[k].begin(), h->recv_blk[k].end(), recv_blocks);
+  return BF_OK;
+}
+
 int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out, int64_t* user_off_in,
                        int64_t* user_off_out) {
   if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
@@ -1663,6 +1695,7 @@ static int dist_run(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ld
   if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
   try {
     require(h->dist, BF_ERR_ARG, "not a distributed handle");
+    require(!h->host_only, BF_ERR_DEVICE, "host-only plan (created with device < 0) cannot apply");
     require(op == BF_OP_N || op == BF_OP_C || op == BF_OP_T, BF_ERR_ARG, "bad op");
     require(nrhs >= 0 && nrhs <= (int64_t)65535 * 32, BF_ERR_ARG, "bad nrhs");
     const int k = op == BF_OP_N ? 0 : 1;

@@ -1,0 +1,192 @@
+"""Distributed butterfly apply: one process per GPU (BASELINE north_star).
+
+P = 2^p ranks.  Rank g owns the column subtree nu_g at level p of T_S (its V leaves, W
+stages and the centre products B for nu under nu_g) and the row subtree tau_g at level p of
+T_O (its R stages and U leaves).  One apply is
+
+    bf_dist_apply_pre   (libbfapply kernels: leaf V, W stages, centre B -> send region)
+    all-to-all          (NCCL over NVLink / NVSwitch: centre slabs nu-owner -> tau-owner)
+    bf_dist_apply_post  (libbfapply kernels: R stages, leaf U -> Y_loc)
+
+for op N; op C / T runs the mirror image (row subtree first).  The exchange is the only
+data-path collective: the paper's own distributed algorithm is "omitted", so this
+layout is the build's; the closure argument (z^l_{tau,nu} depends only on
+X(S_nu), both contributions to y^{l+1}_{tau'} share tau = tau'>>1) is P:302-317.
+
+This module is argument marshalling around the C-ABI plus the collective call: every
+arithmetic step runs in libbfapply's kernels.  With ``device=None`` the handle is a
+HOST-ONLY plan (bf_dist_create with device < 0): its layouts and exchange maps drive the
+multi-process CPU (gloo) tests of the exchange logic.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .bfapply import OPS, BFError, Workspace, _Keep, _check, _check_rhs, _stream_handle, _torch_dtype, lib, make_desc
+
+_SIGS = [
+    ("bf_dist_exchange_blocks", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+]
+
+
+def _lib():
+    L = lib()
+    for name, res, args in _SIGS:
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    return L
+
+
+def _opk(op: str) -> int:
+    return 0 if op == "N" else 1
+
+
+class DistBFHandle:
+    """This rank's share of a butterfly split over ``world`` processes (bf_dist_create)."""
+
+    def __init__(self, bf, rank: int, world: int, device: Optional[int] = 0, group=None):
+        keep = _Keep()
+        d = make_desc(bf, keep)
+        h = C.c_void_p()
+        dev = -1 if device is None else int(device)
+        _check("bf_dist_create", _lib().bf_dist_create(C.byref(d), rank, world, dev, C.byref(h)))
+        self.h, self.rank, self.world, self.device, self.code = h, rank, world, device, d.dtype
+        self.group = group
+        self.cs = 16 if d.dtype == 2 else 8
+        self.m, self.n = bf.m, bf.n
+        self.ws = Workspace(torch.device("cuda", device)) if device is not None else None
+        self._rows = {}
+        for op in ("N", "C"):
+            ri, ro, ui, uo = (C.c_int64() for _ in range(4))
+            _check("bf_dist_local_rows", _lib().bf_dist_local_rows(h, OPS[op], C.byref(ri), C.byref(ro),
+                                                                    C.byref(ui), C.byref(uo)))
+            self._rows[op] = (ri.value, ro.value, ui.value, uo.value)
+        self._rows["T"] = self._rows["C"]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().bf_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # ---- layout -------------------------------------------------------------------
+    def layout(self, op: str, nrhs: int):
+        """(work_bytes, send_off, recv_off, send_counts, recv_counts) -- offsets in bytes,
+        counts in complex elements per peer (bf_dist_layout)."""
+        wb, so, ro = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        sc = (C.c_int64 * self.world)()
+        rc = (C.c_int64 * self.world)()
+        _check("bf_dist_layout", _lib().bf_dist_layout(self.h, OPS[op], nrhs, C.byref(wb), C.byref(so), C.byref(ro),
+                                                        sc, rc))
+        return wb.value, so.value, ro.value, list(sc), list(rc)
+
+    def exchange_blocks(self, op: str):
+        """Centre blocks in send-region and recv-region order (bf_dist_exchange_blocks)."""
+        ns, nr = C.c_int64(), C.c_int64()
+        _check("bf_dist_exchange_blocks", _lib().bf_dist_exchange_blocks(self.h, OPS[op], C.byref(ns), None,
+                                                                          C.byref(nr), None))
+        s = np.zeros(max(ns.value, 1), dtype=np.int64)
+        r = np.zeros(max(nr.value, 1), dtype=np.int64)
+        _check("bf_dist_exchange_blocks", _lib().bf_dist_exchange_blocks(
+            self.h, OPS[op], C.byref(ns), s.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(nr),
+            r.ctypes.data_as(C.POINTER(C.c_int64))))
+        return s[:ns.value], r[:nr.value]
+
+    def local_rows(self, op: str):
+        """(rows_in, rows_out, user_off_in, user_off_out): this rank's slice of X and Y."""
+        return self._rows[op]
+
+    def local_input(self, X: np.ndarray, op: str = "N") -> np.ndarray:
+        """This rank's rows of a full (rows, nrhs) right-hand-side block."""
+        ri, _, ui, _ = self._rows[op]
+        return X[ui:ui + ri]
+
+    def empty_output(self, nrhs: int, op: str = "N") -> torch.Tensor:
+        _, ro, _, _ = self._rows[op]
+        return torch.empty((nrhs, ro), dtype=_torch_dtype(self.code), device=torch.device("cuda", self.device))
+
+    def launches(self, op: str = "N") -> int:
+        n = C.c_int32()
+        _check("bf_rounds", lib().bf_rounds(self.h, OPS[op], C.byref(n)))
+        return n.value
+
+    # ---- apply --------------------------------------------------------------------
+    def exchange(self, work: torch.Tensor, op: str, nrhs: int):
+        """The all-to-all of the centre slabs inside `work` (send region -> recv region)."""
+        _, so, ro, sc, rc = self.layout(op, nrhs)
+        rdt = torch.float64 if self.cs == 16 else torch.float32  # NCCL moves the (re, im) pairs
+        send = work[so:so + sum(sc) * self.cs].view(rdt)
+        recv = work[ro:ro + sum(rc) * self.cs].view(rdt)
+        if self.world == 1:
+            recv.copy_(send)
+            return
+        dist.all_to_all_single(recv, send, output_split_sizes=[2 * c for c in rc],
+                               input_split_sizes=[2 * c for c in sc], group=self.group)
+
+    def apply(self, Xloc: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None,
+              work: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Y_loc = (K X)_loc (op N) or (K^H X)_loc (op C) / (K^T X)_loc (op T)."""
+        if self.ws is None:
+            raise BFError("bf_dist_apply_pre", -8, "host-only plan cannot apply")
+        ri, ro, _, _ = self._rows[op]
+        ldx = _check_rhs(Xloc, ri, self.code, "X_loc")
+        nrhs = Xloc.shape[0]
+        if out is None:
+            out = self.empty_output(nrhs, op)
+        ldy = _check_rhs(out, ro, self.code, "Y_loc")
+        wb = self.layout(op, nrhs)[0]
+        if work is None:
+            work = self.ws.get(wb)
+        st = _stream_handle(stream)
+        _check("bf_dist_apply_pre", lib().bf_dist_apply_pre(self.h, OPS[op], nrhs, C.c_void_p(Xloc.data_ptr()), ldx,
+                                                             C.c_void_p(work.data_ptr()), work.numel(), st))
+        self.exchange(work, op, nrhs)
+        _check("bf_dist_apply_post", lib().bf_dist_apply_post(self.h, OPS[op], nrhs, C.c_void_p(out.data_ptr()), ldy,
+                                                               C.c_void_p(work.data_ptr()), work.numel(), st))
+        return out
+
+    def time_e2e(self, X_loc_host: torch.Tensor, op: str, steps: int, alg_bytes: int):
+        """End-to-end timing through the public API: pinned host X_loc -> device, apply,
+        device -> pinned host Y_loc, every step; max over ranks of the CUDA-event time."""
+        Xp = X_loc_host.contiguous().pin_memory()
+        nrhs = Xp.shape[0]
+        _, ro, _, _ = self._rows[op]
+        Yp = torch.empty((nrhs, ro), dtype=Xp.dtype).pin_memory()
+        Xd = torch.empty_like(Xp, device=torch.device("cuda", self.device))
+        Yd = self.empty_output(nrhs, op)
+        for _ in range(2):
+            Xd.copy_(Xp, non_blocking=True)
+            self.apply(Xd, op, out=Yd)
+            Yp.copy_(Yd, non_blocking=True)
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            Xd.copy_(Xp, non_blocking=True)
+            self.apply(Xd, op, out=Yd)
+            Yp.copy_(Yd, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if self.world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=torch.device("cuda", self.device))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            ms = float(t.item())
+            hb = torch.tensor([Xp.numel() * self.cs, Yp.numel() * self.cs], dtype=torch.int64,
+                              device=torch.device("cuda", self.device))
+            dist.all_reduce(hb, group=self.group)
+            h2d, d2h = int(hb[0].item()), int(hb[1].item())
+        else:
+            h2d, d2h = Xp.numel() * self.cs, Yp.numel() * self.cs
+        return {"value": alg_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "DistBFHandle.apply (pinned host X_loc/Y_loc per rank, copies inside the timed region)"}

@@ -1,0 +1,101 @@
+"""GPU parity of the distributed apply's kernels (bf_dist_apply_pre / _post) against the
+CPU oracle, on ONE device: the P rank-local handles run one after another in this process
+and the all-to-all is replayed as device copies between their workspaces (the same
+send / recv regions NCCL moves; no rank ever waits on another).  World size 1 runs the
+real DistBFHandle.apply with its self exchange."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from bfinputs import random_butterfly, random_ranks_butterfly, random_rhs
+from paper_2007_00202_b200.dist import DistBFHandle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.complex128: 1e-12, np.complex64: 1e-5}
+
+
+def _subtree_perm(n, leaf_ptr, L, p, seed):
+    rng = np.random.default_rng(seed)
+    perm = np.empty(n, dtype=np.int64)
+    w = 1 << (L - p)
+    for g in range(1 << p):
+        a, b = int(leaf_ptr[g * w]), int(leaf_ptr[(g + 1) * w])
+        perm[a:b] = a + rng.permutation(b - a)
+    return perm
+
+
+def emulate(bf, X, op, P):
+    """Run the P-rank split apply on device 0; returns the full (rows_out, nrhs) result."""
+    hs = [DistBFHandle(bf, g, P, 0) for g in range(P)]
+    nrhs = X.shape[1]
+    dt = torch.complex128 if X.dtype == np.complex128 else torch.complex64
+    works, outs = [], []
+    for h in hs:
+        ri, ro, ui, uo = h.local_rows(op)
+        Xl = torch.from_numpy(np.ascontiguousarray(X[ui:ui + ri].T)).cuda()
+        wb = h.layout(op, nrhs)[0]
+        w = torch.zeros(max(wb, 1), dtype=torch.uint8, device="cuda")
+        from paper_2007_00202_b200.bfapply import lib, OPS
+        import ctypes as C
+        rc = lib().bf_dist_apply_pre(h.h, OPS[op], nrhs, C.c_void_p(Xl.data_ptr()), max(ri, 1),
+                                     C.c_void_p(w.data_ptr()), w.numel(), None)
+        assert rc == 0, lib().bf_last_error()
+        works.append(w)
+    cs = hs[0].cs
+    lay = [h.layout(op, nrhs) for h in hs]
+    # replay the all-to-all: rank g's send chunk for q -> rank q's recv chunk from g
+    for g in range(P):
+        _, so, _, sc, _ = lay[g]
+        soff = so
+        for q in range(P):
+            _, _, ro, _, rcq = lay[q]
+            roff = ro + sum(rcq[:g]) * cs
+            n = sc[q] * cs
+            assert n == rcq[g] * cs
+            works[q][roff:roff + n].copy_(works[g][soff:soff + n])
+            soff += n
+    rows_out = bf.m if op == "N" else bf.n
+    Y = np.zeros((rows_out, nrhs), dtype=X.dtype)
+    for h, w in zip(hs, works):
+        ri, ro, ui, uo = h.local_rows(op)
+        Yl = torch.zeros((nrhs, max(ro, 1)), dtype=dt, device="cuda")
+        from paper_2007_00202_b200.bfapply import lib, OPS
+        import ctypes as C
+        rc = lib().bf_dist_apply_post(h.h, OPS[op], nrhs, C.c_void_p(Yl.data_ptr()), max(ro, 1),
+                                      C.c_void_p(w.data_ptr()), w.numel(), None)
+        assert rc == 0, lib().bf_last_error()
+        torch.cuda.synchronize()
+        Y[uo:uo + ro] = Yl[:, :ro].cpu().numpy().T
+    return Y
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("kind", ["uniform", "ragged"])
+def test_dist_emulated(kind, P, dtype):
+    if kind == "uniform":
+        bf = random_butterfly(L=7, leaf=16, r=16, seed=P, dtype=dtype)
+    else:
+        rng = np.random.default_rng(P)
+        bf = random_ranks_butterfly(7, rng.integers(0, 9, 128), rng.integers(1, 9, 128), seed=P, rmin=1,
+                                    rmax=9, dtype=dtype)
+    p = P.bit_length() - 1
+    bf.row_perm = _subtree_perm(bf.m, bf.row_leaf_ptr, bf.L, p, 1)
+    bf.col_perm = _subtree_perm(bf.n, bf.col_leaf_ptr, bf.L, p, 2)
+    K = oracle.bf_dense(bf)
+    for op, nr in (("N", 33), ("C", 20), ("T", 5)):
+        X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=P + nr, dtype=dtype)
+        err = oracle.rel_err(emulate(bf, X, op, P), oracle.apply_op(K, X, op))
+        assert err <= TOL[dtype], (op, err)
+
+
+@pytest.mark.parametrize("op", ["N", "C"])
+def test_dist_world1_self_exchange(op):
+    bf = random_butterfly(L=6, leaf=16, r=16, seed=9)
+    h = DistBFHandle(bf, 0, 1, 0)
+    X = random_rhs(bf.n, 40, seed=4)
+    Y = h.apply(torch.from_numpy(np.ascontiguousarray(X.T)).cuda(), op)
+    torch.cuda.synchronize()
+    assert oracle.rel_err(Y.cpu().numpy().T, oracle.bf_apply(bf, X, op)) <= 1e-12

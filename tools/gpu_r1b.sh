@@ -1,0 +1,6 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 120 ./tools/pipes2 > gpurun_out/pipes2.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_dist.py -x -q > gpurun_out/pytest_dist.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_dist.log
