@@ -376,21 +376,38 @@ struct FastPlan {
   std::vector<FastPass> passes;
   void* F = nullptr;
   int64_t entries = 0;
+  bool contig = false;     // the leaves the X-reading op gathers are runs of consecutive user rows
+  bool even_base = false;  // ... and each starts at an even user row
 };
 
 static bool fast_eligible(const Geom& G, int dtype) {
+  (void)dtype;
   if (G.L < 1) return false;
-  // a leaf operand slot (16 x leaf complex) must fit one factor-ring chunk
-  const int64_t maxleaf = FAST_CHUNK / (FAST_RANK * (dtype == BF_C128 ? 16 : 8));
   for (int32_t v : G.rr)
     if (v != FAST_RANK) return false;
   for (int32_t v : G.rc)
     if (v != FAST_RANK) return false;
   const int64_t lr = G.mt(0), lcn = G.nv(0);
-  if (lr <= 0 || lcn <= 0 || lr % 16 || lcn % 16 || lr > maxleaf || lcn > maxleaf) return false;
-  if ((lr & (lr - 1)) || (lcn & (lcn - 1))) return false;  // slot sizes must divide the chunk
+  // power-of-two leaves, multiples of 16 (whole MMA row groups / k-steps), at most 256 rows
+  if (lr < 16 || lcn < 16 || lr > 256 || lcn > 256) return false;
+  if ((lr & (lr - 1)) || (lcn & (lcn - 1))) return false;
   for (int64_t i = 0; i < G.nb; ++i)
     if (G.mt(i) != lr || G.nv(i) != lcn) return false;
+  return true;
+}
+
+// every leaf of size `leaf` maps to a run of consecutive user rows (so whole rows can be copied)
+static bool leaves_contiguous(const int64_t* perm, int64_t n, int64_t leaf) {
+  if (!perm) return true;
+  for (int64_t s = 0; s < n; s += leaf)
+    for (int64_t i = 1; i < leaf; ++i)
+      if (perm[s + i] != perm[s] + i) return false;
+  return true;
+}
+static bool leaf_bases_even(const int64_t* perm, int64_t n, int64_t leaf) {
+  if (!perm) return leaf % 2 == 0;
+  for (int64_t s = 0; s < n; s += leaf)
+    if (perm[s] & 1) return false;
   return true;
 }
 
@@ -405,33 +422,28 @@ static inline CT cj(CT v, bool c) {
   return v;
 }
 
-// write an M x K operand in the MMA fragment order the fast kernel consumes.
-// complex128 (mma m8n8k4): [mg][ki][mi][lane], lane = 4g + t <-> (row 16mg + 8mi + g, col 4ki + t)
-// complex64 (mma m16n8k8): [mg][ki][lane][e], e: (g, t), (g+8, t), (g, t+4), (g+8, t+4) of the
-//                          16 x 8 block at rows 16mg, cols 8ki
+// one 1 KB k-step record of an M x K operand: row group mg (16 rows), k-step ki, in the MMA
+// fragment order the pass kernel consumes.
+// complex128 (mma m8n8k4, KS = 4): [mi][lane], lane = 4g + t <-> (row 16mg + 8mi + g, col 4ki + t)
+// complex64 (mma m16n8k8, KS = 8): [lane][e], e: (g, t), (g+8, t), (g, t+4), (g+8, t+4) of the
+//                                  16 x 8 block at rows 16mg, cols 8ki
 template <typename CT, typename Fn>
-static void fill_frag(CT* dst, int M, int K, Fn A) {
+static void fill_step(CT* dst, int mg, int ki, Fn A) {
   if (sizeof(CT) == 16) {
-    const int nk = K / 4;
-    for (int mg = 0; mg < M / 16; ++mg)
-      for (int ki = 0; ki < nk; ++ki)
-        for (int mi = 0; mi < 2; ++mi)
-          for (int lane = 0; lane < 32; ++lane) {
-            const int g = lane >> 2, t = lane & 3;
-            dst[((mg * nk + ki) * 2 + mi) * 32 + lane] = A(16 * mg + 8 * mi + g, 4 * ki + t);
-          }
+    for (int mi = 0; mi < 2; ++mi)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, t = lane & 3;
+        dst[mi * 32 + lane] = A(16 * mg + 8 * mi + g, 4 * ki + t);
+      }
   } else {
-    const int nk = K / 8;
-    for (int mg = 0; mg < M / 16; ++mg)
-      for (int ki = 0; ki < nk; ++ki)
-        for (int lane = 0; lane < 32; ++lane) {
-          const int g = lane >> 2, t = lane & 3;
-          CT* d = dst + ((mg * nk + ki) * 32 + lane) * 4;
-          d[0] = A(16 * mg + g, 8 * ki + t);
-          d[1] = A(16 * mg + g + 8, 8 * ki + t);
-          d[2] = A(16 * mg + g, 8 * ki + t + 4);
-          d[3] = A(16 * mg + g + 8, 8 * ki + t + 4);
-        }
+    for (int lane = 0; lane < 32; ++lane) {
+      const int g = lane >> 2, t = lane & 3;
+      CT* d = dst + lane * 4;
+      d[0] = A(16 * mg + g, 8 * ki + t);
+      d[1] = A(16 * mg + g + 8, 8 * ki + t);
+      d[2] = A(16 * mg + g, 8 * ki + t + 4);
+      d[3] = A(16 * mg + g + 8, 8 * ki + t + 4);
+    }
   }
 }
 
@@ -439,13 +451,14 @@ static void fill_frag(CT* dst, int M, int K, Fn A) {
 template <typename CT>
 static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, int opk, size_t* acct) {
   const int L = G.L, lc = G.lc;
+  const int ks = fast_ks((int)sizeof(CT));
   const int np = (L + FAST_DMAX - 1) / FAST_DMAX;
   std::vector<int> lv(np + 1, 0);
   for (int p = 0; p < np; ++p) lv[p + 1] = lv[p] + L / np + (p < L % np ? 1 : 0);
   const int lr = (int)G.mt(0), lcn = (int)G.nv(0);
   const bool adj = opk == 1;
   std::vector<FastPass> passes;
-  int64_t total = 0;
+  int64_t total = 0;  // bytes
   for (int k = 0; k < np; ++k) {
     const int p = adj ? np - 1 - k : k;
     FastPass P{};
@@ -462,6 +475,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       o.kind = kind;
       o.s = s;
       o.leaf = leaf;
+      o.nsteps = fast_nsteps(kind, leaf, ks);
       ops.push_back(o);
     };
     if (!adj) {
@@ -483,16 +497,17 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     }
     require((int)ops.size() <= FAST_MAXOPS, BF_ERR_ARG, "internal: too many ops in a pass");
     P.nops = (int)ops.size();
-    int64_t off = 0;
     const int nslot = 1 << d;
+    int64_t off = 0;
     for (int q = 0; q < P.nops; ++q) {
       ops[q].off = off;
-      off += nslot * fast_slot_size(ops[q]);
+      off += (int64_t)ops[q].nsteps * nslot * FAST_FRAG;
       P.ops[q] = ops[q];
     }
-    P.win_size = off;
+    P.win_bytes = off;
     P.fbase = total;
-    P.factor_entries = off * P.nwin;
+    P.numaj = adj ? 1 : 0;
+    P.factor_entries = off / (int64_t)sizeof(CT) * P.nwin;
     total += off * P.nwin;
     for (int q = 0; q < P.nops; ++q) {
       if (ops[q].kind == FK_LEAF_IN) P.user_in = (adj ? G.m : G.n);
@@ -500,78 +515,92 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     }
     passes.push_back(P);
   }
-  std::vector<CT> host((size_t)total);
+  std::vector<CT> host((size_t)(total / (int64_t)sizeof(CT)));
+  constexpr int REC = FAST_FRAG / (int)sizeof(CT);  // complex entries per k-step record
   for (const FastPass& P : passes) {
     const int d = P.d, nslot = 1 << d;
     for (int64_t w = 0; w < P.nwin; ++w) {
       const int64_t a = w >> P.bbits, b = w & ((int64_t(1) << P.bbits) - 1);
       for (int q = 0; q < P.nops; ++q) {
         const FastOp& op = P.ops[q];
+        CT* base = host.data() + (P.fbase + w * P.win_bytes + op.off) / (int64_t)sizeof(CT);
         for (int o = 0; o < nslot; ++o) {
-          CT* dst = host.data() + P.fbase + w * P.win_size + op.off + o * fast_slot_size(op);
           // block (tau, nu) of slot o at window level s
           auto blk = [&](int s, int64_t& tau, int64_t& nu) {
             const int ds = d - s;
             tau = (a << s) + (o >> ds);
             nu = (b << ds) + (o & ((1 << ds) - 1));
           };
+          // record of k-step `step` of slot o
+          auto rec = [&](int step) { return base + ((int64_t)step * nslot + o) * REC; };
           int64_t tau, nu;
           if (op.kind == FK_LEAF_IN) {
             blk(op.s, tau, nu);
-            if (!adj) {
-              const CT* V = H.Vt + G.vt_off[nu];
-              fill_frag(dst, 16, lcn, [&](int i, int k) { return V[i + k * 16]; });
-            } else {
-              const CT* U = H.U + G.u_off[tau];
-              fill_frag(dst, 16, lr, [&](int i, int k) { return cj(U[k + (int64_t)i * lr], true); });
+            for (int st = 0; st < op.nsteps; ++st) {
+              if (!adj) {
+                const CT* V = H.Vt + G.vt_off[nu];
+                fill_step(rec(st), 0, st, [&](int i, int k) { return V[i + k * 16]; });
+              } else {
+                const CT* U = H.U + G.u_off[tau];
+                fill_step(rec(st), 0, st, [&](int i, int k) { return cj(U[k + (int64_t)i * lr], true); });
+              }
             }
           } else if (op.kind == FK_LEAF_OUT) {
             blk(op.s, tau, nu);
-            if (!adj) {
-              const CT* U = H.U + G.u_off[tau];
-              fill_frag(dst, lr, 16, [&](int i, int k) { return U[i + (int64_t)k * lr]; });
-            } else {
-              const CT* V = H.Vt + G.vt_off[nu];
-              fill_frag(dst, lcn, 16, [&](int i, int k) { return cj(V[k + i * 16], true); });
+            const int kpm = 16 / ks;
+            for (int st = 0; st < op.nsteps; ++st) {
+              const int mg = st / kpm, ki = st % kpm;
+              if (!adj) {
+                const CT* U = H.U + G.u_off[tau];
+                fill_step(rec(st), mg, ki, [&](int i, int k) { return U[i + (int64_t)k * lr]; });
+              } else {
+                const CT* V = H.Vt + G.vt_off[nu];
+                fill_step(rec(st), mg, ki, [&](int i, int k) { return cj(V[k + i * 16], true); });
+              }
             }
           } else if (op.kind == FK_DIAG) {
             blk(op.s, tau, nu);
             const CT* Bb = H.B + G.b_off[G.idx(lc, tau, nu)];
-            fill_frag(dst, 16, 16, [&](int i, int k) { return adj ? cj(Bb[k + i * 16], true) : Bb[i + k * 16]; });
+            for (int st = 0; st < op.nsteps; ++st)
+              fill_step(rec(st), 0, st, [&](int i, int k) { return adj ? cj(Bb[k + i * 16], true) : Bb[i + k * 16]; });
           } else if (op.kind == FK_PAIR_DOWN) {
             blk(op.s + 1, tau, nu);  // output block at level l0 + s + 1
             const int l = P.l0 + op.s + 1;
             if (l <= lc) {  // W_l
               const CT* Wb = H.W + G.w_off[l][G.idx(l, tau, nu)];
-              fill_frag(dst, 16, 32, [&](int i, int k) { return Wb[i + k * 16]; });
+              for (int st = 0; st < op.nsteps; ++st)
+                fill_step(rec(st), 0, st, [&](int i, int k) { return Wb[i + k * 16]; });
             } else {  // R_{l-1}, gather form
               const int lr_ = l - 1;
               const int part = (int)(tau & 1);
               const CT* R0 = H.R + G.r_off[lr_][G.idx(lr_, tau >> 1, 2 * nu)];
               const CT* R1 = H.R + G.r_off[lr_][G.idx(lr_, tau >> 1, 2 * nu + 1)];
-              fill_frag(dst, 16, 32, [&](int i, int k) {
-                const CT* Rs = k < 16 ? R0 : R1;
-                return Rs[(part * 16 + i) + (k & 15) * 32];
-              });
+              for (int st = 0; st < op.nsteps; ++st)
+                fill_step(rec(st), 0, st, [&](int i, int k) {
+                  const CT* Rs = k < 16 ? R0 : R1;
+                  return Rs[(part * 16 + i) + (k & 15) * 32];
+                });
             }
           } else {  // FK_PAIR_UP: output block at level l = l0 + s
             blk(op.s, tau, nu);
             const int l = P.l0 + op.s;
             if (l >= lc) {  // R^H_l: inputs (2tau + p, nu >> 1)
               const CT* Rb = H.R + G.r_off[l][G.idx(l, tau, nu)];
-              fill_frag(dst, 16, 32, [&](int i, int k) {
-                const int pp = k >> 4;
-                return cj(Rb[(pp * 16 + (k & 15)) + i * 32], true);
-              });
+              for (int st = 0; st < op.nsteps; ++st)
+                fill_step(rec(st), 0, st, [&](int i, int k) {
+                  const int pp = k >> 4;
+                  return cj(Rb[(pp * 16 + (k & 15)) + i * 32], true);
+                });
             } else {  // W^H_{l+1}: inputs (2tau + p, nu >> 1) at level l + 1, column part nu & 1
               const int lw = l + 1;
               const CT* W0 = H.W + G.w_off[lw][G.idx(lw, 2 * tau, nu >> 1)];
               const CT* W1 = H.W + G.w_off[lw][G.idx(lw, 2 * tau + 1, nu >> 1)];
               const int cp = (int)(nu & 1);
-              fill_frag(dst, 16, 32, [&](int i, int k) {
-                const CT* Ws = k < 16 ? W0 : W1;
-                return cj(Ws[(k & 15) + (cp * 16 + i) * 16], true);
-              });
+              for (int st = 0; st < op.nsteps; ++st)
+                fill_step(rec(st), 0, st, [&](int i, int k) {
+                  const CT* Ws = k < 16 ? W0 : W1;
+                  return cj(Ws[(k & 15) + (cp * 16 + i) * 16], true);
+                });
             }
           }
         }
@@ -579,11 +608,11 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     }
   }
   FP.passes = std::move(passes);
-  FP.entries = total;
+  FP.entries = total / (int64_t)sizeof(CT);
   if (total) {
-    BF_CK(cudaMalloc(&FP.F, (size_t)total * sizeof(CT)));
-    BF_CK(cudaMemcpy(FP.F, host.data(), (size_t)total * sizeof(CT), cudaMemcpyHostToDevice));
-    *acct += (size_t)total * sizeof(CT);
+    BF_CK(cudaMalloc(&FP.F, (size_t)total));
+    BF_CK(cudaMemcpy(FP.F, host.data(), (size_t)total, cudaMemcpyHostToDevice));
+    *acct += (size_t)total;
   }
 }
 
@@ -896,6 +925,10 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
                                static_cast<const float2*>(d->Vt)};
         for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
       }
+      h->fast[0].contig = leaves_contiguous(d->col_perm, d->n, G.nv(0));
+      h->fast[1].contig = leaves_contiguous(d->row_perm, d->m, G.mt(0));
+      h->fast[0].even_base = leaf_bases_even(d->col_perm, d->n, G.nv(0));
+      h->fast[1].even_base = leaf_bases_even(d->row_perm, d->m, G.mt(0));
       h->use_fast = true;
     }
     h->G = std::move(G);
@@ -954,9 +987,19 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
   const size_t half = fast_ws(h, nrhs) / 2;
   char* buf[2] = {static_cast<char*>(work), static_cast<char*>(work) + half};
   const bool fwd = k == 0;
+  // X rows of a leaf gathered by the producer warp (contiguous leaves only); 16-byte copies when
+  // every leaf row block starts on a 16-byte boundary
+  const bool xpage = FP.contig && !getenv("BF_DISABLE_XPAGE");
+  const bool al16 = h->dtype == BF_C128 ||
+                    (((uintptr_t)X & 15) == 0 && (ldx & 1) == 0 && FP.even_base);
   for (size_t i = 0; i < FP.passes.size(); ++i) {
     FastArgs a{};
     a.p = FP.passes[i];
+    bool has_in = false;
+    for (int q = 0; q < a.p.nops; ++q) has_in |= a.p.ops[q].kind == FK_LEAF_IN;
+    a.p.xpage = has_in && xpage ? 1 : 0;
+    a.xalign16 = al16 ? 1 : 0;
+    if (const char* dg = getenv("BF_FAST_DIAG")) a.diag = atoi(dg);
     a.F = FP.F;
     a.X = X;
     a.ldx = ldx;
