@@ -10,6 +10,12 @@
 
 namespace bfa {
 
+// error carried from deep inside the host logic to the C-ABI boundary
+struct Err {
+  int code;
+  std::string msg;
+};
+
 // One product A * In that contributes to a task's output rows.
 //   A(i, k) = pool[a_off + i * a_rs + k * a_cs]   (conjugated if conj ^ conj_flip)
 //   In(k, :) = slab-space row (in_row + k)        when in_kind == 0

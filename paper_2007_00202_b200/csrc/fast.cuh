@@ -1,23 +1,26 @@
-// Fused "window pass" path for uniform-rank butterflies (rank 16, power-of-two leaves that
-// are multiples of 16).
+// Fast path for uniform-rank butterflies (rank 16, power-of-two leaves that are multiples of 16,
+// at most 256): one apply = a leaf launch, a few window passes, a leaf launch.
 //
-// A pass covers d <= 3 consecutive levels l0..l1 of Eq. (3.3).  One work item is a closed
-// window (SURVEY 7.3 hard part 3): T_O node a at level l0 and T_S node b at level L-l1.  At
-// window level s (0..d) the window holds the S = 2^d slabs (tau, nu) with
+// Leaf launches (leaf.cu): every leaf product of Eq. (3.3)'s outer factors
+// (V^0 = blkdiag(Vt_nu) on the input side, U^L = blkdiag(U_tau) on the output side)
+// in one HBM-bound launch that streams the user block X in / Y out once.
+//
+// Window passes (fast.cu; a2 - a4): a pass covers d <= 3 consecutive levels l0..l1 of
+// Eq. (3.3).  One work item is a closed window (SURVEY 7.3 hard part 3): T_O node a at level l0
+// and T_S node b at level L-l1.  At window level s (0..d) the window holds the S = 2^d slabs
+// (tau, nu) with
 //     tau = a 2^s + (slot >> (d-s)),   nu = b 2^(d-s) + (slot & (2^(d-s)-1)),
-// so every stage inside the pass reads and writes only slabs of the same window, which stay
-// in shared memory.  Between passes, slabs go through two ping-pong HBM buffers in canonical
-// order.
+// so every stage inside the pass reads and writes only slabs of the same window, which stay in
+// shared memory.  Between launches slabs go through two ping-pong HBM buffers in canonical order.
 //
-// Operand stream.  Every op of a pass is a sequence of MMA k-steps; the A operand (the factor
-// block) of one k-step of one slot is one 1 KB fragment-ordered record.  At create time each
-// op's factors are laid out window-major as [step][slot][1 KB], so any run of consecutive
-// k-steps of all slots is one contiguous byte range: the producer warp streams it into 8 KB
-// pages of a shared-memory ring with TMA bulk copies, and all consumer warps walk the pages in
-// order, releasing each page as soon as they have used it.  For the leaf op that reads the
-// user block X, the X rows of each (k-step, slot) are brought in by TMA tensor loads (2-D map
-// over X) into two more pages per A page.
+// Operand stream.  Every op is a sequence of MMA k-steps; the A operand (factor block) of one
+// k-step of one slot is one 1 KB fragment-ordered record.  At create time each op's factors are
+// laid out window-major as [step][slot][1 KB], so any run of consecutive k-steps of all slots
+// is one contiguous byte range that the producer warp streams into 16 KB pages of a shared-
+// memory ring with TMA bulk copies.
 #pragma once
+
+#include <cuda.h>
 
 #include "common.cuh"
 
@@ -29,19 +32,14 @@ constexpr int FAST_NB = 32;                     // right-hand sides per work ite
 constexpr int FAST_DMAX = 3;                    // window levels per pass
 constexpr int FAST_MAXOPS = 8;
 constexpr int FAST_SLAB = FAST_RANK * FAST_NB;  // complex entries per slab (512)
-constexpr int FAST_NCONS = 8;                   // consumer warps
-constexpr int FAST_THREADS = (FAST_NCONS + 1) * 32;  // + one producer warp
+constexpr int FAST_HC = 16;                     // rhs columns per half slab (one pass CTA's share)
+constexpr int FAST_HSLAB = FAST_RANK * FAST_HC; // complex entries per half slab (256)
+constexpr int FAST_NCONS = 16;                  // warps of the pass kernel (no producer warp)
+constexpr int FAST_NCONS_HALF = 8;              // ... per 16-column half
+constexpr int FAST_THREADS = FAST_NCONS * 32;
 constexpr int FAST_FRAG = 1024;                 // bytes of A operand per (k-step, slot)
-constexpr int FAST_PAGE = 16384;                // bytes per ring page
-constexpr int FAST_XBOX = 2048;                 // bytes of X per (k-step, slot): KS rows x 32 rhs
-constexpr int FAST_XSTAGES = 4;                 // X staging depth per consumer warp (k-steps)
-// bytes of the two window buffers; the second doubles as the per-warp X staging of the leaf op
-template <typename E>
-__host__ __device__ constexpr size_t fast_win_region() {
-  constexpr size_t win = (size_t)(1 << FAST_DMAX) * FAST_SLAB * sizeof(E);
-  constexpr size_t xst = (size_t)FAST_NCONS * FAST_XSTAGES * FAST_XBOX;
-  return win + (win > xst ? win : xst);
-}
+constexpr int LEAF_NCONS = 8;                   // warps of the leaf kernels (4 pairs, no producer)
+constexpr int LEAF_THREADS = LEAF_NCONS * 32;
 
 struct FastOp {
   int32_t kind;
@@ -53,8 +51,8 @@ struct FastOp {
 
 struct FastPass {
   int32_t d, L, l0, bbits;  // window levels, tree depth, first level, log2(#b values) = L - l1
-  int32_t nops, in_s, out_s, xpage;  // xpage: LEAF_IN X rows are gathered into ring pages
-  int32_t numaj, pad;                // HBM slab order: 0 tau-major (op N), 1 nu-major (op C / T)
+  int32_t nops, in_s, out_s, leaf;  // leaf: 0 window pass, 1 leaf-in launch, 2 leaf-out launch
+  int32_t numaj, pad;               // HBM slab order: 0 tau-major (op N), 1 nu-major (op C / T)
   int64_t fbase, win_bytes;  // byte offset of window 0's record, bytes per window record
   int64_t nwin;
   int64_t factor_entries, user_in, user_out;  // accounting
@@ -64,25 +62,41 @@ struct FastPass {
 struct FastArgs {
   FastPass p;
   const void* F;
-  const void* X;
-  int64_t ldx;
-  const int64_t* xperm;
-  void* Y;
-  int64_t ldy;
-  const int64_t* yperm;
   const void* Sin;
   void* Sout;
   int64_t nlev;  // slabs per level (2^L)
   int32_t nrhs;
-  int32_t conj_io;  // op T: conjugate X on load and Y on store (K^T X = conj(K^H conj X))
-  int32_t xalign16; // X rows of one leaf start on 16-byte boundaries (else 8-byte cp.async)
-  int32_t diag;     // profiling only (env BF_FAST_DIAG, results are garbage): bit 0 = no operand
-                    // streaming (compute only), bit 1 = inter-pass slabs not written to HBM
+  int32_t diag;  // profiling only (env BF_FAST_DIAG, results are garbage): bit 0 = no operand
+                 // streaming (compute only), bit 1 = output slabs not written to HBM
+};
+
+// Leaf launch: item = (leaf, 32-column tile).  Slab `leaf` of the HBM slab buffer is the leaf's
+// intermediate (both directions: the leaf level's canonical index equals the leaf index).
+struct LeafArgs {
+  CUtensorMap map;       // TMA map over X (mode 0) when tma != 0
+  const void* F;         // leaf records: leaf i at F + i * nsteps KB
+  const void* X;         // mode 0: user block read
+  int64_t ldx;
+  const int64_t* xperm;  // tree position -> user row (NULL = identity)
+  void* Y;               // mode 1: user block written
+  int64_t ldy;
+  const int64_t* yperm;
+  const void* Sin;       // mode 1: slabs read
+  void* Sout;            // mode 0: slabs written
+  int64_t nleaf, nlev;
+  int32_t leaf, nsteps;  // leaf size, k-steps per leaf record
+  int32_t nrhs, conj_io; // conj_io: op T conjugates X on load and Y on store
+  int32_t mode, tma;     // mode 0 = IN, 1 = OUT; tma: X rows by 2-D TMA (contiguous leaves)
+  int32_t npairs, nst;   // concurrent items (warp pairs), smem stages (npairs x depth)
+  int32_t brows, diag;   // chunk rows (IN: leaf rows per stage = TMA box rows; OUT: output rows)
+  int64_t stage_bytes, a_bytes;
 };
 
 void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st);
-size_t fast_smem_bytes(int dtype);
 const char* fast_kernel_name(int dtype);
+// returns false when the leaf launch cannot be configured (shared memory)
+void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st);
+const char* leaf_kernel_name(int dtype, int mode);
 
 // k-steps per MMA along K: complex128 DMMA m8n8k4 -> 4, complex64 TF32 m16n8k8 -> 8
 __host__ __device__ inline int fast_ks(int csize) { return csize == 16 ? 4 : 8; }
@@ -97,5 +111,20 @@ __host__ __device__ inline int fast_nsteps(int kind, int leaf, int ks) {
   }
 }
 
+// HBM ping-pong slab buffers: [rhs tile jt][column half][slab index][16 rows x 16 columns], each
+// half slab swizzled like the shared-memory copies (element (r, c) at r * 16 + (c ^ swz(r))).
+__host__ __device__ inline int64_t half_slab_off(int64_t jt, int half, int64_t nlev, int64_t idx) {
+  return ((jt * 2 + half) * nlev + idx) * FAST_HSLAB;
+}
+
+// slab index of block (tau, nu) at level l in the HBM ping-pong buffers: tau-major for op N,
+// nu-major for op C / T, so that the S slabs a window reads at its input level are contiguous
+// (one bulk copy) in both directions.
+__host__ __device__ inline int64_t slab_index(const FastPass& P, int64_t a, int64_t b, int s, int slot) {
+  const int ds = P.d - s, l = P.l0 + s;
+  const int64_t tau = (a << s) + (slot >> ds);
+  const int64_t nu = (b << ds) + (slot & ((1 << ds) - 1));
+  return P.numaj ? (nu << l) + tau : (tau << (P.L - l)) + nu;
+}
 
 }  // namespace bfa

@@ -1,0 +1,243 @@
+// Leaf kernels of the fast path (SURVEY 8(a) rows a1 and a5, and their adjoints in a6):
+//   IN : z_i = A_i X(rows of leaf i, :)     A_i = Vt_nu (op N) or U_tau^H (op C)    (V^0; U^L)
+//   OUT: Y(rows of leaf i, :) = A_i y_i     A_i = U_tau (op N) or conj(Vt_nu)^T (op C)
+// One item = (leaf, 32-column rhs tile).  Each leaf product is (16 x leaf)(leaf x 32) or
+// (leaf x 16)(16 x 32): HBM-bound (the user block is read / written once, the factor once), so
+// the kernel is built around keeping enough bytes in flight.
+//   * 4 independent warp pairs, item k of the CTA to pair k % npairs; warp h of a pair owns the
+//     rhs columns [16h, 16h + 16).  An item is processed in chunks (IN: KC rows of the leaf, OUT:
+//     MC output rows), each chunk one shared-memory stage: the A records of the chunk (one 1-D
+//     bulk copy) plus, for IN, the chunk's X rows as one 2-D TMA tile (KC rows x 32 columns,
+//     column-major; columns beyond nrhs arrive as zeros), for OUT the leaf's slab (bulk copy).
+//   * each pair streams its own chunks through its own DEP stages: lane 0 of the pair's first
+//     warp keeps DEP chunks in flight and re-arms a stage as soon as both warps are done with it
+//     (a 64-thread named barrier), so no producer warp and no cross-pair coupling.
+//   IN writes the output slab to HBM; OUT writes Y rows straight from the accumulators (each store
+//   instruction covers 8 consecutive rows x 4 columns: full sectors).
+// Leaves whose user rows are not contiguous runs (general permutations) read X through the
+// permutation with plain loads (correct, not fast).
+#include <cstdio>
+
+#include "mma.cuh"
+
+namespace bfa {
+
+template <class Pol, int MODE>
+__global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant__ LeafArgs A) {
+  using E = typename Pol::E;
+  constexpr int KS = Pol::KS;
+  constexpr int NT = Pol::NT;
+  constexpr int KPS = FAST_RANK / KS;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Lf = A.leaf;
+  const int64_t nitems = A.nleaf * ((A.nrhs + FAST_NB - 1) / FAST_NB);
+  const int dep = A.nst / A.npairs, npairs = A.npairs;
+  const int chunk = A.brows;                  // IN: KC leaf rows; OUT: MC output rows
+  const int nch = Lf / chunk;                 // chunks per item
+  const size_t stage = (size_t)A.stage_bytes;
+  const size_t a_item = (size_t)A.nsteps * FAST_FRAG;          // A bytes of one leaf
+  const size_t a_chunk = a_item / nch;                          // A bytes of one chunk
+  const int pr = warp >> 1, h = warp & 1;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + A.nst * stage);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < A.nst; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (pr >= npairs) return;
+  unsigned char* mystages = smem + (size_t)pr * dep * stage;
+  uint64_t* myfull = full + pr * dep;
+  const bool leader = h == 0 && lane == 0;
+  // chunk sequence of this pair: c -> item k = pr + (c / nch) * npairs, chunk c % nch
+  auto issue = [&](int64_t c) {
+    const int64_t item = blockIdx.x + (pr + (c / nch) * npairs) * (int64_t)gridDim.x;
+    if (item >= nitems) return;
+    const int ch = (int)(c % nch);
+    const int64_t leaf = item % A.nleaf, jt = item / A.nleaf;
+    const int st = (int)(c % dep);
+    unsigned char* sb = mystages + st * stage;
+    uint32_t bytes = (uint32_t)a_chunk;
+    if (MODE == 0 && A.tma) bytes += (uint32_t)(chunk * FAST_NB * sizeof(E));
+    if (MODE == 1) bytes += (uint32_t)(2 * FAST_HSLAB * sizeof(E));
+    mbar_expect_tx(&myfull[st], bytes);
+    bulk_g2s(sb, static_cast<const unsigned char*>(A.F) + leaf * a_item + ch * a_chunk, (uint32_t)a_chunk, &myfull[st]);
+    if (MODE == 0 && A.tma) {
+      const int64_t r0 = (A.xperm ? A.xperm[leaf * Lf] : leaf * Lf) + (int64_t)ch * chunk;
+      tma_load_2d(sb + a_chunk, &A.map, (int)(r0 * (int64_t)(sizeof(E) / 8)), (int)(jt * FAST_NB), &myfull[st]);
+    }
+    if (MODE == 1)
+      for (int hh = 0; hh < 2; ++hh)
+        bulk_g2s(sb + a_chunk + hh * FAST_HSLAB * sizeof(E), static_cast<const E*>(A.Sin) + half_slab_off(jt, hh, A.nlev, leaf),
+                 (uint32_t)(FAST_HSLAB * sizeof(E)), &myfull[st]);
+  };
+  if (leader) {
+    if (A.tma && MODE == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&A.map)) : "memory");
+    for (int c = 0; c < dep; ++c) issue(c);
+  }
+
+  const int g = lane >> 2, t = lane & 3;
+  const int c0w = 8 * NT * h;  // first column of this warp inside the 32-column tile (= half h)
+  const bool cj = A.conj_io != 0;
+  int bo[NT];
+#pragma unroll
+  for (int ni = 0; ni < NT; ++ni) bo[ni] = Pol::boff(t, g, 0, ni);
+  int64_t c = 0;  // chunk sequence number
+  for (int64_t item = blockIdx.x + (int64_t)pr * gridDim.x; item < nitems; item += (int64_t)npairs * gridDim.x) {
+    const int64_t leaf = item % A.nleaf, jt = item / A.nleaf;
+    const int j0 = (int)jt * FAST_NB + c0w;  // first rhs column of this warp
+    typename Pol::Acc acc;
+    acc.zero();
+    for (int ch = 0; ch < nch; ++ch, ++c) {
+      const int st = (int)(c % dep);
+      const unsigned char* sb = mystages + st * stage;
+      mbar_wait(&myfull[st], (uint32_t)((c / dep) & 1), 12);
+      if (MODE == 0) {
+        // z += A_leaf(:, chunk rows) * X(chunk rows, tile)
+        const E* xb = reinterpret_cast<const E*>(sb + a_chunk);
+        const int nks = chunk / KS;
+#pragma unroll 4
+        for (int s = 0; s < nks; ++s) {
+          typename Pol::Frags f;
+          Pol::load_a(f, sb + (size_t)s * FAST_FRAG, lane);
+          if (A.tma) {
+            Pol::load_b_col(f, xb, chunk, s * KS, c0w, g, t, cj);
+          } else {
+            int64_t p[Pol::XROWS], rows[Pol::XROWS];
+            Pol::x_rows(p, leaf * Lf + (int64_t)ch * chunk + s * KS, t);
+#pragma unroll
+            for (int e = 0; e < Pol::XROWS; ++e) rows[e] = A.xperm ? A.xperm[p[e]] : p[e];
+            Pol::load_b_x(f, static_cast<const E*>(A.X), rows, A.ldx, j0, g, A.nrhs, cj);
+          }
+          acc.mac(f);
+        }
+      } else {
+        // Y(chunk rows of leaf, tile) = A_leaf(chunk rows, :) (MC x 16) * y (16 x 32), 16 rows at a time
+        const E* ys = reinterpret_cast<const E*>(sb + a_chunk) + h * FAST_HSLAB;  // this warp's half slab
+        E* __restrict__ Y = static_cast<E*>(A.Y);
+        const int64_t base = A.tma ? (A.yperm ? A.yperm[leaf * Lf] : leaf * Lf) : 0;
+        for (int mgl = 0; mgl < chunk / 16; ++mgl) {
+          acc.zero();
+#pragma unroll
+          for (int ki = 0; ki < KPS; ++ki) {
+            typename Pol::Frags f;
+            Pol::load_a(f, sb + (size_t)(mgl * KPS + ki) * FAST_FRAG, lane);
+            Pol::load_b(f, ys + ki * KS * FAST_HC, bo);
+            acc.mac(f);
+          }
+          const int64_t rr = (int64_t)ch * chunk + mgl * 16;  // first leaf row of this group
+          acc.each(g, t, [&](int r, int cc, E v) {
+            const int col = j0 + cc;
+            if (col < A.nrhs) {
+              const int64_t row = A.tma ? base + rr + r : (A.yperm ? A.yperm[leaf * Lf + rr + r] : leaf * Lf + rr + r);
+              if (cj) v.y = -v.y;
+              Y[row + (int64_t)col * A.ldy] = v;
+            }
+          });
+        }
+      }
+      // both warps of the pair are done with the stage: re-arm it DEP chunks ahead
+      named_sync(1 + pr, 64);
+      if (leader) issue(c + dep);
+    }
+    if (MODE == 0) {
+      E* dst = static_cast<E*>(A.Sout) + half_slab_off(jt, h, A.nlev, leaf);
+      acc.each(g, t, [&](int r, int cc, E v) { dst[r * FAST_HC + (cc ^ Pol::swz(r))] = v; });
+    }
+  }
+}
+
+// ---- host side ----------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encode_fn() {
+  static EncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D map over a column-major (rows x nrhs, ld) complex block in 8-byte units; box = brows x 32
+static bool make_map(int dtype, const void* base, int64_t rows, int64_t nrhs, int64_t ld, int brows, CUtensorMap* map) {
+  const int64_t cs = dtype == BF_C128 ? 16 : 8, w = cs / 8;
+  if (((uintptr_t)base & 15) || (ld * cs) % 16 || rows * w >= (int64_t(1) << 31) || nrhs >= (int64_t(1) << 31))
+    return false;
+  if (brows * w > 256) return false;
+  EncodeTiled fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)(rows * w), (cuuint64_t)nrhs};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * cs)};
+  const cuuint32_t box[2] = {(cuuint32_t)(brows * w), (cuuint32_t)FAST_NB};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr size_t LEAF_SMEM = 227 * 1024;
+
+template <class Pol, int MODE>
+static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  using E = typename Pol::E;
+  const int nch = a.leaf / a.brows;
+  const size_t a_chunk = (size_t)a.nsteps * FAST_FRAG / nch;
+  const size_t b_bytes = MODE == 0 ? (a.tma ? (size_t)a.brows * FAST_NB * sizeof(E) : 0) : 2 * FAST_HSLAB * sizeof(E);
+  a.stage_bytes = (int64_t)((a_chunk + b_bytes + 1023) & ~size_t(1023));
+  const size_t avail = LEAF_SMEM - 64 * 8;  // barriers
+  const size_t stg = (size_t)a.stage_bytes;
+  const int np = LEAF_NCONS / 2;
+  int dep = (int)(avail / ((size_t)np * stg));
+  if (dep > 4) dep = 4;
+  if (dep < 1) throw Err{BF_ERR_ARG, "leaf chunk too large for the leaf kernel's shared memory"};
+  a.npairs = np;
+  a.nst = np * dep;
+  const size_t smem = (size_t)a.nst * stg + (size_t)a.nst * 8;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_leaf<Pol, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  const int64_t items = a.nleaf * ((a.nrhs + FAST_NB - 1) / FAST_NB);
+  const unsigned grid = (unsigned)(items < nsm ? items : nsm);
+  k_leaf<Pol, MODE><<<grid, LEAF_THREADS, smem, st>>>(a);
+}
+
+void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
+  const int w = dtype == BF_C128 ? 2 : 1;
+  // chunk: IN 32 (c128) / 64 (c64) leaf rows = 8 KB of A records; OUT 32 output rows
+  const int kc = a.mode == 0 ? (dtype == BF_C128 ? 32 : 64) : 32;
+  a.brows = a.leaf < kc ? a.leaf : kc;
+  // X by TMA when the leaves are contiguous runs of user rows and the block is aligned
+  if (a.tma && a.mode == 0)
+    a.tma = make_map(dtype, a.X, a.nleaf * a.leaf, a.nrhs, a.ldx, a.brows, &a.map) ? 1 : 0;
+  (void)w;
+  if (dtype == BF_C128) {
+    if (a.mode == 0) launch_leaf_t<PolC128<2>, 0>(a, st);
+    else launch_leaf_t<PolC128<2>, 1>(a, st);
+  } else {
+    if (a.mode == 0) launch_leaf_t<PolC64<2>, 0>(a, st);
+    else launch_leaf_t<PolC64<2>, 1>(a, st);
+  }
+}
+
+const char* leaf_kernel_name(int dtype, int mode) {
+  static const char* nm[2][2] = {{"k_leaf<c64,in>", "k_leaf<c64,out>"}, {"k_leaf<c128,in>", "k_leaf<c128,out>"}};
+  return nm[dtype == BF_C128][mode];
+}
+
+}  // namespace bfa

@@ -1,0 +1,319 @@
+// Device building blocks shared by the fast-path kernels (fast.cu: window passes, leaf.cu: leaf
+// products): mbarrier / TMA helpers and the two tensor-pipe complex-product policies.
+//
+// complex128 (PolC128): mma.sync.m8n8k4.f64 ("DMMA") with the 3-multiplication product
+//     P1 = Ar Br,  P2 = Ai Bi,  P3 = (Ar + Ai)(Br + Bi);   Re = P1 - P2,  Im = P3 - P1 - P2.
+// (DMMA and DFMA share one FP64 budget on B200 -- profiles/r01_pipes2.txt -- so fewer
+// multiplications is the lever.)
+// complex64 (PolC64): the same 3M product on mma.sync.m16n8k8.tf32 with the 3xTF32 split
+// x = hi + lo, a*b ~ ah*bh + ah*bl + al*bh: FP32-level accuracy at tensor-pipe rate (plain TF32,
+// ~1e-3, would fail the 1e-5 bar -- SURVEY 7.3).
+//
+// A operands (factor blocks) arrive as 1 KB k-step records in MMA fragment order (written once
+// at bf_create, plan.cu fill_step).  B operands come from
+//   * a half slab in shared memory: 16 rows x 16 columns, element (row, col) at
+//     row*16 + (col ^ swz(row)) (bank-conflict free for C-fragment stores and B-fragment loads);
+//   * a column-major box of user rows in shared memory (TMA 2-D tile of X);
+//   * global memory through a row permutation (gather fallback).
+#pragma once
+
+#include <cuda.h>
+#include <cstdio>
+
+#include "fast.cuh"
+
+namespace bfa {
+
+// ---- mbarrier / TMA helpers -----------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA), completion counted on `bar` (complete_tx)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 2-D tensor tile load (TMA) into shared memory, completion counted on `bar`
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait for the phase of `bar` with the given parity.  A watchdog turns a protocol deadlock into
+// a trapped launch (BF_ERR_CUDA on the next call) instead of a hung device.
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, int tag) {
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > (1ll << 34)) {
+      printf("bfapply: mbarrier watchdog block %d thread %d tag %d parity %u\n", blockIdx.x, threadIdx.x, tag, parity);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
+  if (!mbar_try(bar, parity)) mbar_wait_slow(bar, parity, tag);
+}
+// shared-memory counter increment with acquire-release semantics (the last arriver of a release
+// count re-arms a buffer with TMA: every arriver's reads of it happen before)
+__device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;\n" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+// named barrier over `nthreads` threads (ids >= 1; 0 is __syncthreads)
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ======================================================================================
+// complex128 policy: DMMA m8n8k4, fragments (lane = 4g + t):
+//   A (8x4): A[g][t];  B (4x8): B[t][g];  C (8x8): C[g][2t+e].
+// One k-step record (1 KB): [mi][lane] double2 for the 16 x 4 block.
+// With KS = 4 the slab swizzle of row k0 + t depends only on t, so every B-fragment address is
+// slab + k0 * 16 + (a lane constant).
+// ======================================================================================
+template <int NT_>
+struct PolC128 {
+  using E = double2;
+  static constexpr int KS = 4;
+  static constexpr int NT = NT_;  // 8-column n-tiles per warp
+  __host__ __device__ static __forceinline__ int swz(int row) { return ((row & 3) << 1) | (row & 1); }
+  __device__ static __forceinline__ void mma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+  }
+  // operands of one k-step, with the 3M sums precomputed
+  struct Frags {
+    double2 a[2];
+    double as[2];
+    double2 b[NT];
+    double bs[NT];
+  };
+  // lane-constant element offset of B row t, n-tile ni (k0 = 0) inside a half slab
+  __device__ static __forceinline__ int boff(int t, int g, int c0w, int ni) {
+    return t * FAST_HC + ((c0w + 8 * ni + g) ^ swz(t));
+  }
+  __device__ static __forceinline__ void load_a(Frags& f, const unsigned char* rec, int lane) {
+    const E* p = reinterpret_cast<const E*>(rec);
+    f.a[0] = p[lane];
+    f.a[1] = p[32 + lane];
+    f.as[0] = f.a[0].x + f.a[0].y;
+    f.as[1] = f.a[1].x + f.a[1].y;
+  }
+  __device__ static __forceinline__ void set_b(Frags& f, int ni, E v) {
+    f.b[ni] = v;
+    f.bs[ni] = v.x + v.y;
+  }
+  __device__ static __forceinline__ void load_b(Frags& f, const E* slab_k0, const int (&bo)[NT]) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) set_b(f, ni, slab_k0[bo[ni]]);
+  }
+  // from a column-major box (element (k, c) at c * ldb + k) in shared memory, rows k0..
+  __device__ static __forceinline__ void load_b_col(Frags& f, const E* box, int ldb, int k0, int c0w, int g, int t,
+                                                    bool cj) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      E v = box[(c0w + 8 * ni + g) * ldb + k0 + t];
+      if (cj) v.y = -v.y;
+      set_b(f, ni, v);
+    }
+  }
+  static constexpr int XROWS = 1;
+  __device__ static __forceinline__ void x_rows(int64_t (&p)[XROWS], int64_t k0, int t) { p[0] = k0 + t; }
+  // from global memory: user rows rows[] (already permuted), columns col0 + 8 ni + g
+  __device__ static __forceinline__ void load_b_x(Frags& f, const E* __restrict__ X, const int64_t (&rows)[XROWS],
+                                                  int64_t ldx, int col0, int g, int nrhs, bool cj) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      const int col = col0 + 8 * ni + g;
+      E v = col < nrhs ? __ldg(X + rows[0] + (int64_t)col * ldx) : make_double2(0.0, 0.0);
+      if (cj) v.y = -v.y;
+      set_b(f, ni, v);
+    }
+  }
+  struct Acc {
+    double p[3][2][NT][2];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) p[q][mi][ni][0] = p[q][mi][ni][1] = 0.0;
+    }
+    // one k-step: 3 x 2 x NT DMMAs
+    __device__ __forceinline__ void mac(const Frags& f) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) {
+          mma(p[0][mi][ni][0], p[0][mi][ni][1], f.a[mi].x, f.b[ni].x);
+          mma(p[1][mi][ni][0], p[1][mi][ni][1], f.a[mi].y, f.b[ni].y);
+          mma(p[2][mi][ni][0], p[2][mi][ni][1], f.as[mi], f.bs[ni]);
+        }
+    }
+    // visit every output element: fn(row, col_in_warp_tile, value); rows 0..15, cols 0..8NT-1
+    template <typename Fn>
+    __device__ __forceinline__ void each(int g, int t, Fn fn) const {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double p1 = p[0][mi][ni][e], p2 = p[1][mi][ni][e], p3 = p[2][mi][ni][e];
+            fn(8 * mi + g, 8 * ni + 2 * t + e, make_double2(p1 - p2, p3 - p1 - p2));
+          }
+    }
+  };
+};
+
+// ======================================================================================
+// complex64 policy: 3xTF32 mma.sync m16n8k8, fragments (lane = 4g + t):
+//   A (16x8): a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]
+//   B (8x8):  b0 = B[t][g], b1 = B[t+4][g];   C (16x8): c0,c1 = C[g][2t+e], c2,c3 = C[g+8][2t+e]
+// One k-step record (1 KB): [lane][4] float2 for the 16 x 8 block.  The A operand is split into
+// TF32 hi / lo parts once per k-step (load_a); B per n-tile inside mac().
+// ======================================================================================
+template <int NT_>
+struct PolC64 {
+  using E = float2;
+  static constexpr int KS = 8;
+  static constexpr int NT = NT_;
+  __host__ __device__ static __forceinline__ int swz(int row) { return ((row & 1) << 3) | (((row >> 1) & 1) << 2); }
+  __device__ static __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+  __device__ static __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) {
+    hi = __float_as_uint(x) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
+  }
+  struct Frags {
+    uint32_t ah[3][4], al[3][4];  // (re, im, re + im) x fragment registers
+    float2 b[NT][2];
+  };
+  __device__ static __forceinline__ int boff(int t, int g, int c0w, int ni) {
+    return t * FAST_HC + ((c0w + 8 * ni + g) ^ swz(t));  // row t + 4 is +4*16 (same swizzle)
+  }
+  __device__ static __forceinline__ void load_a(Frags& f, const unsigned char* rec, int lane) {
+    const float4* p = reinterpret_cast<const float4*>(rec) + 2 * lane;
+    const float4 x = p[0], y = p[1];
+    const float2 v[4] = {make_float2(x.x, x.y), make_float2(x.z, x.w), make_float2(y.x, y.y), make_float2(y.z, y.w)};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      split(v[e].x, f.ah[0][e], f.al[0][e]);
+      split(v[e].y, f.ah[1][e], f.al[1][e]);
+      split(v[e].x + v[e].y, f.ah[2][e], f.al[2][e]);
+    }
+  }
+  __device__ static __forceinline__ void load_b(Frags& f, const E* slab_k0, const int (&bo)[NT]) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      f.b[ni][0] = slab_k0[bo[ni]];
+      f.b[ni][1] = slab_k0[bo[ni] + 4 * FAST_HC];
+    }
+  }
+  __device__ static __forceinline__ void load_b_col(Frags& f, const E* box, int ldb, int k0, int c0w, int g, int t,
+                                                    bool cj) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      const E* col = box + (c0w + 8 * ni + g) * ldb + k0 + t;
+      float2 v0 = col[0], v1 = col[4];
+      if (cj) {
+        v0.y = -v0.y;
+        v1.y = -v1.y;
+      }
+      f.b[ni][0] = v0;
+      f.b[ni][1] = v1;
+    }
+  }
+  static constexpr int XROWS = 2;
+  __device__ static __forceinline__ void x_rows(int64_t (&p)[XROWS], int64_t k0, int t) {
+    p[0] = k0 + t;
+    p[1] = k0 + t + 4;
+  }
+  __device__ static __forceinline__ void load_b_x(Frags& f, const E* __restrict__ X, const int64_t (&rows)[XROWS],
+                                                  int64_t ldx, int col0, int g, int nrhs, bool cj) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      const int col = col0 + 8 * ni + g;
+      float2 v0 = make_float2(0.f, 0.f), v1 = v0;
+      if (col < nrhs) {
+        v0 = __ldg(X + rows[0] + (int64_t)col * ldx);
+        v1 = __ldg(X + rows[1] + (int64_t)col * ldx);
+      }
+      if (cj) {
+        v0.y = -v0.y;
+        v1.y = -v1.y;
+      }
+      f.b[ni][0] = v0;
+      f.b[ni][1] = v1;
+    }
+  }
+  struct Acc {
+    float p[3][NT][4];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) p[q][ni][e] = 0.f;
+    }
+    __device__ __forceinline__ void mac(const Frags& f) {
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) {
+        uint32_t bh[3][2], bl[3][2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          split(f.b[ni][e].x, bh[0][e], bl[0][e]);
+          split(f.b[ni][e].y, bh[1][e], bl[1][e]);
+          split(f.b[ni][e].x + f.b[ni][e].y, bh[2][e], bl[2][e]);
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          mma(p[q][ni], f.ah[q], bl[q]);
+          mma(p[q][ni], f.al[q], bh[q]);
+          mma(p[q][ni], f.ah[q], bh[q]);
+        }
+      }
+    }
+    template <typename Fn>
+    __device__ __forceinline__ void each(int g, int t, Fn fn) const {
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p1 = p[0][ni][e], p2 = p[1][ni][e], p3 = p[2][ni][e];
+          fn(g + 8 * (e >> 1), 8 * ni + 2 * t + (e & 1), make_float2(p1 - p2, p3 - p1 - p2));
+        }
+    }
+  };
+};
+
+}  // namespace bfa

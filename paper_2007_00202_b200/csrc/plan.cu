@@ -32,10 +32,6 @@ thread_local std::string g_last_error;
 // are computed, nothing is uploaded, and every apply on the handle fails with BF_ERR_DEVICE.
 thread_local bool g_host_only = false;
 
-struct Err {
-  int code;
-  std::string msg;
-};
 
 #define BF_CK(call)                                                                       \
   do {                                                                                    \
@@ -376,8 +372,8 @@ struct FastPlan {
   std::vector<FastPass> passes;
   void* F = nullptr;
   int64_t entries = 0;
-  bool contig = false;     // the leaves the X-reading op gathers are runs of consecutive user rows
-  bool even_base = false;  // ... and each starts at an even user row
+  bool contig_in = false;   // every leaf the IN launch reads is a run of consecutive user rows
+  bool contig_out = false;  // ... and every leaf the OUT launch writes
 };
 
 static bool fast_eligible(const Geom& G, int dtype) {
@@ -402,12 +398,6 @@ static bool leaves_contiguous(const int64_t* perm, int64_t n, int64_t leaf) {
   for (int64_t s = 0; s < n; s += leaf)
     for (int64_t i = 1; i < leaf; ++i)
       if (perm[s + i] != perm[s] + i) return false;
-  return true;
-}
-static bool leaf_bases_even(const int64_t* perm, int64_t n, int64_t leaf) {
-  if (!perm) return leaf % 2 == 0;
-  for (int64_t s = 0; s < n; s += leaf)
-    if (perm[s] & 1) return false;
   return true;
 }
 
@@ -459,16 +449,10 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   const bool adj = opk == 1;
   std::vector<FastPass> passes;
   int64_t total = 0;  // bytes
-  for (int k = 0; k < np; ++k) {
-    const int p = adj ? np - 1 - k : k;
+  // launch k: 0 = leaf-in, 1..np = window passes, np + 1 = leaf-out
+  for (int k = 0; k < np + 2; ++k) {
     FastPass P{};
     P.L = L;
-    P.l0 = lv[p];
-    P.d = lv[p + 1] - lv[p];
-    const int l0 = P.l0, l1 = lv[p + 1], d = P.d;
-    P.bbits = L - l1;
-    P.nwin = int64_t(1) << (L - d);
-    const bool hasB = (l0 <= lc && lc < l1) || (lc == L && p == np - 1);
     std::vector<FastOp> ops;
     auto add = [&](int kind, int s, int leaf) {
       FastOp o{};
@@ -478,22 +462,41 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       o.nsteps = fast_nsteps(kind, leaf, ks);
       ops.push_back(o);
     };
-    if (!adj) {
-      if (p == 0) add(FK_LEAF_IN, 0, lcn);
-      for (int l = l0 + 1; l <= l1 && l <= lc; ++l) add(FK_PAIR_DOWN, l - 1 - l0, 0);  // W_l
-      if (hasB) add(FK_DIAG, lc - l0, 0);
-      for (int l = std::max(l0, lc); l < l1; ++l) add(FK_PAIR_DOWN, l - l0, 0);      // R_l
-      if (p == np - 1) add(FK_LEAF_OUT, d, lr);
-      P.in_s = p == 0 ? -1 : 0;
-      P.out_s = p == np - 1 ? -1 : d;
+    int d = 0;
+    if (k == 0 || k == np + 1) {
+      // leaf launch (d = 0): window w = one leaf at level 0 (T_S leaf nu = b) or L (T_O leaf tau = a)
+      const bool in = k == 0;
+      const bool at0 = in != adj;  // op N reads X through Vt (level 0); op C through U^H (level L)
+      P.leaf = in ? 1 : 2;
+      P.l0 = at0 ? 0 : L;
+      P.d = 0;
+      P.bbits = L - P.l0;
+      P.nwin = int64_t(1) << L;
+      add(in ? FK_LEAF_IN : FK_LEAF_OUT, 0, at0 ? lcn : lr);
+      P.in_s = in ? -1 : 0;
+      P.out_s = in ? 0 : -1;
     } else {
-      if (p == np - 1) add(FK_LEAF_IN, d, lr);                                       // U^H
-      for (int l = l1 - 1; l >= l0 && l >= lc; --l) add(FK_PAIR_UP, l - l0, 0);        // R^H_l
-      if (hasB) add(FK_DIAG, lc - l0, 0);                                              // B^H
-      for (int l = std::min(l1, lc); l >= l0 + 1; --l) add(FK_PAIR_UP, l - 1 - l0, 0); // W^H_l
-      if (p == 0) add(FK_LEAF_OUT, 0, lcn);                                            // Vt^H
-      P.in_s = p == np - 1 ? -1 : d;
-      P.out_s = p == 0 ? -1 : 0;
+      const int p = adj ? np - k : k - 1;
+      P.l0 = lv[p];
+      P.d = lv[p + 1] - lv[p];
+      const int l0 = P.l0, l1 = lv[p + 1];
+      d = P.d;
+      P.bbits = L - l1;
+      P.nwin = int64_t(1) << (L - d);
+      const bool hasB = (l0 <= lc && lc < l1) || (lc == L && l1 == L);  // lc = L: B after the last W
+      if (!adj) {
+        for (int l = l0 + 1; l <= l1 && l <= lc; ++l) add(FK_PAIR_DOWN, l - 1 - l0, 0);  // W_l
+        if (hasB) add(FK_DIAG, lc - l0, 0);
+        for (int l = std::max(l0, lc); l < l1; ++l) add(FK_PAIR_DOWN, l - l0, 0);      // R_l
+        P.in_s = 0;
+        P.out_s = d;
+      } else {
+        for (int l = l1 - 1; l >= l0 && l >= lc; --l) add(FK_PAIR_UP, l - l0, 0);        // R^H_l
+        if (hasB) add(FK_DIAG, lc - l0, 0);                                              // B^H
+        for (int l = std::min(l1, lc); l >= l0 + 1; --l) add(FK_PAIR_UP, l - 1 - l0, 0); // W^H_l
+        P.in_s = d;
+        P.out_s = 0;
+      }
     }
     require((int)ops.size() <= FAST_MAXOPS, BF_ERR_ARG, "internal: too many ops in a pass");
     P.nops = (int)ops.size();
@@ -925,10 +928,12 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
                                static_cast<const float2*>(d->Vt)};
         for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
       }
-      h->fast[0].contig = leaves_contiguous(d->col_perm, d->n, G.nv(0));
-      h->fast[1].contig = leaves_contiguous(d->row_perm, d->m, G.mt(0));
-      h->fast[0].even_base = leaf_bases_even(d->col_perm, d->n, G.nv(0));
-      h->fast[1].even_base = leaf_bases_even(d->row_perm, d->m, G.mt(0));
+      const bool cc = leaves_contiguous(d->col_perm, d->n, G.nv(0));
+      const bool rc = leaves_contiguous(d->row_perm, d->m, G.mt(0));
+      h->fast[0].contig_in = cc;
+      h->fast[0].contig_out = rc;
+      h->fast[1].contig_in = rc;
+      h->fast[1].contig_out = cc;
       h->use_fast = true;
     }
     h->G = std::move(G);
@@ -987,37 +992,47 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
   const size_t half = fast_ws(h, nrhs) / 2;
   char* buf[2] = {static_cast<char*>(work), static_cast<char*>(work) + half};
   const bool fwd = k == 0;
-  // X rows of a leaf gathered by the producer warp (contiguous leaves only); 16-byte copies when
-  // every leaf row block starts on a 16-byte boundary
-  const bool xpage = FP.contig && !getenv("BF_DISABLE_XPAGE");
-  const bool al16 = h->dtype == BF_C128 ||
-                    (((uintptr_t)X & 15) == 0 && (ldx & 1) == 0 && FP.even_base);
+  const int diag = getenv("BF_FAST_DIAG") ? atoi(getenv("BF_FAST_DIAG")) : 0;
   for (size_t i = 0; i < FP.passes.size(); ++i) {
-    FastArgs a{};
-    a.p = FP.passes[i];
-    bool has_in = false;
-    for (int q = 0; q < a.p.nops; ++q) has_in |= a.p.ops[q].kind == FK_LEAF_IN;
-    a.p.xpage = has_in && xpage ? 1 : 0;
-    a.xalign16 = al16 ? 1 : 0;
-    if (const char* dg = getenv("BF_FAST_DIAG")) a.diag = atoi(dg);
-    a.F = FP.F;
-    a.X = X;
-    a.ldx = ldx;
-    a.xperm = fwd ? h->d_cperm : h->d_rperm;
-    a.Y = Y;
-    a.ldy = ldy;
-    a.yperm = fwd ? h->d_rperm : h->d_cperm;
-    a.Sin = buf[i % 2];
-    a.Sout = buf[(i + 1) % 2];
-    a.nlev = h->G.nb;
-    a.nrhs = (int32_t)nrhs;
-    a.conj_io = op == BF_OP_T ? 1 : 0;
+    const FastPass& P = FP.passes[i];
     if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), st));
-    launch_fast_pass(h->dtype, a, st);
+    if (P.leaf) {
+      LeafArgs a{};
+      a.mode = P.leaf == 1 ? 0 : 1;
+      a.F = static_cast<const char*>(FP.F) + P.fbase;
+      a.X = X;
+      a.ldx = ldx;
+      a.xperm = fwd ? h->d_cperm : h->d_rperm;
+      a.Y = Y;
+      a.ldy = ldy;
+      a.yperm = fwd ? h->d_rperm : h->d_cperm;
+      a.Sin = buf[i % 2];
+      a.Sout = buf[(i + 1) % 2];
+      a.nleaf = P.nwin;
+      a.nlev = h->G.nb;
+      a.leaf = P.ops[0].leaf;
+      a.nsteps = P.ops[0].nsteps;
+      a.nrhs = (int32_t)nrhs;
+      a.conj_io = op == BF_OP_T ? 1 : 0;
+      // user rows of every leaf contiguous: X by TMA tiles (IN) / Y by base + offset (OUT)
+      a.tma = (a.mode == 0 ? FP.contig_in : FP.contig_out) && !getenv("BF_DISABLE_TMA") ? 1 : 0;
+      a.diag = diag;
+      launch_leaf(h->dtype, a, st);
+    } else {
+      FastArgs a{};
+      a.p = P;
+      a.diag = diag;
+      a.F = FP.F;
+      a.Sin = buf[i % 2];
+      a.Sout = buf[(i + 1) % 2];
+      a.nlev = h->G.nb;
+      a.nrhs = (int32_t)nrhs;
+      launch_fast_pass(h->dtype, a, st);
+    }
     if (getenv("BF_DEBUG_SYNC")) {
       cudaError_t e = cudaStreamSynchronize(st);
-      fprintf(stderr, "bfapply debug: pass %zu (d=%d l0=%d nops=%d nwin=%lld) -> %s\n", i, a.p.d, a.p.l0, a.p.nops,
-              (long long)a.p.nwin, cudaGetErrorString(e));
+      fprintf(stderr, "bfapply debug: launch %zu (leaf=%d d=%d l0=%d nops=%d nwin=%lld) -> %s\n", i, P.leaf, P.d, P.l0,
+              P.nops, (long long)P.nwin, cudaGetErrorString(e));
       BF_CK(e);
     }
   }
@@ -1092,14 +1107,15 @@ int bf_round_info(bf_handle h, int op, int32_t round, bf_round_info_t* info) {
       require(info && round >= 0 && round < (int)h->fast[k].passes.size(), BF_ERR_ARG, "round out of range");
       const FastPass& P = h->fast[k].passes[round];
       memset(info, 0, sizeof(*info));
-      info->kernel = 10;
+      info->kernel = P.leaf ? 10 + P.leaf : 10;  // 10 window pass, 11 leaf in, 12 leaf out
       info->ntasks = (int32_t)P.nwin;
       info->factor_entries = P.factor_entries;
       info->user_rows_in = P.user_in;
       info->user_rows_out = P.user_out;
       info->slab_rows_in = P.in_s >= 0 ? h->G.nb * FAST_RANK : 0;
       info->slab_rows_out = P.out_s >= 0 ? h->G.nb * FAST_RANK : 0;
-      strncpy(info->name, fast_kernel_name(h->dtype), sizeof(info->name) - 1);
+      strncpy(info->name, P.leaf ? leaf_kernel_name(h->dtype, P.leaf - 1) : fast_kernel_name(h->dtype),
+              sizeof(info->name) - 1);
       return BF_OK;
     }
     if (h->dist) {

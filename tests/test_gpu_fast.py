@@ -35,7 +35,9 @@ def test_fast_layouts(L, leaf, lc, dtype):
     bf.row_perm = rng.permutation(bf.m).astype(np.int64)
     bf.col_perm = rng.permutation(bf.n).astype(np.int64)
     h = pkg.BFHandle(bf)
-    assert h.rounds("N")[0]["name"].startswith("k_bf_pass"), h.rounds("N")
+    names = [r["name"] for r in h.rounds("N")]
+    assert names[0].startswith("k_leaf") and names[-1].startswith("k_leaf"), names
+    assert all(n.startswith("k_bf_pass") for n in names[1:-1]), names
     K = oracle.bf_dense(bf)
     for op, nr in (("N", 32), ("C", 45), ("T", 7)):
         X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=L + nr, dtype=dtype)
@@ -75,3 +77,63 @@ def test_fast_vs_generic_cfg5(monkeypatch, dtype):
     tol = 1e-13 if dtype == np.complex128 else 1e-5
     assert (torch.linalg.norm(Yf - Yg) / torch.linalg.norm(Yg)).item() <= tol
     assert (torch.linalg.norm(Yfa - Yga) / torch.linalg.norm(Yga)).item() <= tol
+
+
+def leaf_block_perm(n, leaf, seed):
+    """A permutation that moves whole leaves: every leaf is a contiguous run of user rows (the
+    leaf kernels then move X / Y with TMA tiles instead of per-row gathers)."""
+    rng = np.random.default_rng(seed)
+    blocks = rng.permutation(n // leaf)
+    return (blocks[:, None] * leaf + np.arange(leaf)[None, :]).reshape(-1).astype(np.int64)
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("L,leaf,perm", [(3, 16, "id"), (5, 64, "block"), (4, 32, "block"), (7, 16, "id"),
+                                         (2, 128, "block"), (3, 256, "id"), (6, 64, "block")])
+def test_fast_contiguous_leaves(L, leaf, perm, dtype):
+    """Contiguous leaves (identity or leaf-block permutations): X read by 2-D TMA tiles, Y written
+    by row runs; ragged nrhs (out-of-bounds TMA columns are zero-filled), op N / C / T."""
+    bf = random_butterfly(L=L, leaf=leaf, r=16, seed=L + leaf, dtype=dtype)
+    if perm == "block":
+        bf.row_perm = leaf_block_perm(bf.m, leaf, 1)
+        bf.col_perm = leaf_block_perm(bf.n, leaf, 2)
+    h = pkg.BFHandle(bf)
+    K = oracle.bf_dense(bf)
+    for op, nr in (("N", 32), ("C", 45), ("T", 7), ("N", 70)):
+        X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=L + nr, dtype=dtype)
+        err = oracle.rel_err(host(h.apply(dev(X), op)), oracle.apply_op(K, X, op))
+        assert err <= TOL[dtype], (op, nr, err)
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("pad", [1, 2, 16])
+def test_fast_padded_ld(pad, dtype):
+    """X and Y as column blocks of wider buffers (ld > rows): TMA when ld * sizeof is a multiple
+    of 16 bytes, the gather path otherwise (odd ld for complex64)."""
+    bf = random_butterfly(L=5, leaf=32, r=16, seed=pad, dtype=dtype)
+    h = pkg.BFHandle(bf)
+    K = oracle.bf_dense(bf)
+    nr = 40
+    X = random_rhs(bf.n, nr, seed=pad, dtype=dtype)
+    big = torch.zeros((nr, bf.n + pad), dtype=dev(X).dtype, device="cuda")
+    big[:, :bf.n] = dev(X)
+    outb = torch.full((nr, bf.m + pad), 7.0, dtype=big.dtype, device="cuda")
+    Y = h.apply(big[:, :bf.n], "N", out=outb[:, :bf.m])
+    err = oracle.rel_err(host(Y), K @ X)
+    assert err <= TOL[dtype], err
+    assert torch.all(outb[:, bf.m:] == 7.0), "wrote outside the Y block"
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_fast_tma_equals_gather(monkeypatch, dtype):
+    """The TMA tile path and the per-row gather path of the leaf kernels agree bit for bit
+    (same arithmetic, same order; only the data movement differs)."""
+    bf = random_butterfly(L=6, leaf=64, r=16, seed=3, dtype=dtype)
+    X = dev(random_rhs(bf.n, 50, seed=4, dtype=dtype))
+    h = pkg.BFHandle(bf)
+    Y1, Y1c = h.apply(X, "N"), h.apply(X, "C")
+    torch.cuda.synchronize()
+    monkeypatch.setenv("BF_DISABLE_TMA", "1")
+    Y2, Y2c = h.apply(X, "N"), h.apply(X, "C")
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2) and torch.equal(Y1c, Y2c)
