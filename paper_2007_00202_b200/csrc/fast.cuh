@@ -38,7 +38,7 @@ constexpr int FAST_NCONS = 16;                  // warps of the pass kernel (no 
 constexpr int FAST_NCONS_HALF = 8;              // ... per 16-column half
 constexpr int FAST_THREADS = FAST_NCONS * 32;
 constexpr int FAST_FRAG = 1024;                 // bytes of A operand per (k-step, slot)
-constexpr int LEAF_NCONS = 8;                   // warps of the leaf kernels (4 pairs, no producer)
+constexpr int LEAF_NCONS = 8;                   // warps of the leaf kernels (each owns whole items)
 constexpr int LEAF_THREADS = LEAF_NCONS * 32;
 
 struct FastOp {
@@ -87,7 +87,7 @@ struct LeafArgs {
   int32_t leaf, nsteps;  // leaf size, k-steps per leaf record
   int32_t nrhs, conj_io; // conj_io: op T conjugates X on load and Y on store
   int32_t mode, tma;     // mode 0 = IN, 1 = OUT; tma: X rows by 2-D TMA (contiguous leaves)
-  int32_t npairs, nst;   // concurrent items (warp pairs), smem stages (npairs x depth)
+  int32_t npairs, nst;   // concurrent items (item-owning warps), smem stages (npairs x depth)
   int32_t brows, diag;   // chunk rows (IN: leaf rows per stage = TMA box rows; OUT: output rows)
   int64_t stage_bytes, a_bytes;
 };

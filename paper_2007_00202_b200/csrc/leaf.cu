@@ -2,21 +2,21 @@
 //   IN : z_i = A_i X(rows of leaf i, :)     A_i = Vt_nu (op N) or U_tau^H (op C)    (V^0; U^L)
 //   OUT: Y(rows of leaf i, :) = A_i y_i     A_i = U_tau (op N) or conj(Vt_nu)^T (op C)
 // One item = (leaf, 32-column rhs tile).  Each leaf product is (16 x leaf)(leaf x 32) or
-// (leaf x 16)(16 x 32): HBM-bound (the user block is read / written once, the factor once), so
-// the kernel is built around keeping enough bytes in flight.
-//   * 4 independent warp pairs, item k of the CTA to pair k % npairs; warp h of a pair owns the
-//     rhs columns [16h, 16h + 16).  An item is processed in chunks (IN: KC rows of the leaf, OUT:
-//     MC output rows), each chunk one shared-memory stage: the A records of the chunk (one 1-D
-//     bulk copy) plus, for IN, the chunk's X rows as one 2-D TMA tile (KC rows x 32 columns,
-//     column-major; columns beyond nrhs arrive as zeros), for OUT the leaf's slab (bulk copy).
-//   * each pair streams its own chunks through its own DEP stages: lane 0 of the pair's first
-//     warp keeps DEP chunks in flight and re-arms a stage as soon as both warps are done with it
-//     (a 64-thread named barrier), so no producer warp and no cross-pair coupling.
+// (leaf x 16)(16 x 32): the user block is read / written once and the factor once.
+//   * every warp owns whole items (k = warp, warp + 8, ... of the CTA's items) and all 32
+//     columns (NT = 4: A fragments loaded once per k-step, 24 independent MMAs per k-step);
+//   * an item is processed in chunks (IN: KC rows of the leaf, OUT: MC output rows), each chunk
+//     one shared-memory stage of the warp: the chunk's A records (one 1-D bulk copy) plus, for
+//     IN, the chunk's X rows as one 2-D TMA tile (KC rows x 32 columns, column-major; columns
+//     beyond nrhs arrive as zeros), for OUT the leaf's two half slabs (bulk copies);
+//   * lane 0 of the warp keeps DEP chunks in flight in the warp's own stages and re-arms a stage
+//     as soon as the warp is done with it: no producer warp, no barrier between warps.
 //   IN writes the output slab to HBM; OUT writes Y rows straight from the accumulators (each store
 //   instruction covers 8 consecutive rows x 4 columns: full sectors).
 // Leaves whose user rows are not contiguous runs (general permutations) read X through the
 // permutation with plain loads (correct, not fast).
 #include <cstdio>
+#include <cstdlib>
 
 #include "mma.cuh"
 
@@ -27,31 +27,31 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
   using E = typename Pol::E;
   constexpr int KS = Pol::KS;
   constexpr int NT = Pol::NT;
+  static_assert(NT == 4, "a leaf warp covers the 32-column tile");
   constexpr int KPS = FAST_RANK / KS;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Lf = A.leaf;
   const int64_t nitems = A.nleaf * ((A.nrhs + FAST_NB - 1) / FAST_NB);
-  const int dep = A.nst / A.npairs, npairs = A.npairs;
+  const int nw = A.npairs;                    // item-owning warps
+  const int dep = A.nst / nw;
   const int chunk = A.brows;                  // IN: KC leaf rows; OUT: MC output rows
   const int nch = Lf / chunk;                 // chunks per item
   const size_t stage = (size_t)A.stage_bytes;
   const size_t a_item = (size_t)A.nsteps * FAST_FRAG;          // A bytes of one leaf
   const size_t a_chunk = a_item / nch;                          // A bytes of one chunk
-  const int pr = warp >> 1, h = warp & 1;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + A.nst * stage);
   if (threadIdx.x == 0) {
     for (int i = 0; i < A.nst; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (pr >= npairs) return;
-  unsigned char* mystages = smem + (size_t)pr * dep * stage;
-  uint64_t* myfull = full + pr * dep;
-  const bool leader = h == 0 && lane == 0;
-  // chunk sequence of this pair: c -> item k = pr + (c / nch) * npairs, chunk c % nch
+  if (warp >= nw) return;
+  unsigned char* mystages = smem + (size_t)warp * dep * stage;
+  uint64_t* myfull = full + warp * dep;
+  // chunk sequence of this warp: c -> item k = warp + (c / nch) * nw, chunk c % nch
   auto issue = [&](int64_t c) {
-    const int64_t item = blockIdx.x + (pr + (c / nch) * npairs) * (int64_t)gridDim.x;
+    const int64_t item = blockIdx.x + (warp + (c / nch) * nw) * (int64_t)gridDim.x;
     if (item >= nitems) return;
     const int ch = (int)(c % nch);
     const int64_t leaf = item % A.nleaf, jt = item / A.nleaf;
@@ -71,21 +71,20 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
         bulk_g2s(sb + a_chunk + hh * FAST_HSLAB * sizeof(E), static_cast<const E*>(A.Sin) + half_slab_off(jt, hh, A.nlev, leaf),
                  (uint32_t)(FAST_HSLAB * sizeof(E)), &myfull[st]);
   };
-  if (leader) {
+  if (lane == 0) {
     if (A.tma && MODE == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&A.map)) : "memory");
     for (int c = 0; c < dep; ++c) issue(c);
   }
 
   const int g = lane >> 2, t = lane & 3;
-  const int c0w = 8 * NT * h;  // first column of this warp inside the 32-column tile (= half h)
   const bool cj = A.conj_io != 0;
-  int bo[NT];
+  int bo[NT];  // B-fragment offsets in the two half slabs [half][16 x 16] (OUT)
 #pragma unroll
-  for (int ni = 0; ni < NT; ++ni) bo[ni] = Pol::boff(t, g, 0, ni);
+  for (int ni = 0; ni < NT; ++ni) bo[ni] = (ni >> 1) * FAST_HSLAB + Pol::boff(t, g, 8 * (ni & 1), 0);
   int64_t c = 0;  // chunk sequence number
-  for (int64_t item = blockIdx.x + (int64_t)pr * gridDim.x; item < nitems; item += (int64_t)npairs * gridDim.x) {
+  for (int64_t item = blockIdx.x + (int64_t)warp * gridDim.x; item < nitems; item += (int64_t)nw * gridDim.x) {
     const int64_t leaf = item % A.nleaf, jt = item / A.nleaf;
-    const int j0 = (int)jt * FAST_NB + c0w;  // first rhs column of this warp
+    const int j0 = (int)jt * FAST_NB;  // first rhs column of the tile
     typename Pol::Acc acc;
     acc.zero();
     for (int ch = 0; ch < nch; ++ch, ++c) {
@@ -96,12 +95,12 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
         // z += A_leaf(:, chunk rows) * X(chunk rows, tile)
         const E* xb = reinterpret_cast<const E*>(sb + a_chunk);
         const int nks = chunk / KS;
-#pragma unroll 4
+#pragma unroll 2
         for (int s = 0; s < nks; ++s) {
           typename Pol::Frags f;
           Pol::load_a(f, sb + (size_t)s * FAST_FRAG, lane);
           if (A.tma) {
-            Pol::load_b_col(f, xb, chunk, s * KS, c0w, g, t, cj);
+            Pol::load_b_col(f, xb, chunk, s * KS, 0, g, t, cj);
           } else {
             int64_t p[Pol::XROWS], rows[Pol::XROWS];
             Pol::x_rows(p, leaf * Lf + (int64_t)ch * chunk + s * KS, t);
@@ -113,7 +112,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
         }
       } else {
         // Y(chunk rows of leaf, tile) = A_leaf(chunk rows, :) (MC x 16) * y (16 x 32), 16 rows at a time
-        const E* ys = reinterpret_cast<const E*>(sb + a_chunk) + h * FAST_HSLAB;  // this warp's half slab
+        const E* ys = reinterpret_cast<const E*>(sb + a_chunk);
         E* __restrict__ Y = static_cast<E*>(A.Y);
         const int64_t base = A.tma ? (A.yperm ? A.yperm[leaf * Lf] : leaf * Lf) : 0;
         for (int mgl = 0; mgl < chunk / 16; ++mgl) {
@@ -130,19 +129,22 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
             const int col = j0 + cc;
             if (col < A.nrhs) {
               const int64_t row = A.tma ? base + rr + r : (A.yperm ? A.yperm[leaf * Lf + rr + r] : leaf * Lf + rr + r);
-              if (cj) v.y = -v.y;
+              v.y = conj_im(v.y, cj);
               Y[row + (int64_t)col * A.ldy] = v;
             }
           });
         }
       }
-      // both warps of the pair are done with the stage: re-arm it DEP chunks ahead
-      named_sync(1 + pr, 64);
-      if (leader) issue(c + dep);
+      // the warp is done with the stage: re-arm it DEP chunks ahead
+      __syncwarp();
+      if (lane == 0) issue(c + dep);
     }
     if (MODE == 0) {
-      E* dst = static_cast<E*>(A.Sout) + half_slab_off(jt, h, A.nlev, leaf);
-      acc.each(g, t, [&](int r, int cc, E v) { dst[r * FAST_HC + (cc ^ Pol::swz(r))] = v; });
+      E* dst0 = static_cast<E*>(A.Sout) + half_slab_off(jt, 0, A.nlev, leaf);
+      E* dst1 = static_cast<E*>(A.Sout) + half_slab_off(jt, 1, A.nlev, leaf);
+      acc.each(g, t, [&](int r, int cc, E v) {
+        (cc < FAST_HC ? dst0 : dst1)[r * FAST_HC + ((cc & (FAST_HC - 1)) ^ Pol::swz(r))] = v;
+      });
     }
   }
 }
@@ -200,9 +202,11 @@ static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
   a.stage_bytes = (int64_t)((a_chunk + b_bytes + 1023) & ~size_t(1023));
   const size_t avail = LEAF_SMEM - 64 * 8;  // barriers
   const size_t stg = (size_t)a.stage_bytes;
-  const int np = LEAF_NCONS / 2;
+  const int np = LEAF_NCONS;  // item-owning warps
   int dep = (int)(avail / ((size_t)np * stg));
-  if (dep > 4) dep = 4;
+  int maxdep = 4;
+  if (const char* e = getenv("BF_LEAF_DEP")) maxdep = atoi(e);  // tuning knob
+  if (dep > maxdep) dep = maxdep;
   if (dep < 1) throw Err{BF_ERR_ARG, "leaf chunk too large for the leaf kernel's shared memory"};
   a.npairs = np;
   a.nst = np * dep;
@@ -219,19 +223,21 @@ static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
 
 void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
   const int w = dtype == BF_C128 ? 2 : 1;
-  // chunk: IN 32 (c128) / 64 (c64) leaf rows = 8 KB of A records; OUT 32 output rows
-  const int kc = a.mode == 0 ? (dtype == BF_C128 ? 32 : 64) : 32;
+  // chunk rows (measured best on B200, tools/gpu_r2h.sh): IN 16 (c128) / 32 (c64) leaf rows,
+  // OUT 16 (c128) / 64 (c64) output rows; depth 2-4 stages per warp
+  int kc = a.mode == 0 ? (dtype == BF_C128 ? 16 : 32) : (dtype == BF_C128 ? 16 : 64);
+  if (const char* e = getenv(a.mode == 0 ? "BF_LEAF_KC" : "BF_LEAF_MC")) kc = atoi(e);  // tuning knob
   a.brows = a.leaf < kc ? a.leaf : kc;
   // X by TMA when the leaves are contiguous runs of user rows and the block is aligned
   if (a.tma && a.mode == 0)
     a.tma = make_map(dtype, a.X, a.nleaf * a.leaf, a.nrhs, a.ldx, a.brows, &a.map) ? 1 : 0;
   (void)w;
   if (dtype == BF_C128) {
-    if (a.mode == 0) launch_leaf_t<PolC128<2>, 0>(a, st);
-    else launch_leaf_t<PolC128<2>, 1>(a, st);
+    if (a.mode == 0) launch_leaf_t<PolC128<4>, 0>(a, st);
+    else launch_leaf_t<PolC128<4>, 1>(a, st);
   } else {
-    if (a.mode == 0) launch_leaf_t<PolC64<2>, 0>(a, st);
-    else launch_leaf_t<PolC64<2>, 1>(a, st);
+    if (a.mode == 0) launch_leaf_t<PolC64<4>, 0>(a, st);
+    else launch_leaf_t<PolC64<4>, 1>(a, st);
   }
 }
 

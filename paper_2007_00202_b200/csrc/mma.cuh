@@ -81,6 +81,14 @@ __device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
   asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;\n" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
   return old;
 }
+// conditional negation by flipping the sign bit on the integer pipe (a select of -x would cost
+// an FP64-pipe DADD next to the DMMAs)
+__device__ __forceinline__ double conj_im(double x, bool cj) {
+  return __longlong_as_double(__double_as_longlong(x) ^ ((long long)cj << 63));
+}
+__device__ __forceinline__ float conj_im(float x, bool cj) {
+  return __int_as_float(__float_as_int(x) ^ ((int)cj << 31));
+}
 // named barrier over `nthreads` threads (ids >= 1; 0 is __syncthreads)
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
@@ -136,7 +144,7 @@ struct PolC128 {
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
       E v = box[(c0w + 8 * ni + g) * ldb + k0 + t];
-      if (cj) v.y = -v.y;
+      v.y = conj_im(v.y, cj);
       set_b(f, ni, v);
     }
   }
@@ -149,7 +157,7 @@ struct PolC128 {
     for (int ni = 0; ni < NT; ++ni) {
       const int col = col0 + 8 * ni + g;
       E v = col < nrhs ? __ldg(X + rows[0] + (int64_t)col * ldx) : make_double2(0.0, 0.0);
-      if (cj) v.y = -v.y;
+      v.y = conj_im(v.y, cj);
       set_b(f, ni, v);
     }
   }
@@ -244,10 +252,8 @@ struct PolC64 {
     for (int ni = 0; ni < NT; ++ni) {
       const E* col = box + (c0w + 8 * ni + g) * ldb + k0 + t;
       float2 v0 = col[0], v1 = col[4];
-      if (cj) {
-        v0.y = -v0.y;
-        v1.y = -v1.y;
-      }
+      v0.y = conj_im(v0.y, cj);
+      v1.y = conj_im(v1.y, cj);
       f.b[ni][0] = v0;
       f.b[ni][1] = v1;
     }
@@ -267,10 +273,8 @@ struct PolC64 {
         v0 = __ldg(X + rows[0] + (int64_t)col * ldx);
         v1 = __ldg(X + rows[1] + (int64_t)col * ldx);
       }
-      if (cj) {
-        v0.y = -v0.y;
-        v1.y = -v1.y;
-      }
+      v0.y = conj_im(v0.y, cj);
+      v1.y = conj_im(v1.y, cj);
       f.b[ni][0] = v0;
       f.b[ni][1] = v1;
     }

@@ -902,8 +902,14 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
       if (G.len_W) BF_CK(cudaMemcpy(p + F.w * cs, d->W, G.len_W * cs, cudaMemcpyHostToDevice));
       if (G.len_Vt) BF_CK(cudaMemcpy(p + F.vt * cs, d->Vt, G.len_Vt * cs, cudaMemcpyHostToDevice));
     }
-    if (d->row_perm) h->d_rperm = (int64_t*)upload(d->row_perm, d->m * 8, &h->device_bytes);
-    if (d->col_perm) h->d_cperm = (int64_t*)upload(d->col_perm, d->n * 8, &h->device_bytes);
+    // an identity permutation is stored as NULL (no per-row index loads on the device)
+    auto is_id = [](const int64_t* p, int64_t n) {
+      for (int64_t i = 0; i < n; ++i)
+        if (p[i] != i) return false;
+      return true;
+    };
+    if (d->row_perm && !is_id(d->row_perm, d->m)) h->d_rperm = (int64_t*)upload(d->row_perm, d->m * 8, &h->device_bytes);
+    if (d->col_perm && !is_id(d->col_perm, d->n)) h->d_cperm = (int64_t*)upload(d->col_perm, d->n * 8, &h->device_bytes);
     int64_t cursor = 0;
     Slabs S = canonical_slabs(G, cursor);
     h->slab_rows = cursor;
