@@ -66,8 +66,10 @@ struct FastArgs {
   void* Sout;
   int64_t nlev;  // slabs per level (2^L)
   int32_t nrhs;
+  int32_t skew;  // ns the second column half starts late (tuning knob, env BF_FAST_SKEW)
   int32_t diag;  // profiling only (env BF_FAST_DIAG, results are garbage): bit 0 = no operand
-                 // streaming (compute only), bit 1 = output slabs not written to HBM
+                 // streaming (compute only), bit 1 = output slabs not written to HBM, bit 2 = no
+                 // intermediate epilogue / barriers, bit 3 (with 2) = epilogue stores, no barriers
 };
 
 // Leaf launch: item = (leaf, 32-column tile).  Slab `leaf` of the HBM slab buffer is the leaf's

@@ -447,6 +447,61 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   for (int p = 0; p < np; ++p) lv[p + 1] = lv[p] + L / np + (p < L % np ? 1 : 0);
   const int lr = (int)G.mt(0), lcn = (int)G.nv(0);
   const bool adj = opk == 1;
+  // The centre factor B^{lc} is folded into its neighbour at create time: R'_{tau,nu} = R_{tau,nu}
+  // B_{tau,nu} (32x16, Eq. 3.2 left applied to y = B z) when lc < L, else W'_{tau,nu} = B W
+  // (lc = L).  One fewer window op (epilogue + barrier) and 2.7 % fewer entries streamed per
+  // apply; the product is formed in complex128 on the host.
+  const bool fold_r = lc < L;
+  std::vector<CT> fused;
+  int64_t fbase0 = 0;
+  {
+    const std::vector<int64_t>& off = fold_r ? G.r_off[lc] : G.w_off[lc];
+    const int64_t nbl = G.nb;
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int64_t i = 0; i < nbl; ++i) {
+      lo = std::min(lo, off[i]);
+      hi = std::max(hi, off[i] + 32 * 16);
+    }
+    fbase0 = lo;
+    fused.assign((size_t)(hi - lo), CT{});
+    for (int64_t i = 0; i < nbl; ++i) {
+      const CT* Bb = H.B + G.b_off[i];
+      CT* dst = fused.data() + (off[i] - lo);
+      if (fold_r) {  // R (32 x 16, ld 32) * B (16 x 16)
+        const CT* Rb = H.R + off[i];
+        for (int j = 0; j < 16; ++j)
+          for (int r = 0; r < 32; ++r) {
+            double re = 0, im = 0;
+            for (int k = 0; k < 16; ++k) {
+              const CT x = Rb[r + k * 32], y = Bb[k + j * 16];
+              re += (double)x.x * y.x - (double)x.y * y.y;
+              im += (double)x.x * y.y + (double)x.y * y.x;
+            }
+            dst[r + j * 32].x = re;
+            dst[r + j * 32].y = im;
+          }
+      } else {  // B (16 x 16) * W (16 x 32, ld 16)
+        const CT* Wb = H.W + off[i];
+        for (int j = 0; j < 32; ++j)
+          for (int r = 0; r < 16; ++r) {
+            double re = 0, im = 0;
+            for (int k = 0; k < 16; ++k) {
+              const CT x = Bb[r + k * 16], y = Wb[k + j * 16];
+              re += (double)x.x * y.x - (double)x.y * y.y;
+              im += (double)x.x * y.y + (double)x.y * y.x;
+            }
+            dst[r + j * 16].x = re;
+            dst[r + j * 16].y = im;
+          }
+      }
+    }
+  }
+  auto Rblk = [&](int l, int64_t i) -> const CT* {
+    return fold_r && l == lc ? fused.data() + (G.r_off[l][i] - fbase0) : H.R + G.r_off[l][i];
+  };
+  auto Wblk = [&](int l, int64_t i) -> const CT* {
+    return !fold_r && l == lc ? fused.data() + (G.w_off[l][i] - fbase0) : H.W + G.w_off[l][i];
+  };
   std::vector<FastPass> passes;
   int64_t total = 0;  // bytes
   // launch k: 0 = leaf-in, 1..np = window passes, np + 1 = leaf-out
@@ -483,7 +538,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       d = P.d;
       P.bbits = L - l1;
       P.nwin = int64_t(1) << (L - d);
-      const bool hasB = (l0 <= lc && lc < l1) || (lc == L && l1 == L);  // lc = L: B after the last W
+      const bool hasB = false;  // folded into R^{lc} / W^{lc} (above)
       if (!adj) {
         for (int l = l0 + 1; l <= l1 && l <= lc; ++l) add(FK_PAIR_DOWN, l - 1 - l0, 0);  // W_l
         if (hasB) add(FK_DIAG, lc - l0, 0);
@@ -499,6 +554,8 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       }
     }
     require((int)ops.size() <= FAST_MAXOPS, BF_ERR_ARG, "internal: too many ops in a pass");
+    for (const FastOp& o : ops)  // the pass kernel runs pair ops only (the centre is folded)
+      require(o.kind != FK_DIAG, BF_ERR_ARG, "internal: centre op on the fast path");
     P.nops = (int)ops.size();
     const int nslot = 1 << d;
     int64_t off = 0;
@@ -570,14 +627,14 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
             blk(op.s + 1, tau, nu);  // output block at level l0 + s + 1
             const int l = P.l0 + op.s + 1;
             if (l <= lc) {  // W_l
-              const CT* Wb = H.W + G.w_off[l][G.idx(l, tau, nu)];
+              const CT* Wb = Wblk(l, G.idx(l, tau, nu));
               for (int st = 0; st < op.nsteps; ++st)
                 fill_step(rec(st), 0, st, [&](int i, int k) { return Wb[i + k * 16]; });
             } else {  // R_{l-1}, gather form
               const int lr_ = l - 1;
               const int part = (int)(tau & 1);
-              const CT* R0 = H.R + G.r_off[lr_][G.idx(lr_, tau >> 1, 2 * nu)];
-              const CT* R1 = H.R + G.r_off[lr_][G.idx(lr_, tau >> 1, 2 * nu + 1)];
+              const CT* R0 = Rblk(lr_, G.idx(lr_, tau >> 1, 2 * nu));
+              const CT* R1 = Rblk(lr_, G.idx(lr_, tau >> 1, 2 * nu + 1));
               for (int st = 0; st < op.nsteps; ++st)
                 fill_step(rec(st), 0, st, [&](int i, int k) {
                   const CT* Rs = k < 16 ? R0 : R1;
@@ -588,7 +645,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
             blk(op.s, tau, nu);
             const int l = P.l0 + op.s;
             if (l >= lc) {  // R^H_l: inputs (2tau + p, nu >> 1)
-              const CT* Rb = H.R + G.r_off[l][G.idx(l, tau, nu)];
+              const CT* Rb = Rblk(l, G.idx(l, tau, nu));
               for (int st = 0; st < op.nsteps; ++st)
                 fill_step(rec(st), 0, st, [&](int i, int k) {
                   const int pp = k >> 4;
@@ -596,8 +653,8 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
                 });
             } else {  // W^H_{l+1}: inputs (2tau + p, nu >> 1) at level l + 1, column part nu & 1
               const int lw = l + 1;
-              const CT* W0 = H.W + G.w_off[lw][G.idx(lw, 2 * tau, nu >> 1)];
-              const CT* W1 = H.W + G.w_off[lw][G.idx(lw, 2 * tau + 1, nu >> 1)];
+              const CT* W0 = Wblk(lw, G.idx(lw, 2 * tau, nu >> 1));
+              const CT* W1 = Wblk(lw, G.idx(lw, 2 * tau + 1, nu >> 1));
               const int cp = (int)(nu & 1);
               for (int st = 0; st < op.nsteps; ++st)
                 fill_step(rec(st), 0, st, [&](int i, int k) {
@@ -1028,6 +1085,7 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       FastArgs a{};
       a.p = P;
       a.diag = diag;
+      a.skew = getenv("BF_FAST_SKEW") ? atoi(getenv("BF_FAST_SKEW")) : 0;
       a.F = FP.F;
       a.Sin = buf[i % 2];
       a.Sout = buf[(i + 1) % 2];
