@@ -42,6 +42,9 @@ struct Task {
 struct Round {
   const Task* tasks;   // device
   const Term* terms;   // device
+  const int2* units;   // device: (task, 16-row group) work units of the tensor-core kernel
+  int32_t nunits;
+  int32_t pad0;
   int32_t ntasks;
   int32_t out_kind;    // 0 slab space, 1 user Y
   int32_t max_m;
@@ -64,10 +67,11 @@ struct StageArgs {
   void* Y;
   int64_t ldy;
   const int64_t* yperm;
+  const int2* units;
+  int32_t nunits;
   int32_t out_kind;
   int32_t conj_flip;
   int32_t nrhs;
-  int32_t pad;
 };
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);

@@ -5,15 +5,10 @@
 // P:318-354), forward or conjugate-transposed -- and every HOD-BF round is a
 // batch of independent small complex products
 //        out_task = sum_t A_t In_t            (A_t: m x k_t factor block or view)
-// described by Task / Term tables built once at create time (plan.cu).  The generic
-// kernel below runs one task x 32 right-hand sides per CTA:
-//   * lanes map to right-hand sides, so every slab read/write is a coalesced row of
-//     nrhs complex values (the slab space stores each slab rank x nrhs, nrhs fastest);
-//   * factor chunks and input chunks are staged in shared memory; factor entries are
-//     read back as warp-wide broadcasts;
-//   * user X / Y (column-major, leaf rows gathered / scattered through the tree
-//     permutation) are staged through shared memory so global accesses run along rows.
-#include "common.cuh"
+// described by Task / Term tables built once at create time (plan.cu).  This generic path
+// serves ragged ranks (kernel-compressed butterflies, HOD-BF, the distributed split); the
+// uniform rank-16 case has its own fused kernels (fast.cu, leaf.cu).
+#include "mma.cuh"
 
 namespace bfa {
 
@@ -37,114 +32,113 @@ __device__ __forceinline__ V vzero() {
 }
 
 // ------------------------------------------------------------------------------------
-// generic gather-sum product kernel
+// tensor-core gather-sum kernel (the same Task / Term tables): one warp per work unit =
+// (task, 16-row group) x 16 right-hand sides, 4M complex products on the tensor pipe
+// (mma.cuh policies: DMMA for complex128, 3xTF32 for complex64).  Operands are read straight
+// from global memory / L2 (factor blocks with arbitrary row / column strides and conjugation,
+// slab rows or permuted user rows), zero-padded outside the task's rows, the term's K and nrhs.
 // ------------------------------------------------------------------------------------
-template <typename V, int RPT>
-__global__ void __launch_bounds__(128) k_stage_generic(StageArgs a) {
-  using R = typename Scalar<V>::R;
-  constexpr int NT = 128, KC = 32, NR = 4 * RPT;
-  __shared__ V sA[KC][NR];
-  __shared__ V sIn[KC][33];
-  const Task t = a.tasks[blockIdx.x];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int j0 = blockIdx.y * 32;
-  const int jn = min(32, a.nrhs - j0);
-  const V* __restrict__ pool = static_cast<const V*>(a.pool);
-  const V* __restrict__ X = static_cast<const V*>(a.X);
-  V* __restrict__ S = static_cast<V*>(a.S);
-  V* __restrict__ Y = static_cast<V*>(a.Y);
+template <class Pol>
+__device__ __forceinline__ typename Pol::E ldA(const StageArgs& a, const Term& tm, int row, int k, int m, bool cj) {
+  using E = typename Pol::E;
+  E v{};
+  if (row < m && k < tm.k) {
+    v = __ldg(static_cast<const E*>(a.pool) + tm.a_off + (int64_t)row * tm.a_rs + (int64_t)k * tm.a_cs);
+    v.y = conj_im(v.y, cj);
+  }
+  return v;
+}
+template <class Pol>
+__device__ __forceinline__ typename Pol::E ldB(const StageArgs& a, const Term& tm, int k, int col) {
+  using E = typename Pol::E;
+  E v{};
+  if (k < tm.k && col < a.nrhs) {
+    const int64_t p = tm.in_row + k;
+    if (tm.in_kind == 0)
+      v = __ldg(static_cast<const E*>(a.S) + p * a.ldS + col);
+    else
+      v = __ldg(static_cast<const E*>(a.X) + (a.xperm ? a.xperm[p] : p) + (int64_t)col * a.ldx);
+  }
+  return v;
+}
 
-  for (int r0 = 0; r0 < t.m; r0 += NR) {
-    const int rn = min(NR, t.m - r0);
-    R ax[RPT], ay[RPT];
+// fill the fragments of k-step k0 (c128: DMMA m8n8k4 layout; c64: TF32 m16n8k8 layout)
+template <int NT>
+__device__ __forceinline__ void frags(PolC128<NT>& /*tag*/, typename PolC128<NT>::Frags& f, const StageArgs& a,
+                                      const Term& tm, int r0, int m, int k0, int j0, int g, int t, bool cj) {
+  using P = PolC128<NT>;
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) ax[q] = ay[q] = R(0);
-    for (int q = 0; q < t.nterm; ++q) {
-      const Term tm = a.terms[t.term0 + q];
-      const bool cj = (tm.conj != 0) != (a.conj_flip != 0);
-      for (int kc = 0; kc < tm.k; kc += KC) {
-        const int kn = min(KC, tm.k - kc);
-        __syncthreads();
-        if (tm.in_kind == 0) {
-          const V* src = S + (tm.in_row + kc) * a.ldS + j0;
-          for (int e = threadIdx.x; e < KC * 32; e += NT) {
-            const int kk = e >> 5, jj = e & 31;
-            sIn[kk][jj] = (kk < kn && jj < jn) ? src[(int64_t)kk * a.ldS + jj] : vzero<V>();
-          }
-        } else {
-          for (int e = threadIdx.x; e < KC * 32; e += NT) {
-            const int kk = e & 31, jj = e >> 5;
-            V v = vzero<V>();
-            if (kk < kn && jj < jn) {
-              const int64_t p = tm.in_row + kc + kk;
-              const int64_t row = a.xperm ? a.xperm[p] : p;
-              v = X[row + (int64_t)(j0 + jj) * a.ldx];
-            }
-            sIn[kk][jj] = v;
-          }
-        }
-        for (int e = threadIdx.x; e < KC * NR; e += NT) {
-          int ii, kk;
-          if (tm.a_rs == 1) {
-            ii = e % NR;
-            kk = e / NR;
-          } else {
-            kk = e % KC;
-            ii = e / KC;
-          }
-          V v = vzero<V>();
-          if (ii < rn && kk < kn) {
-            v = pool[tm.a_off + (int64_t)(r0 + ii) * tm.a_rs + (int64_t)(kc + kk) * tm.a_cs];
-            if (cj) v.y = -v.y;
-          }
-          sA[kk][ii] = v;
-        }
-        __syncthreads();
-        for (int kk = 0; kk < kn; ++kk) {
-          const V x = sIn[kk][lane];
+  for (int mi = 0; mi < 2; ++mi) {
+    f.a[mi] = ldA<P>(a, tm, r0 + 8 * mi + g, k0 + t, m, cj);
+    f.as[mi] = f.a[mi].x + f.a[mi].y;
+  }
 #pragma unroll
-          for (int q = 0; q < RPT; ++q) {
-            const V av = sA[kk][w * RPT + q];
-            ax[q] = fma(av.x, x.x, ax[q]);
-            ax[q] = fma(-av.y, x.y, ax[q]);
-            ay[q] = fma(av.x, x.y, ay[q]);
-            ay[q] = fma(av.y, x.x, ay[q]);
-          }
-        }
-      }
+  for (int ni = 0; ni < NT; ++ni) P::set_b(f, ni, ldB<P>(a, tm, k0 + t, j0 + 8 * ni + g));
+}
+template <int NT>
+__device__ __forceinline__ void frags(PolC64<NT>& /*tag*/, typename PolC64<NT>::Frags& f, const StageArgs& a,
+                                      const Term& tm, int r0, int m, int k0, int j0, int g, int t, bool cj) {
+  using P = PolC64<NT>;
+  float2 v[4];
+  v[0] = ldA<P>(a, tm, r0 + g, k0 + t, m, cj);
+  v[1] = ldA<P>(a, tm, r0 + g + 8, k0 + t, m, cj);
+  v[2] = ldA<P>(a, tm, r0 + g, k0 + t + 4, m, cj);
+  v[3] = ldA<P>(a, tm, r0 + g + 8, k0 + t + 4, m, cj);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    P::split(v[e].x, f.ah[0][e], f.al[0][e]);
+    P::split(v[e].y, f.ah[1][e], f.al[1][e]);
+    P::split(v[e].x + v[e].y, f.ah[2][e], f.al[2][e]);
+  }
+#pragma unroll
+  for (int ni = 0; ni < NT; ++ni) {
+    f.b[ni][0] = ldB<P>(a, tm, k0 + t, j0 + 8 * ni + g);
+    f.b[ni][1] = ldB<P>(a, tm, k0 + t + 4, j0 + 8 * ni + g);
+  }
+}
+
+template <class Pol>
+__global__ void __launch_bounds__(256, 2) k_stage_mma(StageArgs a) {
+  using E = typename Pol::E;
+  constexpr int KS = Pol::KS;
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (u >= a.nunits) return;
+  const int2 un = a.units[u];
+  const Task tk = a.tasks[un.x];
+  const int r0 = un.y * 16;
+  const int j0 = blockIdx.y * 8 * Pol::NT;
+  const int g = lane >> 2, t = lane & 3;
+  Pol tag;
+  typename Pol::Acc4 acc;  // 4M: exact on selection / identity factors
+  acc.zero();
+  for (int q = 0; q < tk.nterm; ++q) {
+    const Term tm = a.terms[tk.term0 + q];
+    const bool cj = (tm.conj != 0) != (a.conj_flip != 0);
+    typename Pol::Frags f[2];
+    frags(tag, f[0], a, tm, r0, tk.m, 0, j0, g, t, cj);
+    int k0 = 0;
+    for (; k0 + KS < tm.k; k0 += 2 * KS) {
+      frags(tag, f[1], a, tm, r0, tk.m, k0 + KS, j0, g, t, cj);
+      acc.mac(f[0]);
+      if (k0 + 2 * KS < tm.k) frags(tag, f[0], a, tm, r0, tk.m, k0 + 2 * KS, j0, g, t, cj);
+      acc.mac(f[1]);
     }
-    if (a.out_kind == 0) {
-      if (lane < jn) {
-#pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-          const int i = w * RPT + q;
-          if (i < rn) {
-            V v;
-            v.x = ax[q];
-            v.y = ay[q];
-            S[(t.out_row + r0 + i) * a.ldS + j0 + lane] = v;
-          }
-        }
+    if (k0 < tm.k) acc.mac(f[0]);
+  }
+  if (a.out_kind == 0) {
+    E* S = static_cast<E*>(a.S);
+    acc.each(g, t, [&](int r, int c, E v) {
+      if (r0 + r < tk.m && j0 + c < a.nrhs) S[(tk.out_row + r0 + r) * a.ldS + j0 + c] = v;
+    });
+  } else {
+    E* Y = static_cast<E*>(a.Y);
+    acc.each(g, t, [&](int r, int c, E v) {
+      if (r0 + r < tk.m && j0 + c < a.nrhs) {
+        const int64_t p = tk.out_row + r0 + r;
+        Y[(a.yperm ? a.yperm[p] : p) + (int64_t)(j0 + c) * a.ldy] = v;
       }
-    } else {
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < RPT; ++q) {
-        V v;
-        v.x = ax[q];
-        v.y = ay[q];
-        sIn[w * RPT + q][lane] = v;
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < NR * 32; e += NT) {
-        const int ii = e % NR, jj = e / NR;
-        if (ii < rn && jj < jn) {
-          const int64_t p = t.out_row + r0 + ii;
-          const int64_t row = a.yperm ? a.yperm[p] : p;
-          Y[row + (int64_t)(j0 + jj) * a.ldy] = sIn[ii][jj];
-        }
-      }
-    }
+    });
   }
 }
 
@@ -152,19 +146,20 @@ template <typename V>
 static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
   a.tasks = r.tasks;
   a.terms = r.terms;
+  a.units = r.units;
+  a.nunits = r.nunits;
   a.out_kind = r.out_kind;
-  dim3 grid(r.ntasks, (a.nrhs + 31) / 32);
-  if (r.max_m <= 16)
-    k_stage_generic<V, 4><<<grid, 128, 0, st>>>(a);
+  dim3 grid((r.nunits + 7) / 8, (a.nrhs + 15) / 16);  // warp tile: 16 rows x 16 columns
+  if (sizeof(V) == 16)
+    k_stage_mma<PolC128<2>><<<grid, 256, 0, st>>>(a);
   else
-    k_stage_generic<V, 8><<<grid, 128, 0, st>>>(a);
+    k_stage_mma<PolC64<2>><<<grid, 256, 0, st>>>(a);
 }
 
 const char* round_kernel_name(int dtype, const Round& r, int* id) {
-  const bool big = r.max_m > 16;
-  if (id) *id = big ? 2 : 1;
-  if (dtype == BF_C128) return big ? "k_stage_generic<double2,8>" : "k_stage_generic<double2,4>";
-  return big ? "k_stage_generic<float2,8>" : "k_stage_generic<float2,4>";
+  (void)r;
+  if (id) *id = 3;
+  return dtype == BF_C128 ? "k_stage_mma<c128>" : "k_stage_mma<c64>";
 }
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st) {

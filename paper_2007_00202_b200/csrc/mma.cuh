@@ -196,6 +196,40 @@ struct PolC128 {
           }
     }
   };
+  // 4M product (4 real MMAs per complex MMA, no 3M sums): re += ar br + (-ai) bi,
+  // im += ar bi + ai br.  Exact whenever the factor entries are 0 / +-1 / +-i (selection
+  // blocks, identity pins), which the 3M combination is not.
+  struct Acc4 {
+    double p[2][2][NT][2];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) p[q][mi][ni][0] = p[q][mi][ni][1] = 0.0;
+    }
+    __device__ __forceinline__ void mac(const Frags& f) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) {
+          mma(p[0][mi][ni][0], p[0][mi][ni][1], f.a[mi].x, f.b[ni].x);
+          mma(p[0][mi][ni][0], p[0][mi][ni][1], -f.a[mi].y, f.b[ni].y);
+          mma(p[1][mi][ni][0], p[1][mi][ni][1], f.a[mi].x, f.b[ni].y);
+          mma(p[1][mi][ni][0], p[1][mi][ni][1], f.a[mi].y, f.b[ni].x);
+        }
+    }
+    template <typename Fn>
+    __device__ __forceinline__ void each(int g, int t, Fn fn) const {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) fn(8 * mi + g, 8 * ni + 2 * t + e, make_double2(p[0][mi][ni][e], p[1][mi][ni][e]));
+    }
+  };
 };
 
 // ======================================================================================
@@ -316,6 +350,56 @@ struct PolC64 {
           const float p1 = p[0][ni][e], p2 = p[1][ni][e], p3 = p[2][ni][e];
           fn(g + 8 * (e >> 1), 8 * ni + 2 * t + (e & 1), make_float2(p1 - p2, p3 - p1 - p2));
         }
+    }
+  };
+  // 4M product on the 3xTF32 split (see PolC128::Acc4); uses f.ah/al[0] (re) and [1] (im) only
+  struct Acc4 {
+    float p[2][NT][4];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) p[q][ni][e] = 0.f;
+    }
+    __device__ __forceinline__ void mac(const Frags& f) {
+      uint32_t nh[4], nl[4];  // -ai (sign flip is exact on both split parts)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        nh[e] = f.ah[1][e] ^ 0x80000000u;
+        nl[e] = f.al[1][e] ^ 0x80000000u;
+      }
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) {
+        uint32_t bh[2][2], bl[2][2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          split(f.b[ni][e].x, bh[0][e], bl[0][e]);
+          split(f.b[ni][e].y, bh[1][e], bl[1][e]);
+        }
+        // re += ar br - ai bi
+        mma(p[0][ni], f.ah[0], bl[0]);
+        mma(p[0][ni], f.al[0], bh[0]);
+        mma(p[0][ni], f.ah[0], bh[0]);
+        mma(p[0][ni], nh, bl[1]);
+        mma(p[0][ni], nl, bh[1]);
+        mma(p[0][ni], nh, bh[1]);
+        // im += ar bi + ai br
+        mma(p[1][ni], f.ah[0], bl[1]);
+        mma(p[1][ni], f.al[0], bh[1]);
+        mma(p[1][ni], f.ah[0], bh[1]);
+        mma(p[1][ni], f.ah[1], bl[0]);
+        mma(p[1][ni], f.al[1], bh[0]);
+        mma(p[1][ni], f.ah[1], bh[0]);
+      }
+    }
+    template <typename Fn>
+    __device__ __forceinline__ void each(int g, int t, Fn fn) const {
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) fn(g + 8 * (e >> 1), 8 * ni + 2 * t + (e & 1), make_float2(p[0][ni][e], p[1][ni][e]));
     }
   };
 };

@@ -691,7 +691,8 @@ struct Plan {
 
 static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, size_t* bytes) {
   size_t tot = 0;
-  std::vector<size_t> toff, xoff;
+  std::vector<size_t> toff, xoff, uoff;
+  std::vector<std::vector<int2>> units;
   for (int r = round_lo; r < round_hi && r < (int)pb.tasks.size(); ++r) {
     toff.push_back(tot);
     tot += pb.tasks[r].size() * sizeof(Task);
@@ -699,6 +700,14 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
     xoff.push_back(tot);
     tot += pb.terms[r].size() * sizeof(Term);
     tot = (tot + 255) & ~size_t(255);
+    // work units of the tensor-core stage kernel: one per (task, 16-row group)
+    std::vector<int2> u;
+    for (size_t ti = 0; ti < pb.tasks[r].size(); ++ti)
+      for (int rg = 0; rg * 16 < pb.tasks[r][ti].m; ++rg) u.push_back(make_int2((int)ti, rg));
+    uoff.push_back(tot);
+    tot += u.size() * sizeof(int2);
+    tot = (tot + 255) & ~size_t(255);
+    units.push_back(std::move(u));
   }
   if (tot == 0) return;
   std::vector<char> host(tot);
@@ -706,6 +715,7 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
   for (int r = round_lo, q = 0; r < round_hi && r < (int)pb.tasks.size(); ++r, ++q) {
     if (!pb.tasks[r].empty()) memcpy(host.data() + toff[q], pb.tasks[r].data(), pb.tasks[r].size() * sizeof(Task));
     if (!pb.terms[r].empty()) memcpy(host.data() + xoff[q], pb.terms[r].data(), pb.terms[r].size() * sizeof(Term));
+    if (!units[q].empty()) memcpy(host.data() + uoff[q], units[q].data(), units[q].size() * sizeof(int2));
   }
   if (tot) {
     BF_CK(cudaMalloc(&P.dev, tot));
@@ -716,6 +726,8 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
     Round R{};
     R.tasks = reinterpret_cast<const Task*>((char*)P.dev + toff[q]);
     R.terms = reinterpret_cast<const Term*>((char*)P.dev + xoff[q]);
+    R.units = reinterpret_cast<const int2*>((char*)P.dev + uoff[q]);
+    R.nunits = (int32_t)units[q].size();
     R.ntasks = (int32_t)pb.tasks[r].size();
     R.out_kind = pb.okind[r] < 0 ? 0 : pb.okind[r];
     int mm = 0, mk_ = 0;
