@@ -179,6 +179,13 @@ int bf_dist_layout(bf_handle h, int op, int64_t nrhs, size_t* work_bytes, size_t
  * query only the counts. */
 int bf_dist_exchange_blocks(bf_handle h, int op, int64_t* n_send, int64_t* send_blocks, int64_t* n_recv,
                             int64_t* recv_blocks);
+/* Element layout of the send / recv regions.  0: every centre block occupies rank x nrhs
+ * consecutive elements (row-major, nrhs fastest) in bf_dist_exchange_blocks order.  1 (uniform
+ * rank-16 butterflies, fused kernels): each peer's chunk is [rhs tile of 32][column half of 16]
+ * [block, in bf_dist_exchange_blocks order][16 rows][16 columns], the 16 x 16 half slab stored
+ * with the kernels' bank swizzle (element (r, c) at r*16 + (c ^ swz(r))); nrhs is padded to a
+ * multiple of 32.  Either way the regions are moved as opaque bytes by the all-to-all. */
+int bf_dist_slab_format(bf_handle h, int32_t* fmt);
 int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out,
                        int64_t* user_off_in, int64_t* user_off_out);
 int bf_dist_apply_pre(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx,

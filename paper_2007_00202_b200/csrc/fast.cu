@@ -60,7 +60,7 @@ struct Stream {
       r -= np;
     }
     const int s0 = r * SPP, nst = min(SPP, P.ops[q].nsteps - s0);
-    const int64_t w = item & ((int64_t(1) << (P.L - P.d)) - 1);
+    const int64_t w = item & (P.nwin - 1);  // local window index (records of this rank only)
     const unsigned char* src =
         static_cast<const unsigned char*>(A.F) + P.fbase + w * P.win_bytes + P.ops[q].off + (int64_t)s0 * S * FAST_FRAG;
     const int slot = (int)(j % Cfg::NP);
@@ -72,15 +72,21 @@ struct Stream {
     const FastPass& P = A.p;
     const int64_t item = item_of(i);
     if (item >= nitems) return;
-    const int nwin_log = P.L - P.d;
-    const int64_t w = item & ((int64_t(1) << nwin_log) - 1), jt = item >> nwin_log;
-    const int64_t a = w >> P.bbits, b = w & ((int64_t(1) << P.bbits) - 1);
+    const int64_t w = item & (P.nwin - 1), jt = item >> (P.a_log + P.b_log);
+    const int64_t a = P.a_lo + (w >> P.b_log), b = P.b_lo + (w & ((int64_t(1) << P.b_log) - 1));
     const uint32_t bytes = (uint32_t)(S * FAST_HSLAB * sizeof(E));
-    const int64_t idx = slab_index(P, a, b, P.in_s, 0);
     mbar_expect_tx(winF, 2 * bytes);
-    for (int h = 0; h < 2; ++h)
-      bulk_g2s(winbuf + wb * Cfg::WIN + h * Cfg::WINH, static_cast<const E*>(A.Sin) + half_slab_off(jt, h, A.nlev, idx),
-               bytes, winF);
+    const E* Sin = static_cast<const E*>(A.Sin);
+    for (int h = 0; h < 2; ++h) {
+      E* dst = winbuf + wb * Cfg::WIN + h * Cfg::WINH;
+      if (!P.xin) {  // the window's input slabs are contiguous in the slab buffer
+        bulk_g2s(dst, Sin + pass_slab_off(P, 0, jt, h, A.nlev, A.ntiles, a, b, P.in_s, 0), bytes, winF);
+      } else {       // exchange layout: the slabs may come from several peers' chunks
+        for (int o = 0; o < S; ++o)
+          bulk_g2s(dst + o * FAST_HSLAB, Sin + pass_slab_off(P, P.xin, jt, h, A.nlev, A.ntiles, a, b, P.in_s, o),
+                   (uint32_t)(FAST_HSLAB * sizeof(E)), winF);
+      }
+    }
   }
 };
 
@@ -114,8 +120,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   St str{A, ring, winbuf, full, winF, P.nwin * ((A.nrhs + FAST_NB - 1) / FAST_NB), 0};
   for (int q = 0; q < P.nops; ++q) str.ppi += (P.ops[q].nsteps + SPP - 1) / SPP;
   const int64_t nitems = str.nitems;
-  const int nwin_log = P.L - P.d;
-  const int64_t bmask = (int64_t(1) << P.bbits) - 1;
+  const int nwin_log = P.a_log + P.b_log;
+  const int64_t bmask = (int64_t(1) << P.b_log) - 1;
 
   if (threadIdx.x == 0) {
     mbar_init(winF, 1);
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   int cur = 0;    // window buffer holding the current item's input
   for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++i) {
     const int64_t w = item & ((int64_t(1) << nwin_log) - 1), jt = item >> nwin_log;
-    const int64_t a = w >> P.bbits, b = w & bmask;
+    const int64_t a = P.a_lo + (w >> P.b_log), b = P.b_lo + (w & bmask);
     if (!(diag & 1)) mbar_wait(winF, (uint32_t)(i & 1), 3);
     int rd = cur;  // op q reads buffer rd, writes rd ^ 1
     for (int q = 0; q < P.nops; ++q) {
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
       }
       if (last) {
         if (!(diag & 2)) {
-          E* dst = Sout + half_slab_off(jt, half, A.nlev, slab_index(P, a, b, P.out_s, o));
+          E* dst = Sout + pass_slab_off(P, P.xout, jt, half, A.nlev, A.ntiles, a, b, P.out_s, o);
           acc.each(g, t, [&](int r, int c, E v) { dst[r * FAST_HC + ((c0w + c) ^ Pol::swz(r))] = v; });
         }
         cur = rd ^ 1;

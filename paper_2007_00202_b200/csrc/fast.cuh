@@ -52,9 +52,14 @@ struct FastOp {
 struct FastPass {
   int32_t d, L, l0, bbits;  // window levels, tree depth, first level, log2(#b values) = L - l1
   int32_t nops, in_s, out_s, leaf;  // leaf: 0 window pass, 1 leaf-in launch, 2 leaf-out launch
-  int32_t numaj, pad;               // HBM slab order: 0 tau-major (op N), 1 nu-major (op C / T)
+  int32_t numaj, xin;               // HBM slab order: 0 tau-major (op N), 1 nu-major (op C / T);
+                                    // xin / xout: 0 slab buffer, 1 / 2 exchange layout whose
+  int32_t xout, pad;                // peer is the owner of tau / of nu (multi-GPU split)
+  int32_t a_log, b_log;  // the pass's windows: a = a_lo + (w >> b_log), b = b_lo + (w & (2^b_log - 1))
+  int32_t wt_log, wn_log;  // exchange: centre tau / nu per peer = 2^(lc - p) / 2^(L - lc - p)
+  int64_t a_lo, b_lo;
   int64_t fbase, win_bytes;  // byte offset of window 0's record, bytes per window record
-  int64_t nwin;
+  int64_t nwin;              // 2^(a_log + b_log)
   int64_t factor_entries, user_in, user_out;  // accounting
   FastOp ops[FAST_MAXOPS];
 };
@@ -66,6 +71,7 @@ struct FastArgs {
   void* Sout;
   int64_t nlev;  // slabs per level (2^L)
   int32_t nrhs;
+  int32_t ntiles;  // 32-column rhs tiles (exchange layout stride)
   int32_t skew;  // ns the second column half starts late (tuning knob, env BF_FAST_SKEW)
   int32_t diag;  // profiling only (env BF_FAST_DIAG, results are garbage): bit 0 = no operand
                  // streaming (compute only), bit 1 = output slabs not written to HBM, bit 2 = no
@@ -86,6 +92,7 @@ struct LeafArgs {
   const void* Sin;       // mode 1: slabs read
   void* Sout;            // mode 0: slabs written
   int64_t nleaf, nlev;
+  int64_t leaf_lo;       // global index of local leaf 0 (its slab index); X / Y rows are local
   int32_t leaf, nsteps;  // leaf size, k-steps per leaf record
   int32_t nrhs, conj_io; // conj_io: op T conjugates X on load and Y on store
   int32_t mode, tma;     // mode 0 = IN, 1 = OUT; tma: X rows by 2-D TMA (contiguous leaves)
@@ -127,6 +134,23 @@ __host__ __device__ inline int64_t slab_index(const FastPass& P, int64_t a, int6
   const int64_t tau = (a << s) + (slot >> ds);
   const int64_t nu = (b << ds) + (slot & ((1 << ds) - 1));
   return P.numaj ? (nu << l) + tau : (tau << (P.L - l)) + nu;
+}
+
+// element offset of the half slab (jt, half) of window (a, b)'s slot at window level s, in
+// the slab buffer (mode 0) or in the exchange layout of the centre level (mode 1 / 2: peer =
+// owner of tau / of nu): [peer][jt][half][tau_l][nu_l] for op N, [peer][jt][half][nu_l][tau_l]
+// for op C, so the 2^d slabs a receiving window reads are contiguous again.
+__host__ __device__ inline int64_t pass_slab_off(const FastPass& P, int mode, int64_t jt, int half, int64_t nlev,
+                                                 int64_t ntiles, int64_t a, int64_t b, int s, int slot) {
+  if (mode == 0) return half_slab_off(jt, half, nlev, slab_index(P, a, b, s, slot));
+  const int ds = P.d - s;
+  const int64_t tau = (a << s) + (slot >> ds);
+  const int64_t nu = (b << ds) + (slot & ((1 << ds) - 1));
+  const int64_t wt = int64_t(1) << P.wt_log, wn = int64_t(1) << P.wn_log;
+  const int64_t tl = tau & (wt - 1), nl = nu & (wn - 1);
+  const int64_t peer = mode == 1 ? (tau >> P.wt_log) : (nu >> P.wn_log);
+  const int64_t inner = P.numaj ? nl * wt + tl : tl * wn + nl;
+  return (((peer * ntiles + jt) * 2 + half) * (wt * wn) + inner) * FAST_HSLAB;
 }
 
 }  // namespace bfa

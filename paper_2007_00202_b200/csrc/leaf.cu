@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
     }
     if (MODE == 1)
       for (int hh = 0; hh < 2; ++hh)
-        bulk_g2s(sb + a_chunk + hh * FAST_HSLAB * sizeof(E), static_cast<const E*>(A.Sin) + half_slab_off(jt, hh, A.nlev, leaf),
+        bulk_g2s(sb + a_chunk + hh * FAST_HSLAB * sizeof(E),
+                 static_cast<const E*>(A.Sin) + half_slab_off(jt, hh, A.nlev, A.leaf_lo + leaf),
                  (uint32_t)(FAST_HSLAB * sizeof(E)), &myfull[st]);
   };
   if (lane == 0) {
@@ -140,8 +141,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
       if (lane == 0) issue(c + dep);
     }
     if (MODE == 0) {
-      E* dst0 = static_cast<E*>(A.Sout) + half_slab_off(jt, 0, A.nlev, leaf);
-      E* dst1 = static_cast<E*>(A.Sout) + half_slab_off(jt, 1, A.nlev, leaf);
+      E* dst0 = static_cast<E*>(A.Sout) + half_slab_off(jt, 0, A.nlev, A.leaf_lo + leaf);
+      E* dst1 = static_cast<E*>(A.Sout) + half_slab_off(jt, 1, A.nlev, A.leaf_lo + leaf);
       acc.each(g, t, [&](int r, int cc, E v) {
         (cc < FAST_HC ? dst0 : dst1)[r * FAST_HC + ((cc & (FAST_HC - 1)) ^ Pol::swz(r))] = v;
       });

@@ -20,6 +20,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -374,6 +375,7 @@ struct FastPlan {
   int64_t entries = 0;
   bool contig_in = false;   // every leaf the IN launch reads is a run of consecutive user rows
   bool contig_out = false;  // ... and every leaf the OUT launch writes
+  int split = -1;           // multi-GPU split: passes [0, split) before the exchange, the rest after
 };
 
 static bool fast_eligible(const Geom& G, int dtype) {
@@ -439,12 +441,31 @@ static void fill_step(CT* dst, int mg, int ki, Fn A) {
 
 // op 0 = N (forward), 1 = C (adjoint; conjugate-transposed factor views)
 template <typename CT>
-static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, int opk, size_t* acct) {
+static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, int opk, size_t* acct,
+                       int dp = -1, int dg = 0) {
+  // dp >= 0: rank dg's share of the split over 2^dp GPUs: the W side (levels
+  // 0..lc, leaves of T_S) restricted to the column subtree dg at level dp, the R side (levels
+  // lc..L, leaves of T_O) to the row subtree dg; the pass that ends at the centre level writes
+  // the exchange layout and the pass that starts there reads it.
   const int L = G.L, lc = G.lc;
+  const bool split = dp >= 0;
   const int ks = fast_ks((int)sizeof(CT));
-  const int np = (L + FAST_DMAX - 1) / FAST_DMAX;
-  std::vector<int> lv(np + 1, 0);
-  for (int p = 0; p < np; ++p) lv[p + 1] = lv[p] + L / np + (p < L % np ? 1 : 0);
+  std::vector<int> lv;  // level boundaries of the window passes
+  auto chunk = [&](int lo, int hi) {  // split [lo, hi] into near-equal passes of <= FAST_DMAX levels
+    const int n = hi - lo, k = (n + FAST_DMAX - 1) / FAST_DMAX;
+    for (int p = 0, at = lo; p < k; ++p) {
+      at += n / k + (p < n % k ? 1 : 0);
+      lv.push_back(at);
+    }
+  };
+  lv.push_back(0);
+  if (split) {
+    chunk(0, lc);
+    chunk(lc, L);
+  } else {
+    chunk(0, L);
+  }
+  const int np = (int)lv.size() - 1;
   const int lr = (int)G.mt(0), lcn = (int)G.nv(0);
   const bool adj = opk == 1;
   // The centre factor B^{lc} is folded into its neighbour at create time: R'_{tau,nu} = R_{tau,nu}
@@ -518,6 +539,11 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       ops.push_back(o);
     };
     int d = 0;
+    P.xin = P.xout = 0;
+    if (split) {
+      P.wt_log = lc - dp;
+      P.wn_log = L - lc - dp;
+    }
     if (k == 0 || k == np + 1) {
       // leaf launch (d = 0): window w = one leaf at level 0 (T_S leaf nu = b) or L (T_O leaf tau = a)
       const bool in = k == 0;
@@ -526,7 +552,19 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       P.l0 = at0 ? 0 : L;
       P.d = 0;
       P.bbits = L - P.l0;
-      P.nwin = int64_t(1) << L;
+      const int loc = L - (split ? dp : 0);  // log2 of this rank's leaves
+      const int64_t lo = split ? int64_t(dg) << loc : 0;
+      if (at0) {
+        P.a_log = 0;
+        P.a_lo = 0;
+        P.b_log = loc;
+        P.b_lo = lo;
+      } else {
+        P.a_log = loc;
+        P.a_lo = lo;
+        P.b_log = 0;
+        P.b_lo = 0;
+      }
       add(in ? FK_LEAF_IN : FK_LEAF_OUT, 0, at0 ? lcn : lr);
       P.in_s = in ? -1 : 0;
       P.out_s = in ? 0 : -1;
@@ -537,22 +575,36 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       const int l0 = P.l0, l1 = lv[p + 1];
       d = P.d;
       P.bbits = L - l1;
-      P.nwin = int64_t(1) << (L - d);
-      const bool hasB = false;  // folded into R^{lc} / W^{lc} (above)
+      // windows: a over T_O level l0, b over T_S level L - l1 (restricted on a split)
+      P.a_log = l0;
+      P.a_lo = 0;
+      P.b_log = L - l1;
+      P.b_lo = 0;
+      if (split && l1 <= lc) {  // W side: column subtree dg
+        P.b_log = L - l1 - dp;
+        P.b_lo = int64_t(dg) << P.b_log;
+      } else if (split) {  // R side: row subtree dg
+        P.a_log = l0 - dp;
+        P.a_lo = int64_t(dg) << P.a_log;
+      }
       if (!adj) {
         for (int l = l0 + 1; l <= l1 && l <= lc; ++l) add(FK_PAIR_DOWN, l - 1 - l0, 0);  // W_l
-        if (hasB) add(FK_DIAG, lc - l0, 0);
         for (int l = std::max(l0, lc); l < l1; ++l) add(FK_PAIR_DOWN, l - l0, 0);      // R_l
         P.in_s = 0;
         P.out_s = d;
+        if (split && l1 == lc) P.xout = 1;  // send z^lc to the owner of tau
+        if (split && l0 == lc) P.xin = 2;   // receive from the owner of nu
       } else {
         for (int l = l1 - 1; l >= l0 && l >= lc; --l) add(FK_PAIR_UP, l - l0, 0);        // R^H_l
-        if (hasB) add(FK_DIAG, lc - l0, 0);                                              // B^H
         for (int l = std::min(l1, lc); l >= l0 + 1; --l) add(FK_PAIR_UP, l - 1 - l0, 0); // W^H_l
         P.in_s = d;
         P.out_s = 0;
+        if (split && l0 == lc) P.xout = 2;  // send to the owner of nu
+        if (split && l1 == lc) P.xin = 1;   // receive from the owner of tau
       }
+      if (P.xout || P.xin) FP.split = (int)passes.size() + (P.xout ? 1 : 0);
     }
+    P.nwin = int64_t(1) << (P.a_log + P.b_log);
     require((int)ops.size() <= FAST_MAXOPS, BF_ERR_ARG, "internal: too many ops in a pass");
     for (const FastOp& o : ops)  // the pass kernel runs pair ops only (the centre is folded)
       require(o.kind != FK_DIAG, BF_ERR_ARG, "internal: centre op on the fast path");
@@ -570,8 +622,8 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     P.factor_entries = off / (int64_t)sizeof(CT) * P.nwin;
     total += off * P.nwin;
     for (int q = 0; q < P.nops; ++q) {
-      if (ops[q].kind == FK_LEAF_IN) P.user_in = (adj ? G.m : G.n);
-      if (ops[q].kind == FK_LEAF_OUT) P.user_out = (adj ? G.n : G.m);
+      if (ops[q].kind == FK_LEAF_IN) P.user_in = P.nwin * ops[q].leaf;
+      if (ops[q].kind == FK_LEAF_OUT) P.user_out = P.nwin * ops[q].leaf;
     }
     passes.push_back(P);
   }
@@ -580,7 +632,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   for (const FastPass& P : passes) {
     const int d = P.d, nslot = 1 << d;
     for (int64_t w = 0; w < P.nwin; ++w) {
-      const int64_t a = w >> P.bbits, b = w & ((int64_t(1) << P.bbits) - 1);
+      const int64_t a = P.a_lo + (w >> P.b_log), b = P.b_lo + (w & ((int64_t(1) << P.b_log) - 1));
       for (int q = 0; q < P.nops; ++q) {
         const FastOp& op = P.ops[q];
         CT* base = host.data() + (P.fbase + w * P.win_bytes + op.off) / (int64_t)sizeof(CT);
@@ -669,7 +721,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   }
   FP.passes = std::move(passes);
   FP.entries = total / (int64_t)sizeof(CT);
-  if (total) {
+  if (total && !g_host_only) {
     BF_CK(cudaMalloc(&FP.F, (size_t)total));
     BF_CK(cudaMemcpy(FP.F, host.data(), (size_t)total, cudaMemcpyHostToDevice));
     *acct += (size_t)total;
@@ -1030,7 +1082,7 @@ int bf_info(bf_handle h, bf_info_t* info) {
   if (!h || !info) return fail(Err{BF_ERR_ARG, "NULL argument"});
   info->factor_entries = h->factor_entries;
   info->device_bytes = (int64_t)h->device_bytes;
-  if (h->dist) {
+  if (h->dist && !h->use_fast) {
     info->launches_n = h->pre[0].launches() + h->post[0].launches();
     info->launches_c = h->pre[1].launches() + h->post[1].launches();
   } else if (h->use_fast) {
@@ -1045,10 +1097,19 @@ int bf_info(bf_handle h, bf_info_t* info) {
   return BF_OK;
 }
 
+// fast-path workspace: two slab buffers (every slab of a level, [tile][half][slab][16 x 16]) and,
+// on a split handle, the send and recv regions of the centre exchange (2^L / P slabs each)
+static size_t fast_buf_bytes(bf_handle h, int64_t nrhs) {
+  const size_t tiles = (size_t)((nrhs + FAST_NB - 1) / FAST_NB);
+  return align256((size_t)h->G.nb * tiles * FAST_SLAB * csize(h->dtype));
+}
+static size_t fast_x_bytes(bf_handle h, int64_t nrhs) {
+  if (!h->dist) return 0;
+  return align256(fast_buf_bytes(h, nrhs) / (size_t)h->nranks);
+}
 static size_t fast_ws(bf_handle h, int64_t nrhs) {
   if (!h->use_fast) return 0;
-  const size_t tiles = (size_t)((nrhs + FAST_NB - 1) / FAST_NB);
-  return 2 * align256((size_t)h->G.nb * tiles * FAST_SLAB * csize(h->dtype));
+  return 2 * fast_buf_bytes(h, nrhs) + 2 * fast_x_bytes(h, nrhs);
 }
 
 int bf_workspace_size(bf_handle h, int64_t nrhs, size_t* bytes) {
@@ -1060,30 +1121,37 @@ int bf_workspace_size(bf_handle h, int64_t nrhs, size_t* bytes) {
   return BF_OK;
 }
 
+// launches [lo, hi) of the fast plan of op slot k.  Workspace: two slab buffers, then (split
+// handles only) the send and the recv region of the centre exchange.
 static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                     void* work, cudaStream_t st, void* const* ev, int nev) {
+                     void* work, cudaStream_t st, void* const* ev, int nev, int lo = 0, int hi = -1) {
   const FastPlan& FP = h->fast[k];
-  if (ev) require(nev >= (int)FP.passes.size() + 1, BF_ERR_ARG, "need nrounds + 1 events");
-  const size_t half = fast_ws(h, nrhs) / 2;
-  char* buf[2] = {static_cast<char*>(work), static_cast<char*>(work) + half};
+  if (hi < 0) hi = (int)FP.passes.size();
+  if (ev) require(nev >= hi - lo + 1, BF_ERR_ARG, "need nrounds + 1 events");
+  const size_t bufb = fast_buf_bytes(h, nrhs), xb = fast_x_bytes(h, nrhs);
+  char* buf[2] = {static_cast<char*>(work), static_cast<char*>(work) + bufb};
+  char* sendb = static_cast<char*>(work) + 2 * bufb;
+  char* recvb = sendb + xb;
   const bool fwd = k == 0;
   const int diag = getenv("BF_FAST_DIAG") ? atoi(getenv("BF_FAST_DIAG")) : 0;
-  for (size_t i = 0; i < FP.passes.size(); ++i) {
+  const int32_t ntiles = (int32_t)((nrhs + FAST_NB - 1) / FAST_NB);
+  for (int i = lo; i < hi; ++i) {
     const FastPass& P = FP.passes[i];
-    if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), st));
+    if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[i - lo]), st));
     if (P.leaf) {
       LeafArgs a{};
       a.mode = P.leaf == 1 ? 0 : 1;
       a.F = static_cast<const char*>(FP.F) + P.fbase;
       a.X = X;
       a.ldx = ldx;
-      a.xperm = fwd ? h->d_cperm : h->d_rperm;
+      a.xperm = h->dist ? h->d_lperm_in[k] : fwd ? h->d_cperm : h->d_rperm;
       a.Y = Y;
       a.ldy = ldy;
-      a.yperm = fwd ? h->d_rperm : h->d_cperm;
+      a.yperm = h->dist ? h->d_lperm_out[k] : fwd ? h->d_rperm : h->d_cperm;
       a.Sin = buf[i % 2];
       a.Sout = buf[(i + 1) % 2];
       a.nleaf = P.nwin;
+      a.leaf_lo = P.a_lo + P.b_lo;  // one of them is 0 (d = 0 windows)
       a.nlev = h->G.nb;
       a.leaf = P.ops[0].leaf;
       a.nsteps = P.ops[0].nsteps;
@@ -1099,10 +1167,11 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       a.diag = diag;
       a.skew = getenv("BF_FAST_SKEW") ? atoi(getenv("BF_FAST_SKEW")) : 0;
       a.F = FP.F;
-      a.Sin = buf[i % 2];
-      a.Sout = buf[(i + 1) % 2];
+      a.Sin = P.xin ? recvb : buf[i % 2];
+      a.Sout = P.xout ? sendb : buf[(i + 1) % 2];
       a.nlev = h->G.nb;
       a.nrhs = (int32_t)nrhs;
+      a.ntiles = ntiles;
       launch_fast_pass(h->dtype, a, st);
     }
     if (getenv("BF_DEBUG_SYNC")) {
@@ -1112,7 +1181,7 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       BF_CK(e);
     }
   }
-  if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[FP.passes.size()]), st));
+  if (ev) BF_CK(cudaEventRecord(static_cast<cudaEvent_t>(ev[hi - lo]), st));
   BF_CK(cudaGetLastError());
 }
 
@@ -1168,7 +1237,7 @@ int bf_apply_op(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, v
 int bf_rounds(bf_handle h, int op, int32_t* n) {
   if (!h || !n) return fail(Err{BF_ERR_ARG, "NULL argument"});
   const int k = op == BF_OP_N ? 0 : 1;
-  if (h->use_fast && !h->dist)
+  if (h->use_fast)
     *n = (int32_t)h->fast[k].passes.size();
   else
     *n = h->dist ? (int32_t)(h->pre[k].rounds.size() + h->post[k].rounds.size()) : (int32_t)h->plan[k].rounds.size();
@@ -1179,7 +1248,7 @@ int bf_round_info(bf_handle h, int op, int32_t round, bf_round_info_t* info) {
   if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
   try {
     const int k = op == BF_OP_N ? 0 : 1;
-    if (h->use_fast && !h->dist) {
+    if (h->use_fast) {
       require(info && round >= 0 && round < (int)h->fast[k].passes.size(), BF_ERR_ARG, "round out of range");
       const FastPass& P = h->fast[k].passes[round];
       memset(info, 0, sizeof(*info));
@@ -1668,6 +1737,7 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
     own.g = rank;
     std::vector<char> host;
     FBase F;
+    const Geom G0 = G;  // canonical offsets (local_pool rewrites G's to the rank-local pool)
     local_pool(*d, G, own, host, F, cs);
     h->factor_entries = (int64_t)(host.size() / cs);
     if (!host.empty()) h->pool = upload(host.data(), host.size(), &h->device_bytes);
@@ -1775,6 +1845,31 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
       }
     }
     h->slab_rows = max_rows;
+    // fused fast path for uniform rank-16 butterflies: the same split with the window-pass and
+    // leaf kernels; the generic plans above remain the fallback
+    if (fast_eligible(G0, d->dtype) && G0.lc >= 1 && G0.L - G0.lc >= 1 && !getenv("BF_DISABLE_FAST")) {
+      auto build = [&](auto* tag) {
+        using CT = std::remove_pointer_t<decltype(tag)>;
+        HostFactors<CT> HF{static_cast<const CT*>(d->U), static_cast<const CT*>(d->R), static_cast<const CT*>(d->B),
+                           static_cast<const CT*>(d->W), static_cast<const CT*>(d->Vt)};
+        for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G0, HF, k, &h->device_bytes, p, rank);
+      };
+      if (d->dtype == BF_C128) build((double2*)nullptr);
+      else build((float2*)nullptr);
+      const bool ok = true;
+      if (ok) {
+        h->use_fast = true;
+        h->fast[0].contig_in = leaves_contiguous(lpc.empty() ? nullptr : lpc.data(), cs1 - cs0, G0.nv(0));
+        h->fast[0].contig_out = leaves_contiguous(lpr.empty() ? nullptr : lpr.data(), rs1 - rs0, G0.mt(0));
+        h->fast[1].contig_in = h->fast[0].contig_out;
+        h->fast[1].contig_out = h->fast[0].contig_in;
+      } else {
+        for (int k = 0; k < 2; ++k) {
+          if (h->fast[k].F) cudaFree(h->fast[k].F);
+          h->fast[k] = FastPlan{};
+        }
+      }
+    }
     h->G = std::move(G);
     *out = h.release();
     return BF_OK;
@@ -1790,6 +1885,20 @@ int bf_dist_layout(bf_handle h, int op, int64_t nrhs, size_t* work_bytes, size_t
   if (!h || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
   if (!h->dist) return fail(Err{BF_ERR_ARG, "not a distributed handle"});
   const int k = op == BF_OP_N ? 0 : 1;
+  if (h->use_fast) {
+    // fast format: per peer [tile][half][block][16 x 16] (bf_dist_slab_format), equal chunks
+    const size_t xb = fast_x_bytes(h, nrhs), bb = fast_buf_bytes(h, nrhs);
+    const int64_t per = (int64_t)((nrhs + FAST_NB - 1) / FAST_NB) * (h->G.nb / ((int64_t)h->nranks * h->nranks)) *
+                        FAST_SLAB;
+    if (work_bytes) *work_bytes = 2 * bb + 2 * xb;
+    if (send_off) *send_off = 2 * bb;
+    if (recv_off) *recv_off = 2 * bb + xb;
+    for (int q = 0; q < h->nranks; ++q) {
+      if (send_counts) send_counts[q] = per;
+      if (recv_counts) recv_counts[q] = per;
+    }
+    return BF_OK;
+  }
   const size_t row_bytes = (size_t)nrhs * csize(h->dtype);
   if (work_bytes) *work_bytes = align256((size_t)h->slab_rows * row_bytes);
   if (send_off) *send_off = (size_t)h->send_base[k] * row_bytes;
@@ -1808,8 +1917,30 @@ int bf_dist_exchange_blocks(bf_handle h, int op, int64_t* n_send, int64_t* send_
   const int k = op == BF_OP_N ? 0 : 1;
   if (n_send) *n_send = (int64_t)h->send_blk[k].size();
   if (n_recv) *n_recv = (int64_t)h->recv_blk[k].size();
+  if (h->use_fast && k == 1) {
+    // fast format, op C: nu-major inside each peer's chunk
+    const Geom& G = h->G;
+    int p = 0;
+    while ((1 << p) < h->nranks) ++p;
+    const int64_t wt = int64_t(1) << (G.lc - p), wn = int64_t(1) << (G.L - G.lc - p), g = h->rank;
+    int64_t is = 0, ir = 0;
+    for (int64_t q = 0; q < h->nranks; ++q)
+      for (int64_t j = 0; j < wn; ++j)
+        for (int64_t i = 0; i < wt; ++i) {
+          if (send_blocks) send_blocks[is++] = G.idx(G.lc, g * wt + i, q * wn + j);  // sender owns tau
+          if (recv_blocks) recv_blocks[ir++] = G.idx(G.lc, q * wt + i, g * wn + j);  // receiver owns nu
+        }
+    return BF_OK;
+  }
   if (send_blocks) std::copy(h->send_blk[k].begin(), h->send_blk[k].end(), send_blocks);
   if (recv_blocks) std::copy(h->recv_blk[k].begin(), h->recv_blk[k].end(), recv_blocks);
+  return BF_OK;
+}
+
+int bf_dist_slab_format(bf_handle h, int32_t* fmt) {
+  if (!h || !fmt) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  if (!h->dist) return fail(Err{BF_ERR_ARG, "not a distributed handle"});
+  *fmt = h->use_fast ? 1 : 0;
   return BF_OK;
 }
 
@@ -1843,6 +1974,14 @@ static int dist_run(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ld
     else
       require(Y && ldy >= std::max<int64_t>(h->loc_rows_out[k], 1), BF_ERR_ARG, "bad Y_loc / ldy");
     DeviceGuard dg(h->device);
+    if (h->use_fast) {
+      const FastPlan& FP = h->fast[k];
+      if (pre)
+        run_fast(h, k, op, nrhs, X, ldx, nullptr, 0, work, static_cast<cudaStream_t>(stream), nullptr, 0, 0, FP.split);
+      else
+        run_fast(h, k, op, nrhs, nullptr, 0, Y, ldy, work, static_cast<cudaStream_t>(stream), nullptr, 0, FP.split);
+      return BF_OK;
+    }
     StageArgs a{};
     a.pool = h->pool;
     a.X = X;

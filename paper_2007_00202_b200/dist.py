@@ -32,6 +32,7 @@ from .bfapply import OPS, BFError, Workspace, _Keep, _check, _check_rhs, _stream
 _SIGS = [
     ("bf_dist_exchange_blocks", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("bf_dist_slab_format", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
 ]
 
 
@@ -98,6 +99,13 @@ class DistBFHandle:
             self.h, OPS[op], C.byref(ns), s.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(nr),
             r.ctypes.data_as(C.POINTER(C.c_int64))))
         return s[:ns.value], r[:nr.value]
+
+    def slab_format(self) -> int:
+        """0: generic block-contiguous send / recv regions; 1: fused-kernel half-slab chunks
+        (include/bfapply.h, bf_dist_slab_format)."""
+        f = C.c_int32()
+        _check("bf_dist_slab_format", _lib().bf_dist_slab_format(self.h, C.byref(f)))
+        return f.value
 
     def local_rows(self, op: str):
         """(rows_in, rows_out, user_off_in, user_off_out): this rank's slice of X and Y."""

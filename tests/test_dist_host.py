@@ -40,7 +40,9 @@ def _subtree_perm(n, leaf_ptr, L, p, seed):
 
 
 def _case(kind):
-    if kind == "uniform":
+    if kind == "fast":  # uniform rank 16: the fused kernels' split and exchange format
+        bf = random_butterfly(L=8, leaf=16, r=16, seed=7)
+    elif kind == "uniform":
         bf = random_butterfly(L=6, leaf=4, r=3, seed=5)
     else:
         rng = np.random.default_rng(3)
@@ -48,6 +50,48 @@ def _case(kind):
     bf.row_perm = _subtree_perm(bf.m, bf.row_leaf_ptr, bf.L, 2, 1)
     bf.col_perm = _subtree_perm(bf.n, bf.col_leaf_ptr, bf.L, 2, 2)
     return bf
+
+
+def _fast_positions(blocks, per_peer, nrhs):
+    """(element index in the region, tag) pairs of the half-slab exchange format: per peer
+    [tile][half][block][16 rows][16 columns] (include/bfapply.h, bf_dist_slab_format 1)."""
+    ntiles = (nrhs + 31) // 32
+    out = []
+    for qi in range(len(blocks) // per_peer):
+        base = qi * ntiles * 2 * per_peer * 256
+        for jt in range(ntiles):
+            for half in range(2):
+                for bi in range(per_peer):
+                    b = int(blocks[qi * per_peer + bi])
+                    for r in range(16):
+                        for c16 in range(16):
+                            col = jt * 32 + half * 16 + c16
+                            pos = base + ((jt * 2 + half) * per_peer + bi) * 256 + r * 16 + c16
+                            out.append((pos, b, r, col))
+    return out
+
+
+def _check_fast(h, op, nrhs, wb, so, ro, sc, rc, sblk, rblk, L, lc, p, rank, world):
+    per = len(sblk) // world
+    assert len(rblk) == len(sblk) == world * per
+    assert all(c == ((nrhs + 31) // 32) * per * 512 for c in list(sc) + list(rc)), (sc, rc)
+    tau, nu = sblk >> (L - lc), sblk & ((1 << (L - lc)) - 1)
+    own = (nu >> (L - lc - p)) if op == "N" else (tau >> (lc - p))
+    assert np.all(own == rank)
+    dest = (tau >> (lc - p)) if op == "N" else (nu >> (L - lc - p))
+    assert np.all(np.diff(dest) >= 0), "send region not grouped by destination"
+    work = torch.zeros(wb, dtype=torch.uint8)
+    send = work[so:so + sum(sc) * 16].view(torch.float64).view(-1, 2)
+    for pos, b, r, col in _fast_positions(sblk, per, nrhs):
+        send[pos, 0] = float(b)
+        send[pos, 1] = 1000.0 * r + col
+    h.exchange(work, op, nrhs)
+    recv = work[ro:ro + sum(rc) * 16].view(torch.float64).view(-1, 2)
+    for pos, b, r, col in _fast_positions(rblk, per, nrhs):
+        assert recv[pos, 0] == float(b) and recv[pos, 1] == 1000.0 * r + col, (op, b, r, col)
+    rt, rn = rblk >> (L - lc), rblk & ((1 << (L - lc)) - 1)
+    mine = (rt >> (lc - p)) if op == "N" else (rn >> (L - lc - p))
+    assert np.all(mine == rank), (op, "received blocks the rank does not own")
 
 
 def _worker(rank, world, port, kind, q):
@@ -63,10 +107,15 @@ def _worker(rank, world, port, kind, q):
         nrhs = 3
         rank_row = bf.rank_row()[: 1 << L]          # r^lc_{tau,nu}, canonical order
         rank_col = bf.rank_col()[lc << L:]          # c^lc_{tau,nu}
+        fmt = h.slab_format()
+        assert fmt == (1 if kind == "fast" else 0), fmt
         for op in ("N", "C"):
             wb, so, ro, sc, rc = h.layout(op, nrhs)
             sblk, rblk = h.exchange_blocks(op)
             size = rank_row if op == "N" else rank_col
+            if fmt == 1:
+                _check_fast(h, op, nrhs, wb, so, ro, sc, rc, sblk, rblk, L, lc, p, rank, world)
+                continue
             tau, nu = sblk >> (L - lc), sblk & ((1 << (L - lc)) - 1)
             # sender owns the column subtree (op N) / row subtree (op C)
             own = (nu >> (L - lc - p)) if op == "N" else (tau >> (lc - p))
@@ -117,7 +166,7 @@ def _worker(rank, world, port, kind, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("kind", ["uniform", "ragged"])
+@pytest.mark.parametrize("kind", ["uniform", "ragged", "fast"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_dist_exchange_gloo(kind, world):
     ctx = mp.get_context("spawn")

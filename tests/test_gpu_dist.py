@@ -91,6 +91,20 @@ def test_dist_emulated(kind, P, dtype):
         assert err <= TOL[dtype], (op, err)
 
 
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("P,L", [(2, 8), (4, 10), (8, 9)])
+def test_dist_fast_emulated(P, L, dtype):
+    """Uniform rank-16 butterflies take the fused split (leaf + window-pass kernels, half-slab
+    exchange format); identity perms, so the leaf kernels move X / Y with TMA tiles."""
+    bf = random_butterfly(L=L, leaf=16, r=16, seed=L + P, dtype=dtype)
+    assert DistBFHandle(bf, 0, P, 0).slab_format() == 1
+    K = oracle.bf_dense(bf)
+    for op, nr in (("N", 32), ("C", 45), ("T", 7)):
+        X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=P + nr, dtype=dtype)
+        err = oracle.rel_err(emulate(bf, X, op, P), oracle.apply_op(K, X, op))
+        assert err <= TOL[dtype], (op, err)
+
+
 @pytest.mark.parametrize("op", ["N", "C"])
 def test_dist_world1_self_exchange(op):
     bf = random_butterfly(L=6, leaf=16, r=16, seed=9)
