@@ -300,6 +300,34 @@ def hodbf_apply(H, X, op: str = "N") -> np.ndarray:
     return Y
 
 
+def hodbf_rows_apply(H, user_rows, X) -> np.ndarray:
+    """(A X)[user_rows, :] for an HOD-BF too large to densify (config 4):
+    row p of A (tree order) = row p of its leaf block D_t, plus, at every level l, row p of
+    the sibling butterfly A(T_tau, T_{tau^1}) of the node tau containing p, each
+    evaluated with bf_rows_apply on that butterfly (tree-local, identity perms)."""
+    X = np.asarray(X, dtype=C128)
+    user_rows = np.asarray(user_rows, dtype=np.int64)
+    assert len(np.unique(user_rows)) == len(user_rows), "sampled rows must be unique"
+    inv = np.empty(H.n, dtype=np.int64)
+    inv[H.perm] = np.arange(H.n)
+    tree = inv[user_rows]
+    Xt = X[H.perm, :]
+    out = np.zeros((len(tree), X.shape[1]), dtype=C128)
+    leaf = np.searchsorted(H.leaf_ptr, tree, side="right") - 1
+    for t in np.unique(leaf):
+        sel = np.nonzero(leaf == t)[0]
+        a, b = int(H.leaf_ptr[t]), int(H.leaf_ptr[t + 1])
+        out[sel] += np.asarray(H.D.block(int(t)), dtype=C128)[tree[sel] - a, :] @ Xt[a:b]
+    for l in range(1, H.LH + 1):
+        node = leaf >> (H.LH - l)
+        for tau in np.unique(node):
+            sel = np.nonzero(node == tau)[0]
+            r0, r1 = H.node_range(l, int(tau))
+            c0, c1 = H.node_range(l, int(tau) ^ 1)
+            out[sel] += bf_rows_apply(H.offdiag[l - 1][int(tau)], tree[sel] - r0, Xt[c0:c1])
+    return out
+
+
 def rel_err(Y, Yref) -> float:
     """||Y - Yref||_F / ||Yref||_F (the parity metric)."""
     Yref = np.asarray(Yref, dtype=C128)

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         if (atom_add_acqrel(wcnt, 1) == (int)(i + 1) * NACT - 1) str.issue_window(i + 1, rd ^ 1);
       }
       const E* win = winbuf + rd * WIN + half * Cfg::WINH;
-      typename Pol::Acc acc;
+      typename Pol::FAcc acc;
       acc.zero();
       const E* sp0 = win + o * FAST_HSLAB;
       const E* sp1 = sp0;
@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
       const unsigned char* pgn = ring + (size_t)slot * Cfg::PG + o * FAST_FRAG;
       int nslot = slot;
       uint32_t nph = ph;
-      typename Pol::Frags f[2];
-      Pol::load_a(f[0], pgn, lane);
+      typename Pol::FFrags f[2];
+      Pol::load_fa(f[0], pgn, lane);
       Pol::load_b(f[0], bsrc(0), bo);
 #pragma unroll
       for (int k = 0; k < NSTEP; ++k) {
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
             if (!(diag & 1)) mbar_wait(&full[nslot], nph, 4);
             pgn = ring + (size_t)nslot * Cfg::PG + o * FAST_FRAG;
           }
-          Pol::load_a(f[k1 & 1], pgn + (k1 % SPO) * S * FAST_FRAG, lane);
+          Pol::load_fa(f[k1 & 1], pgn + (k1 % SPO) * S * FAST_FRAG, lane);
           Pol::load_b(f[k1 & 1], bsrc(k1), bo);
         }
         acc.mac(f[k & 1]);

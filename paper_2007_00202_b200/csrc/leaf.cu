@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
   for (int64_t item = blockIdx.x + (int64_t)warp * gridDim.x; item < nitems; item += (int64_t)nw * gridDim.x) {
     const int64_t leaf = item % A.nleaf, jt = item / A.nleaf;
     const int j0 = (int)jt * FAST_NB;  // first rhs column of the tile
-    typename Pol::Acc acc;
+    typename Pol::FAcc acc;
     acc.zero();
     for (int ch = 0; ch < nch; ++ch, ++c) {
       const int st = (int)(c % dep);
@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
         const int nks = chunk / KS;
 #pragma unroll 2
         for (int s = 0; s < nks; ++s) {
-          typename Pol::Frags f;
-          Pol::load_a(f, sb + (size_t)s * FAST_FRAG, lane);
+          typename Pol::FFrags f;
+          Pol::load_fa(f, sb + (size_t)s * FAST_FRAG, lane);
           if (A.tma) {
             Pol::load_b_col(f, xb, chunk, s * KS, 0, g, t, cj);
           } else {
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
           acc.zero();
 #pragma unroll
           for (int ki = 0; ki < KPS; ++ki) {
-            typename Pol::Frags f;
-            Pol::load_a(f, sb + (size_t)(mgl * KPS + ki) * FAST_FRAG, lane);
+            typename Pol::FFrags f;
+            Pol::load_fa(f, sb + (size_t)(mgl * KPS + ki) * FAST_FRAG, lane);
             Pol::load_b(f, ys + ki * KS * FAST_HC, bo);
             acc.mac(f);
           }

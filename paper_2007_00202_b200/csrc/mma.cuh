@@ -161,6 +161,11 @@ struct PolC128 {
       set_b(f, ni, v);
     }
   }
+  // the product the fused kernels run: 3M (FP64 pipe is the bound; the 3M sums are cheap)
+  struct Acc;
+  using FFrags = Frags;
+  using FAcc = Acc;
+  __device__ static __forceinline__ void load_fa(Frags& f, const unsigned char* rec, int lane) { load_a(f, rec, lane); }
   struct Acc {
     double p[3][2][NT][2];
     __device__ __forceinline__ void zero() {
@@ -259,6 +264,13 @@ struct PolC64 {
     uint32_t ah[3][4], al[3][4];  // (re, im, re + im) x fragment registers
     float2 b[NT][2];
   };
+  // The product the fused kernels run on complex64: 3M on the 3xTF32 split.  (A 4M variant --
+  // 2 splits per operand element, no sums, 12 instead of 9 HMMAs -- measured slower on B200:
+  // 0.143 vs 0.129 ms per 3-level pass, tools/gpu_r2q.sh.)
+  struct Acc;
+  using FFrags = Frags;
+  using FAcc = Acc;
+  __device__ static __forceinline__ void load_fa(Frags& f, const unsigned char* rec, int lane) { load_a(f, rec, lane); }
   __device__ static __forceinline__ int boff(int t, int g, int c0w, int ni) {
     return t * FAST_HC + ((c0w + 8 * ni + g) ^ swz(t));  // row t + 4 is +4*16 (same swizzle)
   }
@@ -273,14 +285,16 @@ struct PolC64 {
       split(v[e].x + v[e].y, f.ah[2][e], f.al[2][e]);
     }
   }
-  __device__ static __forceinline__ void load_b(Frags& f, const E* slab_k0, const int (&bo)[NT]) {
+  template <class F>
+  __device__ static __forceinline__ void load_b(F& f, const E* slab_k0, const int (&bo)[NT]) {
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
       f.b[ni][0] = slab_k0[bo[ni]];
       f.b[ni][1] = slab_k0[bo[ni] + 4 * FAST_HC];
     }
   }
-  __device__ static __forceinline__ void load_b_col(Frags& f, const E* box, int ldb, int k0, int c0w, int g, int t,
+  template <class F>
+  __device__ static __forceinline__ void load_b_col(F& f, const E* box, int ldb, int k0, int c0w, int g, int t,
                                                     bool cj) {
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
@@ -297,7 +311,8 @@ struct PolC64 {
     p[0] = k0 + t;
     p[1] = k0 + t + 4;
   }
-  __device__ static __forceinline__ void load_b_x(Frags& f, const E* __restrict__ X, const int64_t (&rows)[XROWS],
+  template <class F>
+  __device__ static __forceinline__ void load_b_x(F& f, const E* __restrict__ X, const int64_t (&rows)[XROWS],
                                                   int64_t ldx, int col0, int g, int nrhs, bool cj) {
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {

@@ -214,6 +214,17 @@ def test_P9_sampled_rows_and_cols(kind):
     np.testing.assert_allclose(oracle.bf_cols_apply_adj(bf, cols, Z), Ya[cols], rtol=0, atol=1e-13 * np.abs(Ya).max())
 
 
+def test_P9_hodbf_sampled_rows():
+    """The config-4 oracle (sampled rows of an HOD-BF, per-level bf_rows_apply on the sibling
+    butterflies) equals rows of the dense HOD-BF assembly."""
+    from bfinputs.configs import helmholtz_plane_hodbf
+    H = helmholtz_plane_hodbf(16, 16, 10.0, 1e-4, ncomp=2)
+    X = random_rhs(H.n, 3, seed=5)
+    rows = np.random.default_rng(2).choice(H.n, size=40, replace=False)
+    Y = oracle.hodbf_dense(H) @ X
+    np.testing.assert_allclose(oracle.hodbf_rows_apply(H, rows, X), Y[rows], rtol=0, atol=1e-13 * np.abs(Y).max())
+
+
 # ---------------------------------------------------------------- P8
 def _lowrank_bf_L0(Ablock):
     m, n = Ablock.shape
