@@ -42,7 +42,7 @@ struct Task {
 struct Round {
   const Task* tasks;   // device
   const Term* terms;   // device
-  const int2* units;   // device: (task, 16-row group) work units of the tensor-core kernel
+  const int2* units;   // device: (task, 32-row block) work units of the tensor-core kernel
   int32_t nunits;
   int32_t pad0;
   int32_t ntasks;

@@ -38,108 +38,188 @@ __device__ __forceinline__ V vzero() {
 // from global memory / L2 (factor blocks with arbitrary row / column strides and conjugation,
 // slab rows or permuted user rows), zero-padded outside the task's rows, the term's K and nrhs.
 // ------------------------------------------------------------------------------------
-template <class Pol>
-__device__ __forceinline__ typename Pol::E ldA(const StageArgs& a, const Term& tm, int row, int k, int m, bool cj) {
-  using E = typename Pol::E;
-  E v{};
-  if (row < m && k < tm.k) {
-    v = __ldg(static_cast<const E*>(a.pool) + tm.a_off + (int64_t)row * tm.a_rs + (int64_t)k * tm.a_cs);
-    v.y = conj_im(v.y, cj);
-  }
-  return v;
-}
-template <class Pol>
-__device__ __forceinline__ typename Pol::E ldB(const StageArgs& a, const Term& tm, int k, int col) {
-  using E = typename Pol::E;
-  E v{};
-  if (k < tm.k && col < a.nrhs) {
-    const int64_t p = tm.in_row + k;
-    if (tm.in_kind == 0)
-      v = __ldg(static_cast<const E*>(a.S) + p * a.ldS + col);
-    else
-      v = __ldg(static_cast<const E*>(a.X) + (a.xperm ? a.xperm[p] : p) + (int64_t)col * a.ldx);
-  }
-  return v;
+// ------------------------------------------------------------------------------------
+// tensor-core gather-sum kernel (the same Task / Term tables).  One CTA (8 warps) computes a
+// 32-row x 64-column tile of one task's output: per term, K is streamed in chunks of 16 through
+// two shared-memory stages (cp.async, zero-filled outside the task's rows, the term's K and
+// nrhs), so every A element is read once per 64 columns and every input row once per 32 output
+// rows (the L2 traffic of per-warp direct loads bound the previous version at ~10 TF).  Warp w
+// computes rows 16 (w & 1).. and columns 16 (w >> 1).. with the 4M complex product (DMMA for
+// complex128, 3xTF32 for complex64): exact on 0 / 1 selection factors.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool ok, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
 }
 
-// fill the fragments of k-step k0 (c128: DMMA m8n8k4 layout; c64: TF32 m16n8k8 layout)
+template <class Pol>
+struct TileCfg {
+  using E = typename Pol::E;
+  static constexpr int TR = 32, TC = 64, KC = 16;       // tile rows, columns, K chunk (8 / 32 measured slower)
+  static constexpr int SA = sizeof(E) == 16 ? 34 : 36;  // padded strides (bank-conflict free
+  static constexpr int SB = sizeof(E) == 16 ? 66 : 68;  //   fragment reads)
+  static constexpr int STAGE = KC * (SA + SB);          // elements per stage
+};
+
+// fragments of k-step k0 of a staged chunk: A tile [k][row] (stride SA), B tile [k][col] (SB)
 template <int NT>
-__device__ __forceinline__ void frags(PolC128<NT>& /*tag*/, typename PolC128<NT>::Frags& f, const StageArgs& a,
-                                      const Term& tm, int r0, int m, int k0, int j0, int g, int t, bool cj) {
-  using P = PolC128<NT>;
+__device__ __forceinline__ void tile_frags(PolC128<NT>, typename PolC128<NT>::Frags& f, const double2* sA, const double2* sB, int wr,
+                                           int wc, int k0, int g, int t, bool cj) {
+  using C = TileCfg<PolC128<NT>>;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi) {
-    f.a[mi] = ldA<P>(a, tm, r0 + 8 * mi + g, k0 + t, m, cj);
-    f.as[mi] = f.a[mi].x + f.a[mi].y;
+    double2 v = sA[(k0 + t) * C::SA + wr + 8 * mi + g];
+    v.y = conj_im(v.y, cj);
+    f.a[mi] = v;
   }
 #pragma unroll
-  for (int ni = 0; ni < NT; ++ni) P::set_b(f, ni, ldB<P>(a, tm, k0 + t, j0 + 8 * ni + g));
+  for (int ni = 0; ni < NT; ++ni) f.b[ni] = sB[(k0 + t) * C::SB + wc + 8 * ni + g];
 }
 template <int NT>
-__device__ __forceinline__ void frags(PolC64<NT>& /*tag*/, typename PolC64<NT>::Frags& f, const StageArgs& a,
-                                      const Term& tm, int r0, int m, int k0, int j0, int g, int t, bool cj) {
+__device__ __forceinline__ void tile_frags(PolC64<NT>, typename PolC64<NT>::Frags& f, const float2* sA, const float2* sB, int wr,
+                                           int wc, int k0, int g, int t, bool cj) {
   using P = PolC64<NT>;
+  using C = TileCfg<P>;
   float2 v[4];
-  v[0] = ldA<P>(a, tm, r0 + g, k0 + t, m, cj);
-  v[1] = ldA<P>(a, tm, r0 + g + 8, k0 + t, m, cj);
-  v[2] = ldA<P>(a, tm, r0 + g, k0 + t + 4, m, cj);
-  v[3] = ldA<P>(a, tm, r0 + g + 8, k0 + t + 4, m, cj);
+  v[0] = sA[(k0 + t) * C::SA + wr + g];
+  v[1] = sA[(k0 + t) * C::SA + wr + g + 8];
+  v[2] = sA[(k0 + t + 4) * C::SA + wr + g];
+  v[3] = sA[(k0 + t + 4) * C::SA + wr + g + 8];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
+    v[e].y = conj_im(v[e].y, cj);
     P::split(v[e].x, f.ah[0][e], f.al[0][e]);
     P::split(v[e].y, f.ah[1][e], f.al[1][e]);
-    P::split(v[e].x + v[e].y, f.ah[2][e], f.al[2][e]);
   }
 #pragma unroll
   for (int ni = 0; ni < NT; ++ni) {
-    f.b[ni][0] = ldB<P>(a, tm, k0 + t, j0 + 8 * ni + g);
-    f.b[ni][1] = ldB<P>(a, tm, k0 + t + 4, j0 + 8 * ni + g);
+    f.b[ni][0] = sB[(k0 + t) * C::SB + wc + 8 * ni + g];
+    f.b[ni][1] = sB[(k0 + t + 4) * C::SB + wc + 8 * ni + g];
   }
 }
 
 template <class Pol>
-__global__ void __launch_bounds__(256, 2) k_stage_mma(StageArgs a) {
+__global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   using E = typename Pol::E;
-  constexpr int KS = Pol::KS;
-  const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (u >= a.nunits) return;
-  const int2 un = a.units[u];
+  using C = TileCfg<Pol>;
+  constexpr int KS = Pol::KS, TR = C::TR, TC = C::TC, KC = C::KC, SA = C::SA, SB = C::SB;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  E* sm = reinterpret_cast<E*>(sm_raw);  // 2 stages of [A: KC x SA][B: KC x SB]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int2 un = a.units[blockIdx.x];
   const Task tk = a.tasks[un.x];
-  const int r0 = un.y * 16;
-  const int j0 = blockIdx.y * 8 * Pol::NT;
+  const int r0 = un.y * TR;
+  const int j0 = blockIdx.y * TC;
   const int g = lane >> 2, t = lane & 3;
-  Pol tag;
-  typename Pol::Acc4 acc;  // 4M: exact on selection / identity factors
+  const int wr = 16 * (w & 1), wc = 16 * (w >> 1);  // warp tile origin inside the CTA tile
+  const E* __restrict__ pool = static_cast<const E*>(a.pool);
+  const E* __restrict__ S = static_cast<const E*>(a.S);
+  const E* __restrict__ X = static_cast<const E*>(a.X);
+
+  // chunk c of the flattened (term, K chunk) sequence -> stage c & 1
+  int q_ld = 0, kc_ld = 0;  // next chunk to load
+  auto load = [&](int stg) {
+    if (q_ld >= tk.nterm) return;
+    const Term tm = a.terms[tk.term0 + q_ld];
+    E* sA = sm + stg * C::STAGE;
+    E* sB = sA + KC * SA;
+    // A: TR x KC at (r0, kc_ld); lanes along the contiguous dimension of the factor view
+#pragma unroll
+    for (int e = 0; e < TR * KC / 256; ++e) {
+      const int x = tid + 256 * e;
+      int i, k;
+      if (tm.a_rs == 1) {
+        i = x % TR;
+        k = x / TR;
+      } else {
+        k = x % KC;
+        i = x / KC;
+      }
+      const bool ok = r0 + i < tk.m && kc_ld + k < tm.k;
+      const E* src = pool + (ok ? tm.a_off + (int64_t)(r0 + i) * tm.a_rs + (int64_t)(kc_ld + k) * tm.a_cs : 0);
+      cp_async_el(sA + k * SA + i, src, ok, (int)sizeof(E));
+    }
+    // B: KC x TC input rows (kc_ld..) x columns (j0..)
+#pragma unroll
+    for (int e = 0; e < KC * TC / 256; ++e) {
+      const int x = tid + 256 * e;
+      int k, j;
+      if (tm.in_kind == 0) {  // slab rows: columns contiguous
+        j = x % TC;
+        k = x / TC;
+      } else {  // user X (column-major): rows contiguous
+        k = x % KC;
+        j = x / KC;
+      }
+      const bool ok = kc_ld + k < tm.k && j0 + j < a.nrhs;
+      const E* src = S;
+      if (ok) {
+        const int64_t p = tm.in_row + kc_ld + k;
+        src = tm.in_kind == 0 ? S + p * a.ldS + j0 + j : X + (a.xperm ? a.xperm[p] : p) + (int64_t)(j0 + j) * a.ldx;
+      }
+      cp_async_el(sB + k * SB + j, src, ok, (int)sizeof(E));
+    }
+    kc_ld += KC;
+    if (kc_ld >= tm.k) {
+      kc_ld = 0;
+      ++q_ld;
+    }
+  };
+
+  typename Pol::Acc4 acc;
   acc.zero();
+  load(0);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  int c = 0;
   for (int q = 0; q < tk.nterm; ++q) {
     const Term tm = a.terms[tk.term0 + q];
     const bool cj = (tm.conj != 0) != (a.conj_flip != 0);
-    typename Pol::Frags f[2];
-    frags(tag, f[0], a, tm, r0, tk.m, 0, j0, g, t, cj);
-    int k0 = 0;
-    for (; k0 + KS < tm.k; k0 += 2 * KS) {
-      frags(tag, f[1], a, tm, r0, tk.m, k0 + KS, j0, g, t, cj);
-      acc.mac(f[0]);
-      if (k0 + 2 * KS < tm.k) frags(tag, f[0], a, tm, r0, tk.m, k0 + 2 * KS, j0, g, t, cj);
-      acc.mac(f[1]);
+    for (int kc = 0; kc < tm.k; kc += KC, ++c) {
+      load((c + 1) & 1);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      __syncthreads();
+      const E* sA = sm + (c & 1) * C::STAGE;
+      const E* sB = sA + KC * SA;
+#pragma unroll
+      for (int k0 = 0; k0 < KC; k0 += KS) {
+        typename Pol::Frags f;
+        tile_frags(Pol{}, f, sA, sB, wr, wc, k0, g, t, cj);
+        acc.mac(f);
+      }
+      __syncthreads();
     }
-    if (k0 < tm.k) acc.mac(f[0]);
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  const int rb = r0 + wr, cb = j0 + wc;
   if (a.out_kind == 0) {
-    E* S = static_cast<E*>(a.S);
-    acc.each(g, t, [&](int r, int c, E v) {
-      if (r0 + r < tk.m && j0 + c < a.nrhs) S[(tk.out_row + r0 + r) * a.ldS + j0 + c] = v;
+    E* Sd = static_cast<E*>(a.S);
+    acc.each(g, t, [&](int r, int cc, E v) {
+      if (rb + r < tk.m && cb + cc < a.nrhs) Sd[(tk.out_row + rb + r) * a.ldS + cb + cc] = v;
     });
   } else {
     E* Y = static_cast<E*>(a.Y);
-    acc.each(g, t, [&](int r, int c, E v) {
-      if (r0 + r < tk.m && j0 + c < a.nrhs) {
-        const int64_t p = tk.out_row + r0 + r;
-        Y[(a.yperm ? a.yperm[p] : p) + (int64_t)(j0 + c) * a.ldy] = v;
+    acc.each(g, t, [&](int r, int cc, E v) {
+      if (rb + r < tk.m && cb + cc < a.nrhs) {
+        const int64_t p = tk.out_row + rb + r;
+        Y[(a.yperm ? a.yperm[p] : p) + (int64_t)(cb + cc) * a.ldy] = v;
       }
     });
   }
+}
+
+template <class Pol>
+static void launch_tile(dim3 grid, const StageArgs& a, cudaStream_t st) {
+  constexpr size_t smem = 2 * TileCfg<Pol>::STAGE * sizeof(typename Pol::E);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_stage_tile<Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_stage_tile<Pol><<<grid, 256, smem, st>>>(a);
 }
 
 template <typename V>
@@ -149,17 +229,17 @@ static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
   a.units = r.units;
   a.nunits = r.nunits;
   a.out_kind = r.out_kind;
-  dim3 grid((r.nunits + 7) / 8, (a.nrhs + 15) / 16);  // warp tile: 16 rows x 16 columns
+  dim3 grid(r.nunits, (a.nrhs + 63) / 64);  // CTA tile: 32 rows x 64 columns
   if (sizeof(V) == 16)
-    k_stage_mma<PolC128<2>><<<grid, 256, 0, st>>>(a);
+    launch_tile<PolC128<2>>(grid, a, st);
   else
-    k_stage_mma<PolC64<2>><<<grid, 256, 0, st>>>(a);
+    launch_tile<PolC64<2>>(grid, a, st);
 }
 
 const char* round_kernel_name(int dtype, const Round& r, int* id) {
   (void)r;
   if (id) *id = 3;
-  return dtype == BF_C128 ? "k_stage_mma<c128>" : "k_stage_mma<c64>";
+  return dtype == BF_C128 ? "k_stage_tile<c128>" : "k_stage_tile<c64>";
 }
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st) {

@@ -752,10 +752,10 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
     xoff.push_back(tot);
     tot += pb.terms[r].size() * sizeof(Term);
     tot = (tot + 255) & ~size_t(255);
-    // work units of the tensor-core stage kernel: one per (task, 16-row group)
+    // work units of the tensor-core stage kernel: one per (task, 32-row block)
     std::vector<int2> u;
     for (size_t ti = 0; ti < pb.tasks[r].size(); ++ti)
-      for (int rg = 0; rg * 16 < pb.tasks[r][ti].m; ++rg) u.push_back(make_int2((int)ti, rg));
+      for (int rg = 0; rg * 32 < pb.tasks[r][ti].m; ++rg) u.push_back(make_int2((int)ti, rg));
     uoff.push_back(tot);
     tot += u.size() * sizeof(int2);
     tot = (tot + 255) & ~size_t(255);

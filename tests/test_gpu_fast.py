@@ -70,7 +70,7 @@ def test_fast_vs_generic_cfg5(monkeypatch, dtype):
     del hf
     monkeypatch.setenv("BF_DISABLE_FAST", "1")
     hg = pkg.BFHandle(bf)
-    assert hg.rounds("N")[0]["name"].startswith("k_stage_mma")
+    assert hg.rounds("N")[0]["name"].startswith("k_stage_tile")
     Yg = hg.apply(Xd)
     Yga = hg.apply(Xd, "C")
     torch.cuda.synchronize()

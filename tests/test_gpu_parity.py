@@ -13,7 +13,7 @@ import torch
 import oracle
 from bfinputs import (dft_butterfly, identity_butterfly, random_butterfly, random_ranks_butterfly,
                       random_rhs, butterfly_from_blocks)
-from bfinputs.configs import cfg1, cfg2, cfg3, cfg5, helmholtz_plane_hodbf
+from bfinputs.configs import cfg1, cfg2, cfg3, cfg4, cfg5, helmholtz_plane_hodbf
 import paper_2007_00202_b200 as pkg
 
 pytestmark = pytest.mark.gpu
@@ -236,3 +236,23 @@ def test_cfg3(dtype):
     assert oracle.rel_err(run(h, X, "N"), oracle.hodbf_apply(H, X, "N")) <= TOL[dtype]
     Z = random_rhs(H.n, 64, seed=31, dtype=dtype)
     assert oracle.rel_err(run(h, Z, "C"), oracle.hodbf_apply(H, Z, "C")) <= TOL[dtype]
+
+
+def test_cfg4():
+    """Config 4 (Maxwell-type front, 51200 unknowns, dyadic kernel, nrhs 512; constructed with
+    512 proxy rows / columns per ID): sampled rows of A X against the
+    HOD-BF sampled-row oracle, and the adjoint through <A X, Z> = <X, A^H Z>
+    over full vectors."""
+    H, X = cfg4(proxy_cap=512)
+    h = pkg.HODBFHandle(H)
+    Y = run(h, X, "N")
+    rng = np.random.default_rng(4)
+    rows = np.unique(np.concatenate([np.arange(int(H.leaf_ptr[5]), int(H.leaf_ptr[6])),
+                                     np.arange(int(H.leaf_ptr[700]), int(H.leaf_ptr[701])),
+                                     rng.choice(H.n, 48, replace=False)]))
+    assert oracle.rel_err(Y[rows], oracle.hodbf_rows_apply(H, rows, X)) <= 1e-12
+    Z = random_rhs(H.n, 8, seed=41)
+    Ya = run(h, Z, "C")
+    lhs = np.vdot(Z, Y[:, :8])
+    rhs = np.vdot(Ya, X[:, :8])
+    assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(Z) * np.linalg.norm(Y[:, :8])

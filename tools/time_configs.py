@@ -9,7 +9,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2007_00202_b200 as pkg  # noqa: E402
-from bfinputs.configs import cfg1, cfg2, cfg3  # noqa: E402
+from bfinputs.configs import cfg1, cfg2, cfg3, cfg4  # noqa: E402
 
 
 def timeit(h, X, op, nrhs, alg, steps=20):
@@ -34,7 +34,9 @@ def timeit(h, X, op, nrhs, alg, steps=20):
         h.apply_events(Xd, evs[k], op, out=Y)
     torch.cuda.synchronize()
     per = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(len(rounds))] for e in evs]).mean(0)
-    return {"ms": ms, "GB/s": alg / ms / 1e6, "rounds": len(rounds),
+    detail = [{"ms": round(float(per[i]), 4), "tasks": r["ntasks"], "entries": r["factor_entries"],
+               "tflops": round(8 * r["factor_entries"] * nrhs / (per[i] * 1e-3) / 1e12, 2)} for i, r in enumerate(rounds)]
+    return {"ms": ms, "GB/s": alg / ms / 1e6, "rounds": len(rounds), "detail": detail,
             "by_kernel": {n: round(float(sum(per[i] for i, r in enumerate(rounds) if r["name"] == n)), 4)
                           for n in sorted({r["name"] for r in rounds})}}
 
@@ -45,8 +47,8 @@ def main():
     for c in which:
         for dt in ([np.complex128, np.complex64] if c == "cfg3" else [np.complex128]):
             cs = 16 if dt == np.complex128 else 8
-            if c == "cfg3":
-                H, X = cfg3(dt)
+            if c in ("cfg3", "cfg4"):
+                H, X = cfg3(dt) if c == "cfg3" else cfg4(dt, proxy_cap=512)
                 h = pkg.HODBFHandle(H)
                 nnz = H.nnz()
                 n = m = H.n
