@@ -107,7 +107,7 @@ def cpu_threads():
         return len(os.sched_getaffinity(0))
 
 
-def oracle_sample(bf, X, nrows=(16, 64), centre=3):
+def oracle_sample(bf, X, nrows=(16, 128), centre=3):
     """Time the CPU oracle (sampled-row reconstruction) on rows of one
     centre node and extrapolate to the full apply with a two-point model
     T(rows) = setup + rows * per_row, full = 2^lc * setup + m * per_row."""
@@ -190,7 +190,7 @@ def run_reference(args):
     times = []
     sample = None
     for i in range(args.warmup + args.steps):
-        full, spent, sample = oracle_sample(bf, X, nrows=(8, 40), centre=1 + (i % 8))
+        full, spent, sample = oracle_sample(bf, X, nrows=(8, 64), centre=1 + (i % 8))
         if i >= args.warmup:
             times.append(full)
     t = float(np.median(times))

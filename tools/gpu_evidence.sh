@@ -1,0 +1,23 @@
+#!/bin/bash
+# evidence run: all GPU tests, bench lines (c128 default with cpu_baseline + e2e, c64, op C),
+# reference arm, ncu launch list, DRAM traffic per kernel, ncu --set full of the dominant
+# kernel and the leaf kernels, configs 1-4 on the generic path, split timing
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/ev
+O=gpurun_out/ev
+timeout 1500 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 600 python bench.py > $O/bench_c128.json 2> $O/bench_c128.err
+timeout 600 python bench.py --dtype c64 > $O/bench_c64.json 2> $O/bench_c64.err
+timeout 600 python bench.py --op C --no-cpu-baseline > $O/bench_c128_C.json 2> $O/bench_c128_C.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c128.csv $CMD > /dev/null 2>&1
+for dt in c128 c64; do
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 14 --csv --log-file $O/traffic_$dt.csv $CMD --dtype $dt > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bf_pass -s 6 -c 1 -o $O/full_pass_$dt $CMD --dtype $dt > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_leaf -s 2 -c 2 -o $O/full_leaf_$dt $CMD --dtype $dt > /dev/null 2>&1
+done
+timeout 1500 python tools/time_configs.py cfg1 cfg2 cfg3 cfg4 > $O/configs.txt 2> $O/configs.err
+timeout 900 python tools/time_split.py c128 > $O/split_c128.txt 2>&1
+echo done
