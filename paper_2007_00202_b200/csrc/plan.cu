@@ -1176,7 +1176,7 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
     }
     if (getenv("BF_DEBUG_SYNC")) {
       cudaError_t e = cudaStreamSynchronize(st);
-      fprintf(stderr, "bfapply debug: launch %zu (leaf=%d d=%d l0=%d nops=%d nwin=%lld) -> %s\n", i, P.leaf, P.d, P.l0,
+      fprintf(stderr, "bfapply debug: launch %d (leaf=%d d=%d l0=%d nops=%d nwin=%lld) -> %s\n", i, P.leaf, P.d, P.l0,
               P.nops, (long long)P.nwin, cudaGetErrorString(e));
       BF_CK(e);
     }
