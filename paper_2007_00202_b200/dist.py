@@ -198,3 +198,28 @@ class DistBFHandle:
         return {"value": alg_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "DistBFHandle.apply (pinned host X_loc/Y_loc per rank, copies inside the timed region)"}
+
+
+def rhs_shard(nrhs: int, rank: int, world: int):
+    """Columns [c0, c1) of an nrhs-column block owned by `rank` (contiguous, balanced)."""
+    base, rem = divmod(nrhs, world)
+    c0 = rank * base + min(rank, rem)
+    return c0, c0 + base + (1 if rank < rem else 0)
+
+
+class ShardedHODBF:
+    """HOD-BF apply with the right-hand sides sharded over the ranks (the layout
+    for configs 3-4, which are tensor-pipe bound).  Every rank holds the full HOD-BF on its GPU
+    and applies it to its own columns; there is no data-path collective.  ``apply`` takes and
+    returns the rank's (ncols_loc, n) column block; ``columns(nrhs)`` says which columns."""
+
+    def __init__(self, H, rank: int, world: int, device: int = 0):
+        from .bfapply import HODBFHandle
+        self.h = HODBFHandle(H, device)
+        self.rank, self.world, self.n = rank, world, H.n
+
+    def columns(self, nrhs: int):
+        return rhs_shard(nrhs, self.rank, self.world)
+
+    def apply(self, Xloc: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        return self.h.apply(Xloc, op, out=out)

@@ -200,3 +200,16 @@ def test_dist_rejects_bad_layouts():
     with pytest.raises(BFError) as e:
         h.apply(torch.zeros((1, 16), dtype=torch.complex128))
     assert e.value.code == -8
+
+
+def test_rhs_shard_partition():
+    """The RHS-sharded HOD-BF layout (configs 3-4): every column owned by exactly one rank,
+    contiguous, balanced to within one column."""
+    from paper_2007_00202_b200.dist import rhs_shard
+    for nrhs in (0, 1, 7, 64, 512, 513):
+        for world in (1, 2, 3, 4, 8):
+            parts = [rhs_shard(nrhs, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == nrhs
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1

@@ -113,3 +113,21 @@ def test_dist_world1_self_exchange(op):
     Y = h.apply(torch.from_numpy(np.ascontiguousarray(X.T)).cuda(), op)
     torch.cuda.synchronize()
     assert oracle.rel_err(Y.cpu().numpy().T, oracle.bf_apply(bf, X, op)) <= 1e-12
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_hodbf(world):
+    """RHS-sharded HOD-BF (config 4's multi-GPU layout): the ranks' column blocks, applied one
+    after another on one device, assemble the full result."""
+    from bfinputs.configs import helmholtz_plane_hodbf
+    from paper_2007_00202_b200.dist import ShardedHODBF
+    H = helmholtz_plane_hodbf(16, 16, 10.0, 1e-4, ncomp=2)
+    X = random_rhs(H.n, 37, seed=world)
+    Y = np.zeros_like(X)
+    for r in range(world):
+        s = ShardedHODBF(H, r, world, 0)
+        c0, c1 = s.columns(X.shape[1])
+        Yl = s.apply(torch.from_numpy(np.ascontiguousarray(X[:, c0:c1].T)).cuda())
+        torch.cuda.synchronize()
+        Y[:, c0:c1] = Yl.cpu().numpy().T
+    assert oracle.rel_err(Y, oracle.hodbf_apply(H, X)) <= 1e-12
