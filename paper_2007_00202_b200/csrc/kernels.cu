@@ -62,6 +62,7 @@ struct TileCfg {
   static constexpr int SA = sizeof(E) == 16 ? 34 : 36;  // padded strides (bank-conflict free
   static constexpr int SB = sizeof(E) == 16 ? 66 : 68;  //   fragment reads)
   static constexpr int STAGE = KC * (SA + SB);          // elements per stage
+  static constexpr int NST = 2;                         // cp.async stages (3 measured no faster)
 };
 
 // fragments of k-step k0 of a staged chunk: A tile [k][row] (stride SA), B tile [k][col] (SB)
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   using C = TileCfg<Pol>;
   constexpr int KS = Pol::KS, TR = C::TR, TC = C::TC, KC = C::KC, SA = C::SA, SB = C::SB;
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  E* sm = reinterpret_cast<E*>(sm_raw);  // 2 stages of [A: KC x SA][B: KC x SB]
+  E* sm = reinterpret_cast<E*>(sm_raw);  // C::NST stages of [A: KC x SA][B: KC x SB]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int2 un = a.units[blockIdx.x];
   const Task tk = a.tasks[un.x];
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   const E* __restrict__ S = static_cast<const E*>(a.S);
   const E* __restrict__ X = static_cast<const E*>(a.X);
 
-  // chunk c of the flattened (term, K chunk) sequence -> stage c & 1
+  // chunk c of the flattened (term, K chunk) sequence -> stage c % NST
   int q_ld = 0, kc_ld = 0;  // next chunk to load
   auto load = [&](int stg) {
     if (q_ld >= tk.nterm) return;
@@ -171,18 +172,21 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
 
   typename Pol::Acc4 acc;
   acc.zero();
-  load(0);
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
+#pragma unroll
+  for (int st = 0; st < C::NST - 1; ++st) {
+    load(st);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   int c = 0;
   for (int q = 0; q < tk.nterm; ++q) {
     const Term tm = a.terms[tk.term0 + q];
     const bool cj = (tm.conj != 0) != (a.conj_flip != 0);
     for (int kc = 0; kc < tm.k; kc += KC, ++c) {
-      load((c + 1) & 1);
+      load((c + C::NST - 1) % C::NST);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(C::NST - 1) : "memory");
       __syncthreads();
-      const E* sA = sm + (c & 1) * C::STAGE;
+      const E* sA = sm + (c % C::NST) * C::STAGE;
       const E* sB = sA + KC * SA;
 #pragma unroll
       for (int k0 = 0; k0 < KC; k0 += KS) {
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
 
 template <class Pol>
 static void launch_tile(dim3 grid, const StageArgs& a, cudaStream_t st) {
-  constexpr size_t smem = 2 * TileCfg<Pol>::STAGE * sizeof(typename Pol::E);
+  constexpr size_t smem = TileCfg<Pol>::NST * TileCfg<Pol>::STAGE * sizeof(typename Pol::E);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_stage_tile<Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
