@@ -182,6 +182,61 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         sp0 = win + (((2 * tt) << (ds - 1)) + (u >> 1)) * FAST_HSLAB;
         sp1 = win + (((2 * tt + 1) << (ds - 1)) + (u >> 1)) * FAST_HSLAB;
       }
+      if (op.kind == FK_LEAF_OUT) {
+        // fused row leaf (a5): Y(rows of this slot's leaf) = A (leaf x 16) y (16 x 32), one 16-row
+        // group at a time; A records stream through the ring like any op, y is this slot's slab
+        const int ds2 = P.d - op.s;
+        const int64_t leaf = ((a << op.s) + (o >> ds2)) + ((b << ds2) + (o & ((1 << ds2) - 1)));  // tau or nu
+        const int Lf = op.leaf;
+        const int64_t base = A.ycontig ? (A.yperm ? A.yperm[leaf * Lf] : leaf * Lf) : 0;
+        E* __restrict__ Y = static_cast<E*>(A.Y);
+        const bool cj = A.conj_io != 0;
+        const int n = op.nsteps;
+        static_assert(SPP % KPS == 0, "a page holds whole 16-row groups");
+        const int j0 = (int)jt * FAST_NB + half * FAST_HC + c0w;
+        for (int s0 = 0; s0 < n; s0 += SPP) {
+          if (!(diag & 1)) mbar_wait(&full[slot], ph, 4);
+          const unsigned char* pg = ring + (size_t)slot * Cfg::PG + o * FAST_FRAG;
+          const int ngrp = min(SPP, n - s0) / KPS;
+#pragma unroll 1
+          for (int mg = 0; mg < ngrp; ++mg) {
+            // the KPS k-steps of one 16-row group, software-pipelined
+            typename Pol::FFrags f[2];
+            Pol::load_fa(f[0], pg + (mg * KPS) * S * FAST_FRAG, lane);
+            Pol::load_b(f[0], sp0, bo);
+#pragma unroll
+            for (int ki = 0; ki < KPS; ++ki) {
+              if (ki + 1 < KPS) {
+                Pol::load_fa(f[(ki + 1) & 1], pg + (mg * KPS + ki + 1) * S * FAST_FRAG, lane);
+                Pol::load_b(f[(ki + 1) & 1], sp0 + (ki + 1) * Pol::KS * FAST_HC, bo);
+              }
+              acc.mac(f[ki & 1]);
+            }
+            const int64_t rr = (int64_t)((s0 / KPS) + mg) * 16;  // first leaf row of this group
+            acc.each(g, t, [&](int r, int c, E v) {
+              const int col = j0 + c;
+              if (col < A.nrhs) {
+                const int64_t row = A.ycontig ? base + rr + r : (A.yperm ? A.yperm[leaf * Lf + rr + r] : leaf * Lf + rr + r);
+                v.y = conj_im(v.y, cj);
+                Y[row + (int64_t)col * A.ldy] = v;
+              }
+            });
+            acc.zero();
+          }
+          __syncwarp();
+          if (lane == 0 && !(diag & 1)) {
+            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * NACT - 1) str.issue_page(j + NP);
+          }
+          ++j;
+          if (++slot == NP) {
+            slot = 0;
+            ph ^= 1;
+            ++rnd;
+          }
+        }
+        cur = rd ^ 1;
+        continue;  // (always the last op)
+      }
       // every op of a pass is a pair op of NSTEP = 32 / KS k-steps (the centre is folded into
       // R^{lc} / W^{lc} at create), so the k-step loop is fully unrolled, software-pipelined
       // across page boundaries: the operands of k-step k + 1 load while k-step k's MMAs issue

@@ -69,6 +69,11 @@ struct FastArgs {
   const void* F;
   const void* Sin;
   void* Sout;
+  void* Y;                // fused leaf-out op (last op FK_LEAF_OUT): user block written
+  int64_t ldy;
+  const int64_t* yperm;   // tree position -> user row (NULL = identity)
+  int32_t conj_io;        // op T: conjugate Y on store
+  int32_t ycontig;        // every leaf is a run of consecutive user rows
   int64_t nlev;  // slabs per level (2^L)
   int32_t nrhs;
   int32_t ntiles;  // 32-column rhs tiles (exchange layout stride)

@@ -464,6 +464,13 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     chunk(lc, L);
   } else {
     chunk(0, L);
+    if (opk == 0 && sizeof(CT) == 16) {  // op N: the smaller passes first, so that the last pass
+                                         // (which runs the fused row leaf) is a full-width one;
+                                         // op C runs the passes top-down
+      std::vector<int> r(lv.size());
+      for (size_t i = 0; i < lv.size(); ++i) r[i] = L - lv[lv.size() - 1 - i];
+      lv = r;
+    }
   }
   const int np = (int)lv.size() - 1;
   const int lr = (int)G.mt(0), lcn = (int)G.nv(0);
@@ -525,8 +532,13 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   };
   std::vector<FastPass> passes;
   int64_t total = 0;  // bytes
-  // launch k: 0 = leaf-in, 1..np = window passes, np + 1 = leaf-out
+  // launch k: 0 = leaf-in, 1..np = window passes, np + 1 = leaf-out.  On one GPU the row leaf
+  // (a5) is fused into the last window pass as its final op (FK_LEAF_OUT): the pass's output
+  // slabs never go to HBM and one launch disappears.
+  // (complex128 only: for complex64 the fused op measured no faster than the leaf kernel)
+  const bool fuse_out = !split && sizeof(CT) == 16 && !getenv("BF_NO_FUSE_OUT");
   for (int k = 0; k < np + 2; ++k) {
+    if (k == np + 1 && fuse_out) break;
     FastPass P{};
     P.L = L;
     std::vector<FastOp> ops;
@@ -603,6 +615,10 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
         if (split && l1 == lc) P.xin = 1;   // receive from the owner of tau
       }
       if (P.xout || P.xin) FP.split = (int)passes.size() + (P.xout ? 1 : 0);
+      if (fuse_out && k == np) {
+        add(FK_LEAF_OUT, adj ? 0 : d, adj ? lcn : lr);  // U_tau (level L) / conj(Vt_nu)^T (level 0)
+        P.out_s = -1;
+      }
     }
     P.nwin = int64_t(1) << (P.a_log + P.b_log);
     require((int)ops.size() <= FAST_MAXOPS, BF_ERR_ARG, "internal: too many ops in a pass");
@@ -623,7 +639,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     total += off * P.nwin;
     for (int q = 0; q < P.nops; ++q) {
       if (ops[q].kind == FK_LEAF_IN) P.user_in = P.nwin * ops[q].leaf;
-      if (ops[q].kind == FK_LEAF_OUT) P.user_out = P.nwin * ops[q].leaf;
+      if (ops[q].kind == FK_LEAF_OUT) P.user_out = P.nwin * ops[q].leaf << P.d;
     }
     passes.push_back(P);
   }
@@ -1172,6 +1188,11 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       a.nlev = h->G.nb;
       a.nrhs = (int32_t)nrhs;
       a.ntiles = ntiles;
+      a.Y = Y;  // fused leaf-out (last pass)
+      a.ldy = ldy;
+      a.yperm = fwd ? h->d_rperm : h->d_cperm;
+      a.conj_io = op == BF_OP_T ? 1 : 0;
+      a.ycontig = FP.contig_out ? 1 : 0;
       launch_fast_pass(h->dtype, a, st);
     }
     if (getenv("BF_DEBUG_SYNC")) {

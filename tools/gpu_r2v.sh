@@ -1,0 +1,10 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_fast.py tests/test_gpu_dist.py -x -q > gpurun_out/pytest_fast.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_fast.log
+for dt in c128 c64; do
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --dtype $dt > gpurun_out/b10_$dt.json 2> gpurun_out/b10_$dt.err
+done
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --op C > gpurun_out/b10_C.json 2> gpurun_out/b10_C.err
+echo done
