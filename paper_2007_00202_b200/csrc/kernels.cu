@@ -12,25 +12,6 @@
 
 namespace bfa {
 
-template <typename V>
-struct Scalar;
-template <>
-struct Scalar<double2> {
-  using R = double;
-};
-template <>
-struct Scalar<float2> {
-  using R = float;
-};
-
-template <typename V>
-__device__ __forceinline__ V vzero() {
-  V v;
-  v.x = 0;
-  v.y = 0;
-  return v;
-}
-
 // ------------------------------------------------------------------------------------
 // tensor-core gather-sum kernel (the same Task / Term tables): one warp per work unit =
 // (task, 16-row group) x 16 right-hand sides, 4M complex products on the tensor pipe
