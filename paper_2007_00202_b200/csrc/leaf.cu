@@ -224,7 +224,7 @@ static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
 
 void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
   const int w = dtype == BF_C128 ? 2 : 1;
-  // chunk rows (measured best on B200, tools/gpu_r2h.sh): IN 16 (c128) / 32 (c64) leaf rows,
+  // chunk rows (measured best on B200, tools/gpurun_scripts/gpu_r2h.sh): IN 16 (c128) / 32 (c64) leaf rows,
   // OUT 16 (c128) / 64 (c64) output rows; depth 2-4 stages per warp
   int kc = a.mode == 0 ? (dtype == BF_C128 ? 16 : 32) : (dtype == BF_C128 ? 16 : 64);
   if (const char* e = getenv(a.mode == 0 ? "BF_LEAF_KC" : "BF_LEAF_MC")) kc = atoi(e);  // tuning knob

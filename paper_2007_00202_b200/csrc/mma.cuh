@@ -266,7 +266,7 @@ struct PolC64 {
   };
   // The product the fused kernels run on complex64: 3M on the 3xTF32 split.  (A 4M variant --
   // 2 splits per operand element, no sums, 12 instead of 9 HMMAs -- measured slower on B200:
-  // 0.143 vs 0.129 ms per 3-level pass, tools/gpu_r2q.sh.)
+  // 0.143 vs 0.129 ms per 3-level pass, tools/gpurun_scripts/gpu_r2q.sh.)
   struct Acc;
   using FFrags = Frags;
   using FAcc = Acc;
