@@ -241,7 +241,7 @@ struct PolC128 {
 // complex64 policy: 3xTF32 mma.sync m16n8k8, fragments (lane = 4g + t):
 //   A (16x8): a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]
 //   B (8x8):  b0 = B[t][g], b1 = B[t+4][g];   C (16x8): c0,c1 = C[g][2t+e], c2,c3 = C[g+8][2t+e]
-// One k-step record (1 KB): [lane][4] float2 for the 16 x 8 block.  The A operand is split into
+// One k-step record (1 KB): [2][lane][2] float2 for the 16 x 8 block (two lane-contiguous halves).  The A operand is split into
 // TF32 hi / lo parts once per k-step (load_a); B per n-tile inside mac().
 // ======================================================================================
 template <int NT_>
@@ -275,8 +275,8 @@ struct PolC64 {
     return t * FAST_HC + ((c0w + 8 * ni + g) ^ swz(t));  // row t + 4 is +4*16 (same swizzle)
   }
   __device__ static __forceinline__ void load_a(Frags& f, const unsigned char* rec, int lane) {
-    const float4* p = reinterpret_cast<const float4*>(rec) + 2 * lane;
-    const float4 x = p[0], y = p[1];
+    const float4* p = reinterpret_cast<const float4*>(rec);
+    const float4 x = p[lane], y = p[32 + lane];  // lane-contiguous halves: no bank conflicts
     const float2 v[4] = {make_float2(x.x, x.y), make_float2(x.z, x.w), make_float2(y.x, y.y), make_float2(y.z, y.w)};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {

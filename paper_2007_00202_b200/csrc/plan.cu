@@ -417,8 +417,9 @@ static inline CT cj(CT v, bool c) {
 // one 1 KB k-step record of an M x K operand: row group mg (16 rows), k-step ki, in the MMA
 // fragment order the pass kernel consumes.
 // complex128 (mma m8n8k4, KS = 4): [mi][lane], lane = 4g + t <-> (row 16mg + 8mi + g, col 4ki + t)
-// complex64 (mma m16n8k8, KS = 8): [lane][e], e: (g, t), (g+8, t), (g, t+4), (g+8, t+4) of the
-//                                  16 x 8 block at rows 16mg, cols 8ki
+// complex64 (mma m16n8k8, KS = 8): [h][lane][e2], (h, e2) = (0,0) (g, t), (0,1) (g+8, t),
+//                                  (1,0) (g, t+4), (1,1) (g+8, t+4) of the 16 x 8 block at rows
+//                                  16mg, cols 8ki (each half one conflict-free 16-byte load/lane)
 template <typename CT, typename Fn>
 static void fill_step(CT* dst, int mg, int ki, Fn A) {
   if (sizeof(CT) == 16) {
@@ -430,11 +431,11 @@ static void fill_step(CT* dst, int mg, int ki, Fn A) {
   } else {
     for (int lane = 0; lane < 32; ++lane) {
       const int g = lane >> 2, t = lane & 3;
-      CT* d = dst + lane * 4;
-      d[0] = A(16 * mg + g, 8 * ki + t);
-      d[1] = A(16 * mg + g + 8, 8 * ki + t);
-      d[2] = A(16 * mg + g, 8 * ki + t + 4);
-      d[3] = A(16 * mg + g + 8, 8 * ki + t + 4);
+      // two 512-byte halves, each read by one lane-contiguous 16-byte load per lane
+      dst[2 * lane + 0] = A(16 * mg + g, 8 * ki + t);
+      dst[2 * lane + 1] = A(16 * mg + g + 8, 8 * ki + t);
+      dst[64 + 2 * lane + 0] = A(16 * mg + g, 8 * ki + t + 4);
+      dst[64 + 2 * lane + 1] = A(16 * mg + g + 8, 8 * ki + t + 4);
     }
   }
 }
