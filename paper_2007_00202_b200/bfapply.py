@@ -291,9 +291,15 @@ class BFHandle:
             C.c_void_p(work.data_ptr()), work.numel(), _stream_handle(stream), evs, len(events)))
         return out
 
+    def workspace_size_host(self, nrhs: int, op: str = "N") -> int:
+        s = C.c_size_t()
+        _check("bf_workspace_size_host", lib().bf_workspace_size_host(self.h, OPS[op], nrhs, C.byref(s)))
+        return s.value
+
     def apply_host(self, Xh: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None,
                    work: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-        """End-to-end form: X and Y in (pinned) host memory; copies inside the call."""
+        """End-to-end form: X and Y in (pinned) host memory; copies inside the call, pipelined
+        across calls (include/bfapply.h).  `out` is complete once `stream` synchronises."""
         rin, rout = (self.n, self.m) if op == "N" else (self.m, self.n)
         assert not Xh.is_cuda and Xh.dim() == 2 and Xh.shape[1] == rin and Xh.is_contiguous()
         nrhs = Xh.shape[0]

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <type_traits>
@@ -888,9 +889,25 @@ struct bf_s {
   int64_t loc_user_in[2] = {0, 0}, loc_user_out[2] = {0, 0};
   int64_t* d_lperm_in[2] = {nullptr, nullptr};
   int64_t* d_lperm_out[2] = {nullptr, nullptr};
+  // bf_apply_host pipelining: copy streams, per-buffer-set events, call counter
+  std::mutex hmu;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  int64_t hcalls = 0;
   ~bf_s() {
     if (host_only) return;
     cudaSetDevice(device);
+    if (s_h2d) {
+      cudaStreamSynchronize(s_h2d);
+      cudaStreamSynchronize(s_d2h);
+      cudaStreamDestroy(s_h2d);
+      cudaStreamDestroy(s_d2h);
+      for (int k = 0; k < 2; ++k) {
+        cudaEventDestroy(ev_h2d[k]);
+        cudaEventDestroy(ev_cmp[k]);
+        cudaEventDestroy(ev_d2h[k]);
+      }
+    }
     for (int k = 0; k < 2; ++k) {
       free_plan(plan[k]);
       free_plan(pre[k]);
@@ -1317,10 +1334,16 @@ int bf_workspace_size_host(bf_handle h, int op, int64_t nrhs, size_t* bytes) {
   size_t s = 0;
   bf_workspace_size(h, nrhs, &s);
   const size_t cs = csize(h->dtype);
-  *bytes = s + align256((size_t)rx * nrhs * cs) + align256((size_t)ry * nrhs * cs);
+  // two sets of device X / Y copies: consecutive calls alternate between them
+  *bytes = s + 2 * (align256((size_t)rx * nrhs * cs) + align256((size_t)ry * nrhs * cs));
   return BF_OK;
 }
 
+// Host-memory apply, pipelined across calls: the H2D copy of X and the D2H copy of Y run on the
+// handle's two copy streams (the two PCIe directions are independent), the apply on `stream`.
+// Call k uses device buffer set k % 2, so the H2D copy of call k+1 overlaps the D2H copy of call
+// k; every call's own copies are still inside it: `stream` waits for this call's D2H before
+// anything later on it, so Y_host is complete when the caller synchronises `stream`.
 int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx, void* Yh, int64_t ldy,
                   void* work, size_t work_bytes, bf_stream_t stream) {
   if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
@@ -1333,23 +1356,45 @@ int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx
     validate_apply(nrhs, Xh, ldx, rx, Yh, ldy, ry, work_bytes, need);
     if (nrhs == 0) return BF_OK;
     DeviceGuard dg(h->device);
+    std::lock_guard<std::mutex> lk(h->hmu);
+    if (!h->s_h2d) {
+      BF_CK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+      BF_CK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        BF_CK(cudaEventCreateWithFlags(&h->ev_h2d[k], cudaEventDisableTiming));
+        BF_CK(cudaEventCreateWithFlags(&h->ev_cmp[k], cudaEventDisableTiming));
+        BF_CK(cudaEventCreateWithFlags(&h->ev_d2h[k], cudaEventDisableTiming));
+      }
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t cs = csize(h->dtype);
-    char* dX = static_cast<char*>(work) + s;
-    char* dY = dX + align256((size_t)rx * nrhs * cs);
-    // one copy per call when the host block is dense, else one per column
+    const size_t bx = align256((size_t)rx * nrhs * cs), by = align256((size_t)ry * nrhs * cs);
+    const int set = (int)(h->hcalls & 1);
+    char* dX = static_cast<char*>(work) + s + set * (bx + by);
+    char* dY = dX + bx;
+    // H2D into this set once the apply that last read it (call k - 2) is done
+    if (h->hcalls >= 2) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_cmp[set], 0));
     if (ldx == rx) {
-      BF_CK(cudaMemcpyAsync(dX, Xh, (size_t)rx * nrhs * cs, cudaMemcpyHostToDevice, st));
+      BF_CK(cudaMemcpyAsync(dX, Xh, (size_t)rx * nrhs * cs, cudaMemcpyHostToDevice, h->s_h2d));
     } else {
-      BF_CK(cudaMemcpy2DAsync(dX, rx * cs, Xh, ldx * cs, rx * cs, nrhs, cudaMemcpyHostToDevice, st));
+      BF_CK(cudaMemcpy2DAsync(dX, rx * cs, Xh, ldx * cs, rx * cs, nrhs, cudaMemcpyHostToDevice, h->s_h2d));
     }
+    BF_CK(cudaEventRecord(h->ev_h2d[set], h->s_h2d));
+    // the apply: after this call's H2D; its Y set was last read by call k - 2's D2H, which
+    // `stream` already waited for
+    BF_CK(cudaStreamWaitEvent(st, h->ev_h2d[set], 0));
     int rc = bf_apply_op(h, op, nrhs, dX, std::max<int64_t>(rx, 1), dY, std::max<int64_t>(ry, 1), work, s, stream);
     if (rc != BF_OK) return rc;
+    BF_CK(cudaEventRecord(h->ev_cmp[set], st));
+    BF_CK(cudaStreamWaitEvent(h->s_d2h, h->ev_cmp[set], 0));
     if (ldy == ry) {
-      BF_CK(cudaMemcpyAsync(Yh, dY, (size_t)ry * nrhs * cs, cudaMemcpyDeviceToHost, st));
+      BF_CK(cudaMemcpyAsync(Yh, dY, (size_t)ry * nrhs * cs, cudaMemcpyDeviceToHost, h->s_d2h));
     } else {
-      BF_CK(cudaMemcpy2DAsync(Yh, ldy * cs, dY, ry * cs, ry * cs, nrhs, cudaMemcpyDeviceToHost, st));
+      BF_CK(cudaMemcpy2DAsync(Yh, ldy * cs, dY, ry * cs, ry * cs, nrhs, cudaMemcpyDeviceToHost, h->s_d2h));
     }
+    BF_CK(cudaEventRecord(h->ev_d2h[set], h->s_d2h));
+    BF_CK(cudaStreamWaitEvent(st, h->ev_d2h[set], 0));  // Y_host complete in `stream` order
+    ++h->hcalls;
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);

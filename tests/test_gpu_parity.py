@@ -256,3 +256,22 @@ def test_cfg4():
     lhs = np.vdot(Z, Y[:, :8])
     rhs = np.vdot(Ya, X[:, :8])
     assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(Z) * np.linalg.norm(Y[:, :8])
+
+
+@pytest.mark.parametrize("fast", [True, False])
+def test_host_apply_pipelined(fast):
+    """Back-to-back bf_apply_host calls (pipelined: call k+1's H2D overlaps call k's D2H) on
+    distinct host buffers, alternating op N and C, are all correct after one synchronise."""
+    bf = random_butterfly(L=6, leaf=32, r=16 if fast else 8, seed=12)
+    h = pkg.BFHandle(bf)
+    K = oracle.bf_dense(bf)
+    ops = ["N", "C", "N", "N", "C", "T"]
+    Xs = [random_rhs(bf.n, 33, seed=40 + i) for i in range(len(ops))]
+    Xh = [torch.from_numpy(np.ascontiguousarray(X.T)).pin_memory() for X in Xs]
+    Yh = [torch.empty((33, bf.n), dtype=torch.complex128).pin_memory() for _ in ops]
+    work = torch.empty(h.workspace_size_host(33), dtype=torch.uint8, device="cuda")
+    for x, y, op in zip(Xh, Yh, ops):
+        h.apply_host(x, op, out=y, work=work)
+    torch.cuda.synchronize()
+    for X, y, op in zip(Xs, Yh, ops):
+        assert oracle.rel_err(y.numpy().T, oracle.apply_op(K, X, op)) <= 1e-12, op
