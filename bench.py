@@ -218,6 +218,9 @@ def main():
     ap.add_argument("--nrhs", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: centre exchange by NCCL all-to-all, or fused into the kernel over peer "
+                         "memory (torch symmetric memory; bf_dist_apply_pre_p2p)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -260,6 +263,8 @@ def main():
     else:
         from paper_2007_00202_b200.dist import DistBFHandle
         h = DistBFHandle(bf, rank, world, local)
+        if args.exchange == "p2p":
+            h.enable_p2p(args.nrhs, args.op)
         Xloc = h.local_input(X, args.op)
         Xd = torch.from_numpy(np.ascontiguousarray(Xloc.T)).cuda()
         Yd = h.empty_output(nrhs, args.op)
@@ -355,7 +360,9 @@ def main():
                            "factor_entries": bf.nnz(), "alg_bytes_per_step": ab,
                            "l2": "inputs larger than L2 (factors %.2f GB >> 126 MB); no flush" % (bf.nnz() * cs / 1e9),
                            "parallelism": "single GPU" if world == 1 else
-                           f"tree split over {world} GPUs (column subtrees -> NCCL all-to-all -> row subtrees)"},
+                           f"tree split over {world} GPUs (column subtrees -> "
+                           + ("fused peer-memory exchange" if args.exchange == "p2p" else "NCCL all-to-all")
+                           + " -> row subtrees)"},
                 "rhs_cols_per_s": nrhs / (ms * 1e-3), "hbm_frac": value / peaks["hbm_gbs"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches * args.steps, "clocks": clk.summary(), "per_round": per_round}

@@ -194,6 +194,16 @@ int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out,
                        int64_t* user_off_in, int64_t* user_off_out);
 int bf_dist_apply_pre(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx,
                       void* work, size_t work_bytes, bf_stream_t stream);
+/* Fused exchange (bf_dist_slab_format 1 only): like bf_dist_apply_pre, but the pass that
+ * ends at the centre level stores each slab straight into its receiver's recv region over peer
+ * memory (NVLink / NVSwitch) while it computes -- no send region, no all-to-all.  peer_recv[q]
+ * (host array of nranks device pointers) is rank q's recv-region base as mapped in this
+ * process (e.g. torch symmetric memory, CUDA IPC); this rank's chunk in it is at the offset
+ * its own bf_dist_layout recv region has for source `rank`.  The caller then synchronises the
+ * ranks (every sender done) before bf_dist_apply_post, and again before the next pre writes
+ * into the recv regions. */
+int bf_dist_apply_pre_p2p(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx,
+                          void* work, size_t work_bytes, void* const* peer_recv, bf_stream_t stream);
 int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy,
                        void* work, size_t work_bytes, bf_stream_t stream);
 

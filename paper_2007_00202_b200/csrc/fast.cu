@@ -283,7 +283,15 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
       }
       if (last) {
         if (!(diag & 2)) {
-          E* dst = Sout + pass_slab_off(P, P.xout, jt, half, A.nlev, A.ntiles, a, b, P.out_s, o);
+          E* dst;
+          if (P.xout && A.p2p) {  // fused exchange: straight into the receiver's recv region
+            int peer = 0;
+            const int64_t off =
+                pass_slab_off(P, P.xout, jt, half, A.nlev, A.ntiles, a, b, P.out_s, o, A.myrank, &peer);
+            dst = static_cast<E*>(A.peer[peer]) + off;
+          } else {
+            dst = Sout + pass_slab_off(P, P.xout, jt, half, A.nlev, A.ntiles, a, b, P.out_s, o);
+          }
           acc.each(g, t, [&](int r, int c, E v) { dst[r * FAST_HC + ((c0w + c) ^ Pol::swz(r))] = v; });
         }
         cur = rd ^ 1;

@@ -31,6 +31,7 @@ constexpr int FAST_RANK = 16;                   // r: slab rows
 constexpr int FAST_NB = 32;                     // right-hand sides per work item (slab columns)
 constexpr int FAST_DMAX = 3;                    // window levels per pass
 constexpr int FAST_MAXOPS = 8;
+constexpr int FAST_MAXPEER = 8;                 // ranks the fused peer-memory exchange addresses
 constexpr int FAST_SLAB = FAST_RANK * FAST_NB;  // complex entries per slab (512)
 constexpr int FAST_HC = 16;                     // rhs columns per half slab (one pass CTA's share)
 constexpr int FAST_HSLAB = FAST_RANK * FAST_HC; // complex entries per half slab (256)
@@ -78,6 +79,9 @@ struct FastArgs {
   int32_t nrhs;
   int32_t ntiles;  // 32-column rhs tiles (exchange layout stride)
   int32_t skew;  // ns the second column half starts late (tuning knob, env BF_FAST_SKEW)
+  int32_t p2p;   // xout pass: write each slab straight into its receiver's recv region
+  int32_t myrank;
+  void* peer[FAST_MAXPEER];  // p2p: every rank's recv-region base (peer memory over NVLink)
   int32_t diag;  // profiling only (env BF_FAST_DIAG, results are garbage): bit 0 = no operand
                  // streaming (compute only), bit 1 = output slabs not written to HBM, bit 2 = no
                  // intermediate epilogue / barriers, bit 3 (with 2) = epilogue stores, no barriers
@@ -145,15 +149,20 @@ __host__ __device__ inline int64_t slab_index(const FastPass& P, int64_t a, int6
 // the slab buffer (mode 0) or in the exchange layout of the centre level (mode 1 / 2: peer =
 // owner of tau / of nu): [peer][jt][half][tau_l][nu_l] for op N, [peer][jt][half][nu_l][tau_l]
 // for op C, so the 2^d slabs a receiving window reads are contiguous again.
+// With chunk >= 0 the chunk index is given (the sender's rank when it writes straight into a
+// receiver's recv region) instead of the peer; *peer_out returns the peer.
 __host__ __device__ inline int64_t pass_slab_off(const FastPass& P, int mode, int64_t jt, int half, int64_t nlev,
-                                                 int64_t ntiles, int64_t a, int64_t b, int s, int slot) {
+                                                 int64_t ntiles, int64_t a, int64_t b, int s, int slot,
+                                                 int chunk = -1, int* peer_out = nullptr) {
   if (mode == 0) return half_slab_off(jt, half, nlev, slab_index(P, a, b, s, slot));
   const int ds = P.d - s;
   const int64_t tau = (a << s) + (slot >> ds);
   const int64_t nu = (b << ds) + (slot & ((1 << ds) - 1));
   const int64_t wt = int64_t(1) << P.wt_log, wn = int64_t(1) << P.wn_log;
   const int64_t tl = tau & (wt - 1), nl = nu & (wn - 1);
-  const int64_t peer = mode == 1 ? (tau >> P.wt_log) : (nu >> P.wn_log);
+  int64_t peer = mode == 1 ? (tau >> P.wt_log) : (nu >> P.wn_log);
+  if (peer_out) *peer_out = (int)peer;
+  if (chunk >= 0) peer = chunk;
   const int64_t inner = P.numaj ? nl * wt + tl : tl * wn + nl;
   return (((peer * ntiles + jt) * 2 + half) * (wt * wn) + inner) * FAST_HSLAB;
 }

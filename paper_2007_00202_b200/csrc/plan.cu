@@ -1158,7 +1158,8 @@ int bf_workspace_size(bf_handle h, int64_t nrhs, size_t* bytes) {
 // launches [lo, hi) of the fast plan of op slot k.  Workspace: two slab buffers, then (split
 // handles only) the send and the recv region of the centre exchange.
 static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                     void* work, cudaStream_t st, void* const* ev, int nev, int lo = 0, int hi = -1) {
+                     void* work, cudaStream_t st, void* const* ev, int nev, int lo = 0, int hi = -1,
+                     void* const* peer_recv = nullptr) {
   const FastPlan& FP = h->fast[k];
   if (hi < 0) hi = (int)FP.passes.size();
   if (ev) require(nev >= hi - lo + 1, BF_ERR_ARG, "need nrounds + 1 events");
@@ -1200,6 +1201,11 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       a.p = P;
       a.diag = diag;
       a.skew = getenv("BF_FAST_SKEW") ? atoi(getenv("BF_FAST_SKEW")) : 0;
+      if (peer_recv && P.xout) {  // fused peer-memory exchange
+        a.p2p = 1;
+        a.myrank = h->rank;
+        for (int q = 0; q < h->nranks; ++q) a.peer[q] = peer_recv[q];
+      }
       a.F = FP.F;
       a.Sin = P.xin ? recvb : buf[i % 2];
       a.Sout = P.xout ? sendb : buf[(i + 1) % 2];
@@ -2024,7 +2030,8 @@ int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out,
 }
 
 static int dist_run(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                    void* work, size_t work_bytes, bf_stream_t stream, bool pre) {
+                    void* work, size_t work_bytes, bf_stream_t stream, bool pre,
+                    void* const* peer_recv = nullptr) {
   if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
   try {
     require(h->dist, BF_ERR_ARG, "not a distributed handle");
@@ -2044,7 +2051,8 @@ static int dist_run(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ld
     if (h->use_fast) {
       const FastPlan& FP = h->fast[k];
       if (pre)
-        run_fast(h, k, op, nrhs, X, ldx, nullptr, 0, work, static_cast<cudaStream_t>(stream), nullptr, 0, 0, FP.split);
+        run_fast(h, k, op, nrhs, X, ldx, nullptr, 0, work, static_cast<cudaStream_t>(stream), nullptr, 0, 0, FP.split,
+                 peer_recv);
       else
         run_fast(h, k, op, nrhs, nullptr, 0, Y, ldy, work, static_cast<cudaStream_t>(stream), nullptr, 0, FP.split);
       return BF_OK;
@@ -2071,6 +2079,14 @@ static int dist_run(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ld
 int bf_dist_apply_pre(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx, void* work,
                       size_t work_bytes, bf_stream_t stream) {
   return dist_run(h, op, nrhs, X_loc, ldx, nullptr, 0, work, work_bytes, stream, true);
+}
+
+int bf_dist_apply_pre_p2p(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx, void* work,
+                          size_t work_bytes, void* const* peer_recv, bf_stream_t stream) {
+  if (!h || !peer_recv) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  if (!h->use_fast || h->nranks > FAST_MAXPEER)
+    return fail(Err{BF_ERR_ARG, "peer-memory exchange needs the fused split (bf_dist_slab_format 1, <= 8 ranks)"});
+  return dist_run(h, op, nrhs, X_loc, ldx, nullptr, 0, work, work_bytes, stream, true, peer_recv);
 }
 
 int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy, void* work, size_t work_bytes,

@@ -33,6 +33,8 @@ _SIGS = [
     ("bf_dist_exchange_blocks", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("bf_dist_slab_format", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    ("bf_dist_apply_pre_p2p", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                        C.c_size_t, C.POINTER(C.c_void_p), C.c_void_p]),
 ]
 
 
@@ -138,9 +140,26 @@ class DistBFHandle:
         dist.all_to_all_single(recv, send, output_split_sizes=[2 * c for c in rc],
                                input_split_sizes=[2 * c for c in sc], group=self.group)
 
+    def enable_p2p(self, nrhs: int, op: str = "N"):
+        """Fused peer-memory exchange (bf_dist_apply_pre_p2p): the workspace becomes a torch
+        symmetric-memory buffer mapped on every rank, so the pass that ends at the centre stores
+        its slabs straight into the receivers' recv regions over NVLink; a device-side barrier
+        replaces the all-to-all.  Needs the fused split (slab_format() == 1)."""
+        import torch.distributed._symmetric_memory as symm_mem
+        assert self.slab_format() == 1, "peer-memory exchange needs the fused split"
+        wb, so, ro, sc, rc = self.layout(op, nrhs)
+        buf = symm_mem.empty(wb, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        grp = self.group if self.group is not None else dist.group.WORLD
+        hdl = symm_mem.rendezvous(buf, grp)
+        self._p2p = {"key": (op, nrhs), "work": buf, "hdl": hdl,
+                     "peers": (C.c_void_p * self.world)(*[int(pt) + ro for pt in hdl.buffer_ptrs])}
+
     def apply(self, Xloc: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None,
               work: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """Y_loc = (K X)_loc (op N) or (K^H X)_loc (op C) / (K^T X)_loc (op T)."""
+        p2p = getattr(self, "_p2p", None)
+        if p2p is not None and p2p["key"] == (op, Xloc.shape[0]):
+            return self._apply_p2p(Xloc, op, out, stream)
         if self.ws is None:
             raise BFError("bf_dist_apply_pre", -8, "host-only plan cannot apply")
         ri, ro, _, _ = self._rows[op]
@@ -158,6 +177,25 @@ class DistBFHandle:
         self.exchange(work, op, nrhs)
         _check("bf_dist_apply_post", lib().bf_dist_apply_post(self.h, OPS[op], nrhs, C.c_void_p(out.data_ptr()), ldy,
                                                                C.c_void_p(work.data_ptr()), work.numel(), st))
+        return out
+
+    def _apply_p2p(self, Xloc, op, out, stream):
+        p2p = self._p2p
+        ri, ro, _, _ = self._rows[op]
+        ldx = _check_rhs(Xloc, ri, self.code, "X_loc")
+        nrhs = Xloc.shape[0]
+        if out is None:
+            out = self.empty_output(nrhs, op)
+        ldy = _check_rhs(out, ro, self.code, "Y_loc")
+        work = p2p["work"]
+        st = _stream_handle(stream)
+        _check("bf_dist_apply_pre_p2p", _lib().bf_dist_apply_pre_p2p(
+            self.h, OPS[op], nrhs, C.c_void_p(Xloc.data_ptr()), ldx, C.c_void_p(work.data_ptr()), work.numel(),
+            p2p["peers"], st))
+        p2p["hdl"].barrier(channel=0)   # every sender's slabs have landed
+        _check("bf_dist_apply_post", lib().bf_dist_apply_post(self.h, OPS[op], nrhs, C.c_void_p(out.data_ptr()), ldy,
+                                                               C.c_void_p(work.data_ptr()), work.numel(), st))
+        p2p["hdl"].barrier(channel=0)   # every receiver has read them (the next pre may write)
         return out
 
     def time_e2e(self, X_loc_host: torch.Tensor, op: str, steps: int, alg_bytes: int):
