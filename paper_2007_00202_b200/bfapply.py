@@ -291,6 +291,13 @@ class BFHandle:
             C.c_void_p(work.data_ptr()), work.numel(), _stream_handle(stream), evs, len(events)))
         return out
 
+    def graph(self, X: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None,
+              work: Optional[torch.Tensor] = None) -> "ApplyGraph":
+        """Capture one apply on the static buffers X / out / work into a CUDA graph (the whole
+        launch sequence replays with one host call: for small, launch-bound butterflies).
+        Refill X in place and call .replay(); the result lands in .out."""
+        return ApplyGraph(self, X, op, out, work)
+
     def workspace_size_host(self, nrhs: int, op: str = "N") -> int:
         s = C.c_size_t()
         _check("bf_workspace_size_host", lib().bf_workspace_size_host(self.h, OPS[op], nrhs, C.byref(s)))
@@ -351,6 +358,30 @@ def make_hodbf_desc(H, keep: _Keep) -> hodbf_desc:
     return d
 
 
+class ApplyGraph:
+    """One butterfly / HOD-BF apply captured into a torch.cuda.CUDAGraph (see BFHandle.graph)."""
+
+    def __init__(self, h, X: torch.Tensor, op: str, out: Optional[torch.Tensor], work: Optional[torch.Tensor]):
+        nrhs = X.shape[0]
+        rows_out = (h.m if op == "N" else h.n) if hasattr(h, "m") else h.n
+        self.X = X
+        self.out = out if out is not None else torch.empty((nrhs, rows_out), dtype=X.dtype, device=X.device)
+        self.work = work if work is not None else torch.empty(max(h.workspace_size(nrhs), 1), dtype=torch.uint8,
+                                                             device=X.device)
+        s = torch.cuda.Stream(device=X.device)
+        s.wait_stream(torch.cuda.current_stream(X.device))
+        with torch.cuda.stream(s):  # warm-up outside the capture (one-time kernel attributes)
+            h.apply(self.X, op, out=self.out, work=self.work, stream=s)
+        torch.cuda.current_stream(X.device).wait_stream(s)
+        self.g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g):
+            h.apply(self.X, op, out=self.out, work=self.work, stream=torch.cuda.current_stream(X.device))
+
+    def replay(self) -> torch.Tensor:
+        self.g.replay()
+        return self.out
+
+
 class HODBFHandle:
     """An HOD-BF matrix uploaded to one device (hodbf_create)."""
 
@@ -393,6 +424,10 @@ class HODBFHandle:
 
     def rounds(self, op: str = "N"):
         return _rounds(lib().hodbf_rounds, lib().hodbf_round_info, self.h, op)
+
+    def graph(self, X: torch.Tensor, op: str = "N", out=None, work=None) -> ApplyGraph:
+        """See BFHandle.graph."""
+        return ApplyGraph(self, X, op, out, work)
 
     def apply_events(self, X, events, op: str = "N", out=None, work=None, stream=None):
         ldx = _check_rhs(X, self.n, self.code, "X")

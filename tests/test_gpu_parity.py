@@ -275,3 +275,23 @@ def test_host_apply_pipelined(fast):
     torch.cuda.synchronize()
     for X, y, op in zip(Xs, Yh, ops):
         assert oracle.rel_err(y.numpy().T, oracle.apply_op(K, X, op)) <= 1e-12, op
+
+
+@pytest.mark.parametrize("kind", ["generic", "fast", "hodbf"])
+def test_cuda_graph_replay(kind):
+    """An apply captured into a CUDA graph (BFHandle.graph) replays to the direct result,
+    bit for bit, after the static input is refilled."""
+    if kind == "hodbf":
+        H = helmholtz_plane_hodbf(16, 16, 10.0, 1e-4)
+        h, n = pkg.HODBFHandle(H), H.n
+    else:
+        bf = random_butterfly(L=5, leaf=32, r=16 if kind == "fast" else 8, seed=3)
+        h, n = pkg.BFHandle(bf), bf.n
+    X1 = dev(random_rhs(n, 24, seed=1))
+    X2 = dev(random_rhs(n, 24, seed=2))
+    gr = h.graph(X1.clone(), "N")
+    gr.X.copy_(X2)
+    Yg = gr.replay().clone()
+    Yd = h.apply(X2, "N")
+    torch.cuda.synchronize()
+    assert torch.equal(Yg, Yd)

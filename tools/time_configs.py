@@ -36,7 +36,18 @@ def timeit(h, X, op, nrhs, alg, steps=20):
     per = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(len(rounds))] for e in evs]).mean(0)
     detail = [{"ms": round(float(per[i]), 4), "tasks": r["ntasks"], "entries": r["factor_entries"],
                "tflops": round(8 * r["factor_entries"] * nrhs / (per[i] * 1e-3) / 1e12, 2)} for i, r in enumerate(rounds)]
-    return {"ms": ms, "GB/s": alg / ms / 1e6, "rounds": len(rounds), "detail": detail,
+    gr = h.graph(Xd.clone(), op)  # the same apply replayed from a CUDA graph (launch-bound configs)
+    gr.replay()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_graph = e0.elapsed_time(e1) / steps
+    return {"ms": ms, "ms_graph": ms_graph, "GB/s": alg / ms / 1e6, "rounds": len(rounds), "detail": detail,
             "by_kernel": {n: round(float(sum(per[i] for i, r in enumerate(rounds) if r["name"] == n)), 4)
                           for n in sorted({r["name"] for r in rounds})}}
 
