@@ -39,7 +39,7 @@ __device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool ok,
 template <class Pol>
 struct TileCfg {
   using E = typename Pol::E;
-  static constexpr int TR = 32, TC = 64, KC = 16;       // tile rows, columns, K chunk (8 / 32 measured slower)
+  static constexpr int TR = 32, TC = 64, KC = 16;       // tile rows (64: slower), columns, K chunk (8 / 32: slower)
   static constexpr int SA = sizeof(E) == 16 ? 34 : 36;  // padded strides (bank-conflict free
   static constexpr int SB = sizeof(E) == 16 ? 66 : 68;  //   fragment reads)
   static constexpr int STAGE = KC * (SA + SB);          // elements per stage
