@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         // fused row leaf (a5): Y(rows of this slot's leaf) = A (leaf x 16) y (16 x 32), one 16-row
         // group at a time; A records stream through the ring like any op, y is this slot's slab
         const int ds2 = P.d - op.s;
-        const int64_t leaf = ((a << op.s) + (o >> ds2)) + ((b << ds2) + (o & ((1 << ds2) - 1)));  // tau or nu
+        const int64_t leaf = ((a << op.s) + (o >> ds2)) + ((b << ds2) + (o & ((1 << ds2) - 1))) -
+                             P.yleaf_lo;  // tau or nu, relative to the local Y rows
         const int Lf = op.leaf;
         const int64_t base = A.ycontig ? (A.yperm ? A.yperm[leaf * Lf] : leaf * Lf) : 0;
         E* __restrict__ Y = static_cast<E*>(A.Y);

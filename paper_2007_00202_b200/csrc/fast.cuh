@@ -59,6 +59,7 @@ struct FastPass {
   int32_t a_log, b_log;  // the pass's windows: a = a_lo + (w >> b_log), b = b_lo + (w & (2^b_log - 1))
   int32_t wt_log, wn_log;  // exchange: centre tau / nu per peer = 2^(lc - p) / 2^(L - lc - p)
   int64_t a_lo, b_lo;
+  int64_t yleaf_lo;          // fused leaf-out: global index of the first leaf of the local Y rows
   int64_t fbase, win_bytes;  // byte offset of window 0's record, bytes per window record
   int64_t nwin;              // 2^(a_log + b_log)
   int64_t factor_entries, user_in, user_out;  // accounting

@@ -538,7 +538,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   // (a5) is fused into the last window pass as its final op (FK_LEAF_OUT): the pass's output
   // slabs never go to HBM and one launch disappears.
   // (complex128 only: for complex64 the fused op measured no faster than the leaf kernel)
-  const bool fuse_out = !split && sizeof(CT) == 16 && !getenv("BF_NO_FUSE_OUT");
+  const bool fuse_out = sizeof(CT) == 16 && !getenv("BF_NO_FUSE_OUT");
   for (int k = 0; k < np + 2; ++k) {
     if (k == np + 1 && fuse_out) break;
     FastPass P{};
@@ -620,6 +620,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       if (fuse_out && k == np) {
         add(FK_LEAF_OUT, adj ? 0 : d, adj ? lcn : lr);  // U_tau (level L) / conj(Vt_nu)^T (level 0)
         P.out_s = -1;
+        P.yleaf_lo = split ? int64_t(dg) << (L - dp) : 0;  // Y rows are rank-local on a split
       }
     }
     P.nwin = int64_t(1) << (P.a_log + P.b_log);
@@ -1214,7 +1215,7 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       a.ntiles = ntiles;
       a.Y = Y;  // fused leaf-out (last pass)
       a.ldy = ldy;
-      a.yperm = fwd ? h->d_rperm : h->d_cperm;
+      a.yperm = h->dist ? h->d_lperm_out[k] : fwd ? h->d_rperm : h->d_cperm;
       a.conj_io = op == BF_OP_T ? 1 : 0;
       a.ycontig = FP.contig_out ? 1 : 0;
       launch_fast_pass(h->dtype, a, st);

@@ -19,5 +19,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bf
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_leaf -s 2 -c 2 -o $O/full_leaf_$dt $CMD --dtype $dt > /dev/null 2>&1
 done
 timeout 1500 python tools/time_configs.py cfg1 cfg2 cfg3 cfg4 > $O/configs.txt 2> $O/configs.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage_tile -s 4 -c 1 -o $O/full_tile_cfg3 python tools/time_configs.py cfg3 > /dev/null 2>&1
 timeout 900 python tools/time_split.py c128 > $O/split_c128.txt 2>&1
 echo done
