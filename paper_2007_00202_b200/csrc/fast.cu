@@ -40,6 +40,9 @@ struct Stream {
   using Cfg = PassCfg<Pol>;
   static constexpr int S = 1 << D;
   static constexpr int SPP = Cfg::PG / (S * FAST_FRAG);  // k-steps per page
+  static constexpr int SPL = fast_spl((int)sizeof(E), S); // k-steps per page of the column-leaf op
+  static constexpr int XT = SPL * Pol::KS * FAST_NB * (int)sizeof(E);  // X tile bytes per slot
+  __host__ __device__ static int steps_per_page(int kind) { return kind == FK_LEAF_IN ? SPL : SPP; }
   const FastArgs& A;
   unsigned char* ring;
   E* winbuf;
@@ -55,18 +58,37 @@ struct Stream {
     if (item >= nitems) return;
     int r = (int)(j - i * ppi), q = 0;
     for (;; ++q) {
-      const int np = (P.ops[q].nsteps + SPP - 1) / SPP;
+      const int sp = steps_per_page(P.ops[q].kind);
+      const int np = (P.ops[q].nsteps + sp - 1) / sp;
       if (r < np) break;
       r -= np;
     }
-    const int s0 = r * SPP, nst = min(SPP, P.ops[q].nsteps - s0);
+    const FastOp& op = P.ops[q];
+    const int sp = steps_per_page(op.kind);
+    const int s0 = r * sp, nst = min(sp, op.nsteps - s0);
     const int64_t w = item & (P.nwin - 1);  // local window index (records of this rank only)
     const unsigned char* src =
-        static_cast<const unsigned char*>(A.F) + P.fbase + w * P.win_bytes + P.ops[q].off + (int64_t)s0 * S * FAST_FRAG;
+        static_cast<const unsigned char*>(A.F) + P.fbase + w * P.win_bytes + op.off + (int64_t)s0 * S * FAST_FRAG;
     const int slot = (int)(j % Cfg::NP);
+    unsigned char* pg = ring + (size_t)slot * Cfg::PG;
     const uint32_t bytes = (uint32_t)(nst * S * FAST_FRAG);
-    mbar_expect_tx(&full[slot], bytes);
-    bulk_g2s(ring + (size_t)slot * Cfg::PG, src, bytes, &full[slot]);
+    if (op.kind != FK_LEAF_IN) {
+      mbar_expect_tx(&full[slot], bytes);
+      bulk_g2s(pg, src, bytes, &full[slot]);
+      return;
+    }
+    // column leaf: the A records plus, per slot, SPL * KS rows x 32 columns of X (2-D TMA tile)
+    mbar_expect_tx(&full[slot], bytes + S * XT);
+    bulk_g2s(pg, src, bytes, &full[slot]);
+    const int64_t jt = item >> (P.a_log + P.b_log);
+    const int64_t a = P.a_lo + (w >> P.b_log), b = P.b_lo + (w & ((int64_t(1) << P.b_log) - 1));
+    const int ds = P.d - op.s;
+    for (int o = 0; o < S; ++o) {
+      const int64_t leaf = ((a << op.s) + (o >> ds)) + ((b << ds) + (o & ((1 << ds) - 1)));  // tau or nu
+      const int64_t r0 = (A.xperm ? A.xperm[leaf * op.leaf] : leaf * op.leaf) + (int64_t)s0 * Pol::KS;
+      tma_load_2d(pg + SPL * S * FAST_FRAG + o * XT, &A.xmap, (int)(r0 * (int64_t)(sizeof(E) / 8)),
+                  (int)(jt * FAST_NB), &full[slot]);
+    }
   }
   __device__ void issue_window(int64_t i, int wb) const {
     const FastPass& P = A.p;
@@ -118,7 +140,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int diag = A.diag;
   St str{A, ring, winbuf, full, winF, P.nwin * ((A.nrhs + FAST_NB - 1) / FAST_NB), 0};
-  for (int q = 0; q < P.nops; ++q) str.ppi += (P.ops[q].nsteps + SPP - 1) / SPP;
+  for (int q = 0; q < P.nops; ++q) {
+    const int sp = St::steps_per_page(P.ops[q].kind);
+    str.ppi += (P.ops[q].nsteps + sp - 1) / sp;
+  }
   const int64_t nitems = str.nitems;
   const int nwin_log = P.a_log + P.b_log;
   const int64_t bmask = (int64_t(1) << P.b_log) - 1;
@@ -132,7 +157,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
     }
     fence_mbar_init();
     if (!(diag & 1)) {
-      str.issue_window(0, 0);
+      if (P.in_s >= 0) str.issue_window(0, 0);
+      else if (P.xleaf) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&A.xmap)) : "memory");
       for (int j = 0; j < NP; ++j) str.issue_page(j);
     }
   }
@@ -158,12 +184,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++i) {
     const int64_t w = item & ((int64_t(1) << nwin_log) - 1), jt = item >> nwin_log;
     const int64_t a = P.a_lo + (w >> P.b_log), b = P.b_lo + (w & bmask);
-    if (!(diag & 1)) mbar_wait(winF, (uint32_t)(i & 1), 3);
+    if (!(diag & 1) && P.in_s >= 0) mbar_wait(winF, (uint32_t)(i & 1), 3);
     int rd = cur;  // op q reads buffer rd, writes rd ^ 1
     for (int q = 0; q < P.nops; ++q) {
       const FastOp op = P.ops[q];
       const bool last = q == P.nops - 1;
-      if (last && lane == 0 && !(diag & 1)) {
+      if (last && lane == 0 && !(diag & 1) && P.in_s >= 0) {
         // every warp past op q-1 -> buffer rd ^ 1 is free: the last one in loads the next window
         if (atom_add_acqrel(wcnt, 1) == (int)(i + 1) * NACT - 1) str.issue_window(i + 1, rd ^ 1);
       }
@@ -238,6 +264,36 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         cur = rd ^ 1;
         continue;  // (always the last op)
       }
+      if (op.kind == FK_LEAF_IN) {
+        // fused column leaf (a1): z = A (16 x leaf) X(rows of this slot's leaf, tile); every page
+        // carries SPL k-steps of A records and of X rows (the 2-D TMA tiles of Stream::issue_page)
+        constexpr int SPL = St::SPL;
+        const bool cj = A.conj_io != 0;
+        const int cx = half * FAST_HC + c0w;  // first column of this warp inside the 32-column X tile
+        const int n = op.nsteps;
+        for (int s0 = 0; s0 < n; s0 += SPL) {
+          if (!(diag & 1)) mbar_wait(&full[slot], ph, 4);
+          const unsigned char* pg = ring + (size_t)slot * Cfg::PG;
+          const E* xt = reinterpret_cast<const E*>(pg + SPL * S * FAST_FRAG + o * St::XT);
+#pragma unroll
+          for (int st = 0; st < SPL; ++st) {
+            typename Pol::FFrags f;
+            Pol::load_fa(f, pg + (st * S + o) * FAST_FRAG, lane);
+            Pol::load_b_col(f, xt, SPL * Pol::KS, st * Pol::KS, cx, g, t, cj);
+            acc.mac(f);
+          }
+          __syncwarp();
+          if (lane == 0 && !(diag & 1)) {
+            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * NACT - 1) str.issue_page(j + NP);
+          }
+          ++j;
+          if (++slot == NP) {
+            slot = 0;
+            ph ^= 1;
+            ++rnd;
+          }
+        }
+      } else {
       // every op of a pass is a pair op of NSTEP = 32 / KS k-steps (the centre is folded into
       // R^{lc} / W^{lc} at create), so the k-step loop is fully unrolled, software-pipelined
       // across page boundaries: the operands of k-step k + 1 load while k-step k's MMAs issue
@@ -282,6 +338,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
         }
       }
+      }  // pair op
       if (last) {
         if (!(diag & 2)) {
           E* dst;

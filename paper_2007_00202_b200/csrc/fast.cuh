@@ -55,7 +55,8 @@ struct FastPass {
   int32_t nops, in_s, out_s, leaf;  // leaf: 0 window pass, 1 leaf-in launch, 2 leaf-out launch
   int32_t numaj, xin;               // HBM slab order: 0 tau-major (op N), 1 nu-major (op C / T);
                                     // xin / xout: 0 slab buffer, 1 / 2 exchange layout whose
-  int32_t xout, pad;                // peer is the owner of tau / of nu (multi-GPU split)
+  int32_t xout, xleaf;              // peer is the owner of tau / of nu (multi-GPU split);
+                                    // xleaf: op 0 is the column leaf reading X (no window input)
   int32_t a_log, b_log;  // the pass's windows: a = a_lo + (w >> b_log), b = b_lo + (w & (2^b_log - 1))
   int32_t wt_log, wn_log;  // exchange: centre tau / nu per peer = 2^(lc - p) / 2^(L - lc - p)
   int64_t a_lo, b_lo;
@@ -67,7 +68,10 @@ struct FastPass {
 };
 
 struct FastArgs {
+  CUtensorMap xmap;       // xleaf pass: 2-D map over X, box = SPL*KS rows x 32 columns
   FastPass p;
+  const void* X;          // xleaf pass: user block read
+  const int64_t* xperm;   // tree position -> user row (contiguous leaves: only the first row used)
   const void* F;
   const void* Sin;
   void* Sout;
@@ -115,10 +119,17 @@ void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st);
 const char* fast_kernel_name(int dtype);
 // returns false when the leaf launch cannot be configured (shared memory)
 void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st);
+// 2-D TMA map over a column-major (rows x nrhs, ld) complex block, box = brows x 32 (false when
+// the block's base / stride are not 16-byte aligned)
+bool fast_make_xmap(int dtype, const void* X, int64_t rows, int64_t nrhs, int64_t ld, int brows, CUtensorMap* map);
 const char* leaf_kernel_name(int dtype, int mode);
 
 // k-steps per MMA along K: complex128 DMMA m8n8k4 -> 4, complex64 TF32 m16n8k8 -> 8
 __host__ __device__ inline int fast_ks(int csize) { return csize == 16 ? 4 : 8; }
+
+// k-steps per ring page of the fused column-leaf op: each step carries S A records and the S
+// slots' X rows (KS rows x 32 columns each) of a 32 KB page
+__host__ __device__ constexpr int fast_spl(int csize, int S) { return 32768 / (S * (1024 + (csize == 16 ? 4 : 8) * 32 * csize)); }
 
 __host__ __device__ inline int fast_nsteps(int kind, int leaf, int ks) {
   switch (kind) {

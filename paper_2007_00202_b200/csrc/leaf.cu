@@ -186,6 +186,10 @@ static bool make_map(int dtype, const void* base, int64_t rows, int64_t nrhs, in
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool fast_make_xmap(int dtype, const void* X, int64_t rows, int64_t nrhs, int64_t ld, int brows, CUtensorMap* map) {
+  return make_map(dtype, X, rows, nrhs, ld, brows, map);
+}
+
 constexpr size_t LEAF_SMEM = 227 * 1024;
 
 template <class Pol, int MODE>

@@ -444,7 +444,7 @@ static void fill_step(CT* dst, int mg, int ki, Fn A) {
 // op 0 = N (forward), 1 = C (adjoint; conjugate-transposed factor views)
 template <typename CT>
 static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, int opk, size_t* acct,
-                       int dp = -1, int dg = 0) {
+                       int dp = -1, int dg = 0, bool x_contig = false) {
   // dp >= 0: rank dg's share of the split over 2^dp GPUs: the W side (levels
   // 0..lc, leaves of T_S) restricted to the column subtree dg at level dp, the R side (levels
   // lc..L, leaves of T_O) to the row subtree dg; the pass that ends at the centre level writes
@@ -539,8 +539,14 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   // slabs never go to HBM and one launch disappears.
   // (complex128 only: for complex64 the fused op measured no faster than the leaf kernel)
   const bool fuse_out = sizeof(CT) == 16 && !getenv("BF_NO_FUSE_OUT");
+  // The column leaf (a1) can likewise run as the first op of the first pass (FK_LEAF_IN, X rows
+  // by 2-D TMA tiles in the ring pages; needs every leaf to be a run of consecutive user rows),
+  // but measured slower than the separate leaf kernel on config 5 (0.42 vs 0.17 + 0.14 ms: the
+  // X stream outruns the 3-page ring of a 2-level pass), so it is opt-in (env BF_FUSE_IN).
+  const bool fuse_in = sizeof(CT) == 16 && !split && x_contig && getenv("BF_FUSE_IN");
   for (int k = 0; k < np + 2; ++k) {
     if (k == np + 1 && fuse_out) break;
+    if (k == 0 && fuse_in) continue;
     FastPass P{};
     P.L = L;
     std::vector<FastOp> ops;
@@ -601,17 +607,21 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
         P.a_log = l0 - dp;
         P.a_lo = int64_t(dg) << P.a_log;
       }
+      if (fuse_in && k == 1) {
+        add(FK_LEAF_IN, adj ? d : 0, adj ? lr : lcn);  // Vt_nu on X (level 0) / U_tau^H on X (level L)
+        P.xleaf = 1;                                     // window pass whose input is X, not slabs
+      }
       if (!adj) {
         for (int l = l0 + 1; l <= l1 && l <= lc; ++l) add(FK_PAIR_DOWN, l - 1 - l0, 0);  // W_l
         for (int l = std::max(l0, lc); l < l1; ++l) add(FK_PAIR_DOWN, l - l0, 0);      // R_l
-        P.in_s = 0;
+        P.in_s = P.xleaf ? -1 : 0;
         P.out_s = d;
         if (split && l1 == lc) P.xout = 1;  // send z^lc to the owner of tau
         if (split && l0 == lc) P.xin = 2;   // receive from the owner of nu
       } else {
         for (int l = l1 - 1; l >= l0 && l >= lc; --l) add(FK_PAIR_UP, l - l0, 0);        // R^H_l
         for (int l = std::min(l1, lc); l >= l0 + 1; --l) add(FK_PAIR_UP, l - 1 - l0, 0); // W^H_l
-        P.in_s = d;
+        P.in_s = P.xleaf ? -1 : d;
         P.out_s = 0;
         if (split && l0 == lc) P.xout = 2;  // send to the owner of nu
         if (split && l1 == lc) P.xin = 1;   // receive from the owner of tau
@@ -641,7 +651,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     P.factor_entries = off / (int64_t)sizeof(CT) * P.nwin;
     total += off * P.nwin;
     for (int q = 0; q < P.nops; ++q) {
-      if (ops[q].kind == FK_LEAF_IN) P.user_in = P.nwin * ops[q].leaf;
+      if (ops[q].kind == FK_LEAF_IN) P.user_in = P.nwin * ops[q].leaf << P.d;
       if (ops[q].kind == FK_LEAF_OUT) P.user_out = P.nwin * ops[q].leaf << P.d;
     }
     passes.push_back(P);
@@ -1079,19 +1089,19 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
       upload_plan(h->plan[k], pb, 0, (int)pb.tasks.size(), &h->device_bytes);
     }
     if (fast_eligible(G, d->dtype) && !getenv("BF_DISABLE_FAST")) {
+      const bool cc = leaves_contiguous(d->col_perm, d->n, G.nv(0));
+      const bool rc = leaves_contiguous(d->row_perm, d->m, G.mt(0));
       if (d->dtype == BF_C128) {
         HostFactors<double2> HF{static_cast<const double2*>(d->U), static_cast<const double2*>(d->R),
                                 static_cast<const double2*>(d->B), static_cast<const double2*>(d->W),
                                 static_cast<const double2*>(d->Vt)};
-        for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
+        for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes, -1, 0, k == 0 ? cc : rc);
       } else {
         HostFactors<float2> HF{static_cast<const float2*>(d->U), static_cast<const float2*>(d->R),
                                static_cast<const float2*>(d->B), static_cast<const float2*>(d->W),
                                static_cast<const float2*>(d->Vt)};
         for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
       }
-      const bool cc = leaves_contiguous(d->col_perm, d->n, G.nv(0));
-      const bool rc = leaves_contiguous(d->row_perm, d->m, G.mt(0));
       h->fast[0].contig_in = cc;
       h->fast[0].contig_out = rc;
       h->fast[1].contig_in = rc;
@@ -1213,6 +1223,14 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       a.nlev = h->G.nb;
       a.nrhs = (int32_t)nrhs;
       a.ntiles = ntiles;
+      if (P.xleaf) {  // fused column leaf: X rows by 2-D TMA tiles
+        const int S = 1 << P.d, cs = (int)csize(h->dtype);
+        const int64_t rows = P.user_in;
+        require(fast_make_xmap(h->dtype, X, rows, nrhs, ldx, fast_spl(cs, S) * fast_ks(cs), &a.xmap), BF_ERR_ARG,
+                "X must be 16-byte aligned with a 16-byte multiple column stride");
+        a.X = X;
+        a.xperm = fwd ? h->d_cperm : h->d_rperm;
+      }
       a.Y = Y;  // fused leaf-out (last pass)
       a.ldy = ldy;
       a.yperm = h->dist ? h->d_lperm_out[k] : fwd ? h->d_rperm : h->d_cperm;

@@ -158,3 +158,23 @@ def test_fused_leaf_out_equals_separate(monkeypatch, dtype):
     Y2, Y2c = h2.apply(X, "N"), h2.apply(X, "C")
     torch.cuda.synchronize()
     assert torch.equal(Y1, Y2) and torch.equal(Y1c, Y2c)
+
+
+@pytest.mark.parametrize("L,leaf", [(6, 32), (5, 64), (7, 16)])
+def test_fused_leaf_in_equals_separate(monkeypatch, L, leaf):
+    """complex128, contiguous leaves: the column leaf fused into the first window pass (X rows by
+    2-D TMA tiles in the ring pages) equals the separate leaf kernel bit for bit, op N / C / T."""
+    bf = random_butterfly(L=L, leaf=leaf, r=16, seed=L + leaf)
+    K = oracle.bf_dense(bf)
+    monkeypatch.setenv("BF_FUSE_IN", "1")  # opt-in (measured slower on config 5, DESIGN.md)
+    h1 = pkg.BFHandle(bf)
+    assert h1.rounds("N")[0]["name"].startswith("k_bf_pass"), h1.rounds("N")
+    monkeypatch.delenv("BF_FUSE_IN")
+    h2 = pkg.BFHandle(bf)
+    assert h2.rounds("N")[0]["name"].startswith("k_leaf")
+    for op, nr in (("N", 32), ("C", 45), ("T", 7)):
+        X = dev(random_rhs(bf.n, nr, seed=nr))
+        Y1, Y2 = h1.apply(X, op), h2.apply(X, op)
+        torch.cuda.synchronize()
+        assert oracle.rel_err(host(Y1), oracle.apply_op(K, host(X), op)) <= 1e-12, op
+        assert torch.equal(Y1, Y2), op
