@@ -187,7 +187,8 @@ int bf_dist_exchange_blocks(bf_handle h, int op, int64_t* n_send, int64_t* send_
  * consecutive elements (row-major, nrhs fastest) in bf_dist_exchange_blocks order.  1 (uniform
  * rank-16 butterflies, fused kernels): each peer's chunk is [rhs tile of 32][column half of 16]
  * [block, in bf_dist_exchange_blocks order][16 rows][16 columns], the 16 x 16 half slab stored
- * with the kernels' bank swizzle (element (r, c) at r*16 + (c ^ swz(r))); nrhs is padded to a
+ * in the kernels' half-slab layout (complex128: element (r, c) at r*16 + (c ^ swz(r)); complex64:
+ * MMA-fragment order [r/8][re | im][lane][4] floats, see mma.cuh PolC64T); nrhs is padded to a
  * multiple of 32.  Either way the regions are moved as opaque bytes by the all-to-all. */
 int bf_dist_slab_format(bf_handle h, int32_t* fmt);
 int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out,

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         sp0 = win + (((2 * tt) << (ds - 1)) + (u >> 1)) * FAST_HSLAB;
         sp1 = win + (((2 * tt + 1) << (ds - 1)) + (u >> 1)) * FAST_HSLAB;
       }
-      if (op.kind == FK_LEAF_OUT) {
+      if (Pol::LEAF_OPS && op.kind == FK_LEAF_OUT) {
+        if constexpr (Pol::LEAF_OPS) {
         // fused row leaf (a5): Y(rows of this slot's leaf) = A (leaf x 16) y (16 x 32), one 16-row
         // group at a time; A records stream through the ring like any op, y is this slot's slab
         const int ds2 = P.d - op.s;
@@ -261,10 +262,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
             ++rnd;
           }
         }
+        }
         cur = rd ^ 1;
         continue;  // (always the last op)
       }
-      if (op.kind == FK_LEAF_IN) {
+      if (Pol::LEAF_OPS && op.kind == FK_LEAF_IN) {
+        if constexpr (Pol::LEAF_OPS) {
         // fused column leaf (a1): z = A (16 x leaf) X(rows of this slot's leaf, tile); every page
         // carries SPL k-steps of A records and of X rows (the 2-D TMA tiles of Stream::issue_page)
         constexpr int SPL = St::SPL;
@@ -293,6 +296,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
             ++rnd;
           }
         }
+        }
       } else {
       // every op of a pass is a pair op of NSTEP = 32 / KS k-steps (the centre is folded into
       // R^{lc} / W^{lc} at create), so the k-step loop is fully unrolled, software-pipelined
@@ -302,7 +306,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
       static_assert(NSTEP % SPO == 0, "pages must split ops evenly");
       auto bsrc = [&](int k) { return (k < KPS ? sp0 : sp1) + (k & (KPS - 1)) * Pol::KS * FAST_HC; };
       if (!(diag & 1)) mbar_wait(&full[slot], ph, 4);
-      const unsigned char* pgn = ring + (size_t)slot * Cfg::PG + o * FAST_FRAG;
+      const int roff = o * FAST_FRAG + Pol::rec_off(c0w);  // the warp's part of its slot's records
+      const unsigned char* pgn = ring + (size_t)slot * Cfg::PG + roff;
       int nslot = slot;
       uint32_t nph = ph;
       typename Pol::FFrags f[2];
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
               nph ^= 1;
             }
             if (!(diag & 1)) mbar_wait(&full[nslot], nph, 4);
-            pgn = ring + (size_t)nslot * Cfg::PG + o * FAST_FRAG;
+            pgn = ring + (size_t)nslot * Cfg::PG + roff;
           }
           Pol::load_fa(f[k1 & 1], pgn + (k1 % SPO) * S * FAST_FRAG, lane);
           Pol::load_b(f[k1 & 1], bsrc(k1), bo);
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           } else {
             dst = Sout + pass_slab_off(P, P.xout, jt, half, A.nlev, A.ntiles, a, b, P.out_s, o);
           }
-          acc.each(g, t, [&](int r, int c, E v) { dst[r * FAST_HC + ((c0w + c) ^ Pol::swz(r))] = v; });
+          Pol::store_slab(acc, dst, c0w, g, t, lane);
         }
         cur = rd ^ 1;
       } else {
@@ -358,12 +363,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           // op 0 writes the buffer the previous item's last op read: the half must be past it
           if (q == 0) named_sync(hbar, NACTH * 32);
           E* dst = winbuf + (rd ^ 1) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
-          acc.each(g, t, [&](int r, int c, E v) { dst[r * FAST_HC + ((c0w + c) ^ Pol::swz(r))] = v; });
+          Pol::store_slab(acc, dst, c0w, g, t, lane);
           // the next (pair) op reads other slots: their writes must be visible
           named_sync(hbar, NACTH * 32);
         } else if (diag & 8) {  // profiling: epilogue stores without the barriers
           E* dst = winbuf + (rd ^ 1) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
-          acc.each(g, t, [&](int r, int c, E v) { dst[r * FAST_HC + ((c0w + c) ^ Pol::swz(r))] = v; });
+          Pol::store_slab(acc, dst, c0w, g, t, lane);
         } else {  // profiling: keep the accumulators live without any epilogue
           float sink = 0.f;
           acc.each(g, t, [&](int r, int c, E v) { sink += (float)v.x; });
@@ -404,9 +409,9 @@ void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
     else if (d == 2) launch_one<PolC128<2>, 2>(a, grid, st);  // 8 warps x 16 columns: 3 % faster than 16 x 8
     else launch_one<PolC128<1>, 1>(a, grid, st);
   } else {
-    if (d == 3) launch_one<PolC64<2>, 3>(a, grid, st);
-    else if (d == 2) launch_one<PolC64<1>, 2>(a, grid, st);
-    else launch_one<PolC64<1>, 1>(a, grid, st);
+    if (d == 3) launch_one<PolC64T<2>, 3>(a, grid, st);
+    else if (d == 2) launch_one<PolC64T<1>, 2>(a, grid, st);
+    else launch_one<PolC64T<1>, 1>(a, grid, st);
   }
 }
 

@@ -142,7 +142,8 @@ __host__ __device__ inline int fast_nsteps(int kind, int leaf, int ks) {
 }
 
 // HBM ping-pong slab buffers: [rhs tile jt][column half][slab index][16 rows x 16 columns], each
-// half slab swizzled like the shared-memory copies (element (r, c) at r * 16 + (c ^ swz(r))).
+// half slab laid out like the shared-memory copies (complex128: element (r, c) at
+// r * 16 + (c ^ swz(r)); complex64: the MMA-fragment order of mma.cuh PolC64T).
 __host__ __device__ inline int64_t half_slab_off(int64_t jt, int half, int64_t nlev, int64_t idx) {
   return ((jt * 2 + half) * nlev + idx) * FAST_HSLAB;
 }

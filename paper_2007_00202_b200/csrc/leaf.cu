@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
   const bool cj = A.conj_io != 0;
   int bo[NT];  // B-fragment offsets in the two half slabs [half][16 x 16] (OUT)
 #pragma unroll
-  for (int ni = 0; ni < NT; ++ni) bo[ni] = (ni >> 1) * FAST_HSLAB + Pol::boff(t, g, 8 * (ni & 1), 0);
+  for (int ni = 0; ni < NT; ++ni) bo[ni] = Pol::leaf_boff(ni, t, g);
   int64_t c = 0;  // chunk sequence number
   for (int64_t item = blockIdx.x + (int64_t)warp * gridDim.x; item < nitems; item += (int64_t)nw * gridDim.x) {
     const int64_t leaf = item % A.nleaf, jt = item / A.nleaf;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
       E* dst0 = static_cast<E*>(A.Sout) + half_slab_off(jt, 0, A.nlev, A.leaf_lo + leaf);
       E* dst1 = static_cast<E*>(A.Sout) + half_slab_off(jt, 1, A.nlev, A.leaf_lo + leaf);
       acc.each(g, t, [&](int r, int cc, E v) {
-        (cc < FAST_HC ? dst0 : dst1)[r * FAST_HC + ((cc & (FAST_HC - 1)) ^ Pol::swz(r))] = v;
+        Pol::slab_put(cc < FAST_HC ? dst0 : dst1, r, cc & (FAST_HC - 1), v);
       });
     }
   }

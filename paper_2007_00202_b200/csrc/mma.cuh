@@ -119,9 +119,22 @@ struct PolC128 {
     double2 b[NT];
     double bs[NT];
   };
+  static constexpr bool LEAF_OPS = true;  // the pass kernel may run the fused leaf ops
   // lane-constant element offset of B row t, n-tile ni (k0 = 0) inside a half slab
   __device__ static __forceinline__ int boff(int t, int g, int c0w, int ni) {
     return t * FAST_HC + ((c0w + 8 * ni + g) ^ swz(t));
+  }
+  // leaf kernels: n-tile ni of the 32-column tile = [half ni / 2][columns 8 (ni & 1) ..]
+  __device__ static __forceinline__ int leaf_boff(int ni, int t, int g) {
+    return (ni >> 1) * FAST_HSLAB + boff(t, g, 8 * (ni & 1), 0);
+  }
+  // byte offset of the warp's part of a factor record (all of it)
+  __device__ static __forceinline__ int rec_off(int) { return 0; }
+  // half-slab element (r, c): r * 16 + (c ^ swz(r))
+  __device__ static __forceinline__ void slab_put(E* hs, int r, int c, E v) { hs[r * FAST_HC + (c ^ swz(r))] = v; }
+  template <class Ac>
+  __device__ static __forceinline__ void store_slab(const Ac& acc, E* hs, int c0w, int g, int t, int) {
+    acc.each(g, t, [&](int r, int c, E v) { slab_put(hs, r, c0w + c, v); });
   }
   __device__ static __forceinline__ void load_a(Frags& f, const unsigned char* rec, int lane) {
     const E* p = reinterpret_cast<const E*>(rec);
@@ -238,11 +251,13 @@ struct PolC128 {
 };
 
 // ======================================================================================
-// complex64 policy: 3xTF32 mma.sync m16n8k8, fragments (lane = 4g + t):
+// complex64 policy (leaf kernels): 3xTF32 mma.sync m16n8k8, fragments (lane = 4g + t):
 //   A (16x8): a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]
 //   B (8x8):  b0 = B[t][g], b1 = B[t+4][g];   C (16x8): c0,c1 = C[g][2t+e], c2,c3 = C[g+8][2t+e]
-// One k-step record (1 KB): [2][lane][2] float2 for the 16 x 8 block (two lane-contiguous halves).  The A operand is split into
-// TF32 hi / lo parts once per k-step (load_a); B per n-tile inside mac().
+// One k-step record (1 KB): [re | im][lane][a0..a3] floats (planar: each plane one lane-
+// contiguous 16-byte load straight into the MMA's A registers).  Column-leaf records (B = X)
+// use the natural K order; row-leaf records (B = a slab) the slab's K order kappa = t <-> row
+// 2t, kappa = t + 4 <-> row 2t + 1 (see PolC64T for the complex64 half-slab layout).
 // ======================================================================================
 template <int NT_>
 struct PolC64 {
@@ -274,24 +289,38 @@ struct PolC64 {
   __device__ static __forceinline__ int boff(int t, int g, int c0w, int ni) {
     return t * FAST_HC + ((c0w + 8 * ni + g) ^ swz(t));  // row t + 4 is +4*16 (same swizzle)
   }
+  static constexpr bool LEAF_OPS = true;
   __device__ static __forceinline__ void load_a(Frags& f, const unsigned char* rec, int lane) {
     const float4* p = reinterpret_cast<const float4*>(rec);
-    const float4 x = p[lane], y = p[32 + lane];  // lane-contiguous halves: no bank conflicts
-    const float2 v[4] = {make_float2(x.x, x.y), make_float2(x.z, x.w), make_float2(y.x, y.y), make_float2(y.z, y.w)};
+    const float4 x = p[lane], y = p[32 + lane];  // re / im planes
+    const float re[4] = {x.x, x.y, x.z, x.w}, im[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      split(v[e].x, f.ah[0][e], f.al[0][e]);
-      split(v[e].y, f.ah[1][e], f.al[1][e]);
-      split(v[e].x + v[e].y, f.ah[2][e], f.al[2][e]);
+      split(re[e], f.ah[0][e], f.al[0][e]);
+      split(im[e], f.ah[1][e], f.al[1][e]);
+      split(re[e] + im[e], f.ah[2][e], f.al[2][e]);
     }
+  }
+  // leaf kernels: float offset of n-tile ni's B values in the two half slabs (PolC64T layout):
+  // lane (g, t)'s own fragment, component (ni & 1) = column g / g + 8, rows 2t (+0) / 2t+1 (+2)
+  __device__ static __forceinline__ int leaf_boff(int ni, int t, int g) {
+    return 2 * (ni >> 1) * FAST_HSLAB + 4 * (4 * g + t) + (ni & 1);
   }
   template <class F>
   __device__ static __forceinline__ void load_b(F& f, const E* slab_k0, const int (&bo)[NT]) {
+    const float* s = reinterpret_cast<const float*>(slab_k0);
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
-      f.b[ni][0] = slab_k0[bo[ni]];
-      f.b[ni][1] = slab_k0[bo[ni] + 4 * FAST_HC];
+      f.b[ni][0] = make_float2(s[bo[ni]], s[bo[ni] + 128]);
+      f.b[ni][1] = make_float2(s[bo[ni] + 2], s[bo[ni] + 130]);
     }
+  }
+  // half-slab element (r, c) in the PolC64T layout
+  __device__ static __forceinline__ void slab_put(E* hs, int r, int c, E v) {
+    const int kb = r >> 3, t = (r & 7) >> 1, lane = 4 * (c & 7) + t, comp = (c >> 3) + 2 * (r & 1);
+    float* f = reinterpret_cast<float*>(hs) + kb * 256 + 4 * lane + comp;
+    f[0] = v.x;
+    f[128] = v.y;
   }
   template <class F>
   __device__ static __forceinline__ void load_b_col(F& f, const E* box, int ldb, int k0, int c0w, int g, int t,
@@ -417,6 +446,117 @@ struct PolC64 {
         for (int e = 0; e < 4; ++e) fn(g + 8 * (e >> 1), 8 * ni + 2 * t + (e & 1), make_float2(p[0][ni][e], p[1][ni][e]));
     }
   };
+};
+
+// ======================================================================================
+// complex64 window-pass policy, transposed product: out^T (16 columns x 8NT rows) =
+// slab^T (16 columns x K) * F^T (K x 8NT rows), i.e. M = the 16 rhs columns of a half slab,
+// N = output rows, K = input rows.  Both operands then load straight into their MMA registers
+// (the slab's re / im planes: one lane-contiguous 16-byte load each; the factor: one per n-tile)
+// and the accumulator tile of lane (g, t) is exactly the slab fragment lane (g, t) loads in the
+// next op, so the epilogue is two 16-byte stores per n-tile.  (The row-major formulation needed
+// ~50 % more instructions per HMMA: register moves to assemble re / im operand pairs from
+// interleaved complex loads, tools/tf32_loop.cu: 168 vs 201 TF of HMMA issue.)
+// K order inside a k-step: kappa = t <-> row 2t, kappa = t + 4 <-> row 2t + 1.
+// complex64 half slab (HBM and shared memory, 2 KB): [kb = row / 8][re | im][lane][4] floats,
+//   lane (g, t): (row 8kb + 2t, col g), (8kb + 2t, g + 8), (8kb + 2t + 1, g), (8kb + 2t + 1, g + 8).
+// Factor record (1 KB per k-step and slot): [j = output row / 8][lane][re b0, re b1, im b0, im b1],
+//   b0 = F(8j + g, 8ki + 2t), b1 = F(8j + g, 8ki + 2t + 1).
+// ======================================================================================
+template <int NT_>
+struct PolC64T {
+  using E = float2;
+  static constexpr int KS = 8;
+  static constexpr int NT = NT_;  // 8-row n-tiles per warp (NT = 1: the warp's c0w / 8 selects which)
+  static constexpr bool LEAF_OPS = false;
+  __device__ static __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) { PolC64<1>::split(x, hi, lo); }
+  __device__ static __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    PolC64<1>::mma(c, a, b);
+  }
+  struct Frags {
+    float4 sr, si;   // slab fragment (A role): re, im
+    float4 f[NT];    // factor fragments (B role): re b0, re b1, im b0, im b1
+  };
+  struct Acc;
+  using FFrags = Frags;
+  using FAcc = Acc;
+  __device__ static __forceinline__ int boff(int t, int g, int, int) { return 4 * g + t; }  // = lane
+  __device__ static __forceinline__ int rec_off(int c0w) { return (c0w >> 3) * 512; }
+  __device__ static __forceinline__ void load_fa(Frags& f, const unsigned char* rec, int lane) {
+    const float4* p = reinterpret_cast<const float4*>(rec);
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) f.f[ni] = p[ni * 32 + lane];
+  }
+  __device__ static __forceinline__ void load_b(Frags& f, const E* slab_k0, const int (&bo)[NT]) {
+    const float4* p = reinterpret_cast<const float4*>(slab_k0);
+    f.sr = p[bo[0]];
+    f.si = p[32 + bo[0]];
+  }
+  struct Acc {
+    float p[3][NT][4];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) p[q][ni][e] = 0.f;
+    }
+    __device__ __forceinline__ void mac(const Frags& f) {
+      uint32_t ah[3][4], al[3][4];
+      const float re[4] = {f.sr.x, f.sr.y, f.sr.z, f.sr.w}, im[4] = {f.si.x, f.si.y, f.si.z, f.si.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        split(re[e], ah[0][e], al[0][e]);
+        split(im[e], ah[1][e], al[1][e]);
+        split(re[e] + im[e], ah[2][e], al[2][e]);
+      }
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) {
+        uint32_t bh[3][2], bl[3][2];
+        const float br[2] = {f.f[ni].x, f.f[ni].y}, bi[2] = {f.f[ni].z, f.f[ni].w};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          split(br[e], bh[0][e], bl[0][e]);
+          split(bi[e], bh[1][e], bl[1][e]);
+          split(br[e] + bi[e], bh[2][e], bl[2][e]);
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          mma(p[q][ni], ah[q], bl[q]);
+          mma(p[q][ni], al[q], bh[q]);
+          mma(p[q][ni], ah[q], bh[q]);
+        }
+      }
+    }
+    // every output element: fn(row of the warp's n-tiles, column in the half, value)
+    template <typename Fn>
+    __device__ __forceinline__ void each(int g, int t, Fn fn) const {
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p1 = p[0][ni][e], p2 = p[1][ni][e], p3 = p[2][ni][e];
+          fn(8 * ni + 2 * t + (e & 1), g + 8 * (e >> 1), make_float2(p1 - p2, p3 - p1 - p2));
+        }
+    }
+  };
+  // the warp's output rows 8 (c0w / 8 + ni) .. of the half slab: two 16-byte stores per n-tile
+  __device__ static __forceinline__ void store_slab(const Acc& acc, E* hs, int c0w, int, int, int lane) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      float re[4], im[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float p1 = acc.p[0][ni][e], p2 = acc.p[1][ni][e], p3 = acc.p[2][ni][e];
+        re[e] = p1 - p2;
+        im[e] = p3 - p1 - p2;
+      }
+      float4* d = reinterpret_cast<float4*>(hs + ((c0w >> 3) + ni) * 128);
+      d[lane] = make_float4(re[0], re[2], re[1], re[3]);
+      d[32 + lane] = make_float4(im[0], im[2], im[1], im[3]);
+    }
+  }
 };
 
 }  // namespace bfa

@@ -416,27 +416,46 @@ static inline CT cj(CT v, bool c) {
 }
 
 // one 1 KB k-step record of an M x K operand: row group mg (16 rows), k-step ki, in the MMA
-// fragment order the pass kernel consumes.
+// fragment order the kernels consume (mma.cuh).
 // complex128 (mma m8n8k4, KS = 4): [mi][lane], lane = 4g + t <-> (row 16mg + 8mi + g, col 4ki + t)
-// complex64 (mma m16n8k8, KS = 8): [h][lane][e2], (h, e2) = (0,0) (g, t), (0,1) (g+8, t),
-//                                  (1,0) (g, t+4), (1,1) (g+8, t+4) of the 16 x 8 block at rows
-//                                  16mg, cols 8ki (each half one conflict-free 16-byte load/lane)
+// complex64 (mma m16n8k8, KS = 8), `mode`:
+//   REC_A_NAT  (column-leaf records, B = X): [re | im][lane][a0..a3], a0..a3 = (g, t), (g+8, t),
+//              (g, t+4), (g+8, t+4) of the 16 x 8 block at rows 16mg, cols 8ki
+//   REC_A_PAIR (row-leaf records, B = a slab): as REC_A_NAT with K order kappa = t <-> col 2t,
+//              kappa = t + 4 <-> col 2t + 1 (the complex64 slab's K order)
+//   REC_B_T    (window-pass records, PolC64T: the factor is the B operand of out^T = slab^T F^T):
+//              [j][lane][re b0, re b1, im b0, im b1], b0 = (8j + g, 8ki + 2t), b1 = (8j + g, 8ki + 2t + 1)
+enum { REC_A_NAT = 0, REC_A_PAIR = 1, REC_B_T = 2 };
 template <typename CT, typename Fn>
-static void fill_step(CT* dst, int mg, int ki, Fn A) {
+static void fill_step(CT* dst, int mg, int ki, Fn A, int mode) {
   if (sizeof(CT) == 16) {
     for (int mi = 0; mi < 2; ++mi)
       for (int lane = 0; lane < 32; ++lane) {
         const int g = lane >> 2, t = lane & 3;
         dst[mi * 32 + lane] = A(16 * mg + 8 * mi + g, 4 * ki + t);
       }
-  } else {
-    for (int lane = 0; lane < 32; ++lane) {
-      const int g = lane >> 2, t = lane & 3;
-      // two 512-byte halves, each read by one lane-contiguous 16-byte load per lane
-      dst[2 * lane + 0] = A(16 * mg + g, 8 * ki + t);
-      dst[2 * lane + 1] = A(16 * mg + g + 8, 8 * ki + t);
-      dst[64 + 2 * lane + 0] = A(16 * mg + g, 8 * ki + t + 4);
-      dst[64 + 2 * lane + 1] = A(16 * mg + g + 8, 8 * ki + t + 4);
+    return;
+  }
+  auto* f = reinterpret_cast<decltype(dst->x)*>(dst);
+  for (int lane = 0; lane < 32; ++lane) {
+    const int g = lane >> 2, t = lane & 3;
+    if (mode == REC_B_T) {
+      for (int j = 0; j < 2; ++j) {
+        const CT v0 = A(8 * j + g, 8 * ki + 2 * t), v1 = A(8 * j + g, 8 * ki + 2 * t + 1);
+        auto* q = f + (j * 32 + lane) * 4;
+        q[0] = v0.x;
+        q[1] = v1.x;
+        q[2] = v0.y;
+        q[3] = v1.y;
+      }
+      continue;
+    }
+    const int k0 = mode == REC_A_PAIR ? 2 * t : t, k1 = mode == REC_A_PAIR ? 2 * t + 1 : t + 4;
+    const CT a[4] = {A(16 * mg + g, 8 * ki + k0), A(16 * mg + g + 8, 8 * ki + k0), A(16 * mg + g, 8 * ki + k1),
+                     A(16 * mg + g + 8, 8 * ki + k1)};
+    for (int e = 0; e < 4; ++e) {
+      f[4 * lane + e] = a[e].x;
+      f[128 + 4 * lane + e] = a[e].y;
     }
   }
 }
@@ -680,10 +699,10 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
             for (int st = 0; st < op.nsteps; ++st) {
               if (!adj) {
                 const CT* V = H.Vt + G.vt_off[nu];
-                fill_step(rec(st), 0, st, [&](int i, int k) { return V[i + k * 16]; });
+                fill_step(rec(st), 0, st, [&](int i, int k) { return V[i + k * 16]; }, REC_A_NAT);
               } else {
                 const CT* U = H.U + G.u_off[tau];
-                fill_step(rec(st), 0, st, [&](int i, int k) { return cj(U[k + (int64_t)i * lr], true); });
+                fill_step(rec(st), 0, st, [&](int i, int k) { return cj(U[k + (int64_t)i * lr], true); }, REC_A_NAT);
               }
             }
           } else if (op.kind == FK_LEAF_OUT) {
@@ -693,24 +712,24 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
               const int mg = st / kpm, ki = st % kpm;
               if (!adj) {
                 const CT* U = H.U + G.u_off[tau];
-                fill_step(rec(st), mg, ki, [&](int i, int k) { return U[i + (int64_t)k * lr]; });
+                fill_step(rec(st), mg, ki, [&](int i, int k) { return U[i + (int64_t)k * lr]; }, REC_A_PAIR);
               } else {
                 const CT* V = H.Vt + G.vt_off[nu];
-                fill_step(rec(st), mg, ki, [&](int i, int k) { return cj(V[k + i * 16], true); });
+                fill_step(rec(st), mg, ki, [&](int i, int k) { return cj(V[k + i * 16], true); }, REC_A_PAIR);
               }
             }
           } else if (op.kind == FK_DIAG) {
             blk(op.s, tau, nu);
             const CT* Bb = H.B + G.b_off[G.idx(lc, tau, nu)];
             for (int st = 0; st < op.nsteps; ++st)
-              fill_step(rec(st), 0, st, [&](int i, int k) { return adj ? cj(Bb[k + i * 16], true) : Bb[i + k * 16]; });
+              fill_step(rec(st), 0, st, [&](int i, int k) { return adj ? cj(Bb[k + i * 16], true) : Bb[i + k * 16]; }, REC_B_T);
           } else if (op.kind == FK_PAIR_DOWN) {
             blk(op.s + 1, tau, nu);  // output block at level l0 + s + 1
             const int l = P.l0 + op.s + 1;
             if (l <= lc) {  // W_l
               const CT* Wb = Wblk(l, G.idx(l, tau, nu));
               for (int st = 0; st < op.nsteps; ++st)
-                fill_step(rec(st), 0, st, [&](int i, int k) { return Wb[i + k * 16]; });
+                fill_step(rec(st), 0, st, [&](int i, int k) { return Wb[i + k * 16]; }, REC_B_T);
             } else {  // R_{l-1}, gather form
               const int lr_ = l - 1;
               const int part = (int)(tau & 1);
@@ -720,7 +739,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
                 fill_step(rec(st), 0, st, [&](int i, int k) {
                   const CT* Rs = k < 16 ? R0 : R1;
                   return Rs[(part * 16 + i) + (k & 15) * 32];
-                });
+                }, REC_B_T);
             }
           } else {  // FK_PAIR_UP: output block at level l = l0 + s
             blk(op.s, tau, nu);
@@ -731,7 +750,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
                 fill_step(rec(st), 0, st, [&](int i, int k) {
                   const int pp = k >> 4;
                   return cj(Rb[(pp * 16 + (k & 15)) + i * 32], true);
-                });
+                }, REC_B_T);
             } else {  // W^H_{l+1}: inputs (2tau + p, nu >> 1) at level l + 1, column part nu & 1
               const int lw = l + 1;
               const CT* W0 = Wblk(lw, G.idx(lw, 2 * tau, nu >> 1));
@@ -741,7 +760,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
                 fill_step(rec(st), 0, st, [&](int i, int k) {
                   const CT* Ws = k < 16 ? W0 : W1;
                   return cj(Ws[(k & 15) + (cp * 16 + i) * 16], true);
-                });
+                }, REC_B_T);
             }
           }
         }
