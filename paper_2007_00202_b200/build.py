@@ -28,7 +28,8 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC] + FLAGS + SRC + ["-o", LIB + ".tmp"]
+    extra = os.environ.get("BF_NVCC_EXTRA", "").split()  # experiments: e.g. -DBF_C64_NP=5
+    cmd = [NVCC] + FLAGS + extra + SRC + ["-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

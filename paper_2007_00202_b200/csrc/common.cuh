@@ -1,6 +1,7 @@
 // Shared definitions of libbfapply (host + device).
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include <string>
@@ -75,6 +76,28 @@ struct StageArgs {
 };
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);
+
+// Launch with programmatic stream serialization (PDL, see mma.cuh pdl_wait) unless env BF_NO_PDL
+// is set; the kernel must call pdl_wait() before touching stream-ordered memory.
+inline bool pdl_enabled() {
+  static const bool on = getenv("BF_NO_PDL") == nullptr;
+  return on;
+}
+template <typename Arg>
+inline void launch_pdl(void (*kernel)(Arg), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       const Arg& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, a);
+}
 const char* round_kernel_name(int dtype, const Round& r, int* id);
 
 }  // namespace bfa

@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
     for (int i = 0; i < A.nst; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
+  pdl_wait();  // X / slabs are written by earlier stream work
+  pdl_trigger();
   __syncthreads();
   if (warp >= nw) return;
   unsigned char* mystages = smem + (size_t)warp * dep * stage;
@@ -223,7 +225,7 @@ static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
   }
   const int64_t items = a.nleaf * ((a.nrhs + FAST_NB - 1) / FAST_NB);
   const unsigned grid = (unsigned)(items < nsm ? items : nsm);
-  k_leaf<Pol, MODE><<<grid, LEAF_THREADS, smem, st>>>(a);
+  launch_pdl(k_leaf<Pol, MODE>, grid, LEAF_THREADS, smem, st, a);
 }
 
 void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {

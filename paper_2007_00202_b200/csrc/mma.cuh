@@ -89,6 +89,14 @@ __device__ __forceinline__ double conj_im(double x, bool cj) {
 __device__ __forceinline__ float conj_im(float x, bool cj) {
   return __int_as_float(__float_as_int(x) ^ ((int)cj << 31));
 }
+// Programmatic dependent launch (PDL): the fused-path kernels are launched with programmatic
+// stream serialization, so the next launch's CTAs start (barrier init, factor prefetch) on SMs
+// this grid's tail frees.  pdl_wait() returns once every earlier grid on the stream has completed
+// and its memory is visible -- no thread touches memory earlier stream work may write or read
+// (slabs, X, Y) before it; factor records are immutable after create and may be read before.
+// Both are no-ops for a launch without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 // named barrier over `nthreads` threads (ids >= 1; 0 is __syncthreads)
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
