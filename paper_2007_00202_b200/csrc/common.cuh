@@ -73,6 +73,7 @@ struct StageArgs {
   int32_t out_kind;
   int32_t conj_flip;
   int32_t nrhs;
+  int32_t m3;  // 3M complex products (0: 4M, exact on selection factors)
 };
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);

@@ -115,10 +115,19 @@ struct Stream {
       E* dst = winbuf + wb * Cfg::WIN + h * Cfg::WINH;
       if (!P.xin) {  // the window's input slabs are contiguous in the slab buffer
         bulk_g2s(dst, Sin + pass_slab_off(P, 0, jt, h, A.nlev, A.ntiles, a, b, P.in_s, 0), bytes, winF);
-      } else {       // exchange layout: the slabs may come from several peers' chunks
-        for (int o = 0; o < S; ++o)
-          bulk_g2s(dst + o * FAST_HSLAB, Sin + pass_slab_off(P, P.xin, jt, h, A.nlev, A.ntiles, a, b, P.in_s, o),
-                   (uint32_t)(FAST_HSLAB * sizeof(E)), winF);
+      } else {  // exchange layout: the slabs may come from several peers' chunks
+        int p0 = 0, p1 = 0;
+        const int64_t o0 = pass_slab_off(P, P.xin, jt, h, A.nlev, A.ntiles, a, b, P.in_s, 0, -1, &p0);
+        const int64_t o1 = pass_slab_off(P, P.xin, jt, h, A.nlev, A.ntiles, a, b, P.in_s, S - 1, -1, &p1);
+        if (p0 == p1 && o1 - o0 == (int64_t)(S - 1) * FAST_HSLAB) {
+          // one peer's chunk holds the window's slabs in slot order: one copy (small copies are
+          // issue-bound, ~0.3 us each)
+          bulk_g2s(dst, Sin + o0, bytes, winF);
+        } else {
+          for (int o = 0; o < S; ++o)
+            bulk_g2s(dst + o * FAST_HSLAB, Sin + pass_slab_off(P, P.xin, jt, h, A.nlev, A.ntiles, a, b, P.in_s, o),
+                     (uint32_t)(FAST_HSLAB * sizeof(E)), winF);
+        }
       }
     }
   }

@@ -8,25 +8,21 @@
 // described by Task / Term tables built once at create time (plan.cu).  This generic path
 // serves ragged ranks (kernel-compressed butterflies, HOD-BF, the distributed split); the
 // uniform rank-16 case has its own fused kernels (fast.cu, leaf.cu).
+#include <type_traits>
+
 #include "mma.cuh"
 
 namespace bfa {
 
-// ------------------------------------------------------------------------------------
-// tensor-core gather-sum kernel (the same Task / Term tables): one warp per work unit =
-// (task, 16-row group) x 16 right-hand sides, 4M complex products on the tensor pipe
-// (mma.cuh policies: DMMA for complex128, 3xTF32 for complex64).  Operands are read straight
-// from global memory / L2 (factor blocks with arbitrary row / column strides and conjugation,
-// slab rows or permuted user rows), zero-padded outside the task's rows, the term's K and nrhs.
-// ------------------------------------------------------------------------------------
 // ------------------------------------------------------------------------------------
 // tensor-core gather-sum kernel (the same Task / Term tables).  One CTA (8 warps) computes a
 // 32-row x 64-column tile of one task's output: per term, K is streamed in chunks of 16 through
 // two shared-memory stages (cp.async, zero-filled outside the task's rows, the term's K and
 // nrhs), so every A element is read once per 64 columns and every input row once per 32 output
 // rows (the L2 traffic of per-warp direct loads bound the previous version at ~10 TF).  Warp w
-// computes rows 16 (w & 1).. and columns 16 (w >> 1).. with the 4M complex product (DMMA for
-// complex128, 3xTF32 for complex64): exact on 0 / 1 selection factors.
+// computes rows 16 (w & 1).. and columns 16 (w >> 1).. with the 3M complex product (DMMA for
+// complex128, 3xTF32 for complex64), or 4M when every factor entry is 0 / +-1 / +-i (selection
+// blocks: the 4M product keeps those applies exact; StageArgs::m3).
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool ok, int bytes) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -47,7 +43,8 @@ struct TileCfg {
 };
 
 // fragments of k-step k0 of a staged chunk: A tile [k][row] (stride SA), B tile [k][col] (SB)
-template <int NT>
+// (M3: also the 3M sums re + im of both operands)
+template <bool M3, int NT>
 __device__ __forceinline__ void tile_frags(PolC128<NT>, typename PolC128<NT>::Frags& f, const double2* sA, const double2* sB, int wr,
                                            int wc, int k0, int g, int t, bool cj) {
   using C = TileCfg<PolC128<NT>>;
@@ -56,11 +53,15 @@ __device__ __forceinline__ void tile_frags(PolC128<NT>, typename PolC128<NT>::Fr
     double2 v = sA[(k0 + t) * C::SA + wr + 8 * mi + g];
     v.y = conj_im(v.y, cj);
     f.a[mi] = v;
+    if (M3) f.as[mi] = v.x + v.y;
   }
 #pragma unroll
-  for (int ni = 0; ni < NT; ++ni) f.b[ni] = sB[(k0 + t) * C::SB + wc + 8 * ni + g];
+  for (int ni = 0; ni < NT; ++ni) {
+    f.b[ni] = sB[(k0 + t) * C::SB + wc + 8 * ni + g];
+    if (M3) f.bs[ni] = f.b[ni].x + f.b[ni].y;
+  }
 }
-template <int NT>
+template <bool M3, int NT>
 __device__ __forceinline__ void tile_frags(PolC64<NT>, typename PolC64<NT>::Frags& f, const float2* sA, const float2* sB, int wr,
                                            int wc, int k0, int g, int t, bool cj) {
   using P = PolC64<NT>;
@@ -75,6 +76,7 @@ __device__ __forceinline__ void tile_frags(PolC64<NT>, typename PolC64<NT>::Frag
     v[e].y = conj_im(v[e].y, cj);
     P::split(v[e].x, f.ah[0][e], f.al[0][e]);
     P::split(v[e].y, f.ah[1][e], f.al[1][e]);
+    if (M3) P::split(v[e].x + v[e].y, f.ah[2][e], f.al[2][e]);
   }
 #pragma unroll
   for (int ni = 0; ni < NT; ++ni) {
@@ -83,7 +85,7 @@ __device__ __forceinline__ void tile_frags(PolC64<NT>, typename PolC64<NT>::Frag
   }
 }
 
-template <class Pol>
+template <class Pol, bool M3>
 __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   using E = typename Pol::E;
   using C = TileCfg<Pol>;
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
     }
   };
 
-  typename Pol::Acc4 acc;
+  std::conditional_t<M3, typename Pol::Acc, typename Pol::Acc4> acc;
   acc.zero();
 #pragma unroll
   for (int st = 0; st < C::NST - 1; ++st) {
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
 #pragma unroll
       for (int k0 = 0; k0 < KC; k0 += KS) {
         typename Pol::Frags f;
-        tile_frags(Pol{}, f, sA, sB, wr, wc, k0, g, t, cj);
+        tile_frags<M3>(Pol{}, f, sA, sB, wr, wc, k0, g, t, cj);
         acc.mac(f);
       }
       __syncthreads();
@@ -196,15 +198,20 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   }
 }
 
-template <class Pol>
-static void launch_tile(dim3 grid, const StageArgs& a, cudaStream_t st) {
+template <class Pol, bool M3>
+static void launch_tile_t(dim3 grid, const StageArgs& a, cudaStream_t st) {
   constexpr size_t smem = TileCfg<Pol>::NST * TileCfg<Pol>::STAGE * sizeof(typename Pol::E);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_stage_tile<Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_stage_tile<Pol, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_stage_tile<Pol><<<grid, 256, smem, st>>>(a);
+  k_stage_tile<Pol, M3><<<grid, 256, smem, st>>>(a);
+}
+template <class Pol>
+static void launch_tile(dim3 grid, const StageArgs& a, cudaStream_t st) {
+  if (a.m3) launch_tile_t<Pol, true>(grid, a, st);
+  else launch_tile_t<Pol, false>(grid, a, st);
 }
 
 template <typename V>

@@ -893,11 +893,30 @@ static void round_info(int dtype, const Plan& P, int round, bf_round_info_t* inf
 // ======================================================================================
 using namespace bfa;
 
+// The generic kernel's complex product: 3M (three real products, 25 % fewer tensor-core
+// instructions) unless every factor entry is 0, +-1, +-i -- selection blocks such as the identity
+// pin, for which the 4M product keeps the apply exact (3M's (a_r + a_i)(b_r + b_i)
+// - a_r b_r - a_i b_i rounds even when a is a selection).
+static bool selection_only(const void* p, int64_t entries, size_t cs) {
+  const int64_t n = entries * 2;
+  if (cs == 16) {
+    const double* v = static_cast<const double*>(p);
+    for (int64_t i = 0; i < n; ++i)
+      if (v[i] != 0.0 && v[i] != 1.0 && v[i] != -1.0) return false;
+  } else {
+    const float* v = static_cast<const float*>(p);
+    for (int64_t i = 0; i < n; ++i)
+      if (v[i] != 0.f && v[i] != 1.f && v[i] != -1.f) return false;
+  }
+  return true;
+}
+
 struct bf_s {
   int dtype = BF_C128;
   int device = 0;
   Geom G;
   void* pool = nullptr;
+  int32_t m3 = 1;  // generic kernel: 3M complex products (0: 4M, every factor entry 0 / +-1 / +-i)
   int64_t* d_rperm = nullptr;
   int64_t* d_cperm = nullptr;
   int64_t slab_rows = 0;
@@ -959,6 +978,7 @@ struct hodbf_s {
   int64_t n = 0;
   int LH = 0;
   void* pool = nullptr;
+  int32_t m3 = 1;  // as bf_s::m3
   int64_t* d_perm = nullptr;
   int64_t slab_rows = 0;
   int64_t factor_entries = 0;
@@ -1087,6 +1107,9 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
       if (G.len_W) BF_CK(cudaMemcpy(p + F.w * cs, d->W, G.len_W * cs, cudaMemcpyHostToDevice));
       if (G.len_Vt) BF_CK(cudaMemcpy(p + F.vt * cs, d->Vt, G.len_Vt * cs, cudaMemcpyHostToDevice));
     }
+    h->m3 = !(selection_only(d->U, G.len_U, cs) && selection_only(d->R, G.len_R, cs) &&
+              selection_only(d->B, G.len_B, cs) && selection_only(d->W, G.len_W, cs) &&
+              selection_only(d->Vt, G.len_Vt, cs));
     // an identity permutation is stored as NULL (no per-row index loads on the device)
     auto is_id = [](const int64_t* p, int64_t n) {
       for (int64_t i = 0; i < n; ++i)
@@ -1290,6 +1313,7 @@ int bf_apply_op_events(bf_handle h, int op, int64_t nrhs, const void* X, int64_t
     }
     StageArgs a{};
     a.pool = h->pool;
+    a.m3 = h->m3;
     a.X = X;
     a.ldx = ldx;
     a.xperm = fwd ? h->d_cperm : h->d_rperm;
@@ -1566,6 +1590,7 @@ int hodbf_create(const hodbf_desc* d, int device, hodbf_handle* out) {
       if (G[k].len_W) memcpy(hp + F[k].w * cs, b.W, (size_t)G[k].len_W * cs);
     }
     if (pool_len) h->pool = upload(hp, (size_t)pool_len * cs, &h->device_bytes);
+    h->m3 = !selection_only(hp, pool_len, cs);
     if (d->perm) h->d_perm = (int64_t*)upload(d->perm, d->n * 8, &h->device_bytes);
     // ---- slab space: per leaf the z^0 group and the y^L group, then each bf's inner levels
     std::vector<Slabs> S(nbf);
@@ -1705,6 +1730,7 @@ int hodbf_apply_events(hodbf_handle h, int op, int64_t nrhs, const void* X, int6
     DeviceGuard dg(h->device);
     StageArgs a{};
     a.pool = h->pool;
+    a.m3 = h->m3;
     a.X = X;
     a.ldx = ldx;
     a.xperm = h->d_perm;
@@ -1852,6 +1878,7 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
     local_pool(*d, G, own, host, F, cs);
     h->factor_entries = (int64_t)(host.size() / cs);
     if (!host.empty()) h->pool = upload(host.data(), host.size(), &h->device_bytes);
+    h->m3 = !selection_only(host.data(), (int64_t)(host.size() / cs), cs);
     const int L = G.L, lc = G.lc;
     const int64_t P = nranks, g = rank;
     // local row ranges (tree positions) and local perms
@@ -2097,6 +2124,7 @@ static int dist_run(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ld
     }
     StageArgs a{};
     a.pool = h->pool;
+    a.m3 = h->m3;
     a.X = X;
     a.ldx = ldx;
     a.xperm = h->d_lperm_in[k];

@@ -21,4 +21,6 @@ done
 timeout 1500 python tools/time_configs.py cfg1 cfg2 cfg3 cfg4 > $O/configs.txt 2> $O/configs.err
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage_tile -s 4 -c 1 -o $O/full_tile_cfg3 python tools/time_configs.py cfg3 > /dev/null 2>&1
 timeout 900 python tools/time_split.py c128 > $O/split_c128.txt 2>&1
+timeout 900 python tools/time_split.py c64 > $O/split_c64.txt 2>&1
+for dt in c128 c64; do timeout 120 python tools/time_apply.py $dt >> $O/apply_plain.txt 2>&1; done
 echo done
