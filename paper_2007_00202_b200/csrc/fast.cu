@@ -23,10 +23,10 @@
 
 namespace bfa {
 
-template <class Pol>
+template <class Pol, int D>
 struct PassCfg {
   using E = typename Pol::E;
-  static constexpr int WINH = (1 << FAST_DMAX) * FAST_HSLAB;  // half window (elements)
+  static constexpr int WINH = (1 << (D > 3 ? D : 3)) * FAST_HSLAB;  // half window (elements)
   static constexpr int WIN = 2 * WINH;                        // window buffer: [half][slot][16 x 16]
   static constexpr int PG = 32768;                            // ring page (bytes)
 #ifndef BF_C64_NP
@@ -35,7 +35,7 @@ struct PassCfg {
 #ifndef BF_C64_NWB
 #define BF_C64_NWB 2
 #endif
-  static constexpr int NP = sizeof(E) == 16 ? 3 : BF_C64_NP;  // ring pages
+  static constexpr int NP = sizeof(E) == 16 ? 3 : D > 3 ? 3 : BF_C64_NP;  // ring pages
   // window buffers: 2 = ping-pong (the next window loads during the item's last op); 3 = two
   // input buffers + one scratch (the next window loads a whole item ahead; complex64 only, a
   // third complex128 window does not fit next to its ring)
@@ -49,7 +49,7 @@ struct PassCfg {
 template <class Pol, int D>
 struct Stream {
   using E = typename Pol::E;
-  using Cfg = PassCfg<Pol>;
+  using Cfg = PassCfg<Pol, D>;
   static constexpr int S = 1 << D;
   static constexpr int SPP = Cfg::PG / (S * FAST_FRAG);  // k-steps per page
   static constexpr int SPL = fast_spl((int)sizeof(E), S); // k-steps per page of the column-leaf op
@@ -136,12 +136,15 @@ struct Stream {
 template <class Pol, int D>
 __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_constant__ FastArgs A) {
   using E = typename Pol::E;
-  using Cfg = PassCfg<Pol>;
+  using Cfg = PassCfg<Pol, D>;
   using St = Stream<Pol, D>;
   constexpr int NT = Pol::NT;
   constexpr int S = 1 << D;                          // slots of the window
   constexpr int CT = 2 / NT;                         // column tiles per slot (in a half)
-  constexpr int NACTH = S * CT;                      // active warps per half
+  // slots per warp: 2 for 4-level windows (16 slots, 8 warps per half), else 1
+  constexpr int SPW = S * CT > FAST_NCONS_HALF ? S * CT / FAST_NCONS_HALF : 1;
+  static_assert(SPW == 1 || CT == 1, "several slots per warp need whole-slot warps");
+  constexpr int NACTH = S * CT / SPW;                // active warps per half
   constexpr int NACT = 2 * NACTH;                    // active warps
   constexpr int SPP = St::SPP;                       // k-steps per page
   constexpr int NP = Cfg::NP;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
 
   if (half == 1 && A.skew > 0) __nanosleep(A.skew);
   const int g = lane >> 2, t = lane & 3;
-  const int o = hw % S;                   // slot
+  const int o0 = hw % (S / SPW);          // the warp's first slot (its others: o0 + S / SPW, ...)
   const int c0w = 8 * NT * (hw / S);      // first column of this warp inside the half
   const int hbar = 1 + half;              // the half's named barrier
   int bo[NT];                             // lane-constant B-fragment offsets inside a half slab
@@ -229,6 +232,11 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           str.issue_window(i + 1, NWB == 3 ? (int)((i + 1) & 1) : rd ^ 1);
       }
       const E* win = winbuf + rd * WIN + half * Cfg::WINH;
+      bool leaf_out_done = false;
+      for (int sl = 0; sl < SPW; ++sl) {
+      const int o = o0 + sl * (S / SPW);  // slot
+      const bool rel = sl == SPW - 1;     // the warp's last slot releases the op's pages
+      (void)rel;
       typename Pol::FAcc acc;
       acc.zero();
       const E* sp0 = win + o * FAST_HSLAB;
@@ -298,8 +306,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
         }
         }
-        cur = rd ^ 1;
-        continue;  // (always the last op)
+        leaf_out_done = true;
+        break;  // (always the last op; one slot per warp)
       }
       if (Pol::LEAF_OPS && op.kind == FK_LEAF_IN) {
         if constexpr (Pol::LEAF_OPS) {
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           Pol::load_b(f[k1 & 1], bsrc(k1), bo);
         }
         acc.mac(f[k & 1]);
-        if ((k + 1) % SPO == 0) {
+        if ((k + 1) % SPO == 0 && rel) {
           // release the page; the last warp out re-arms it with page j + NP
           __syncwarp();
           if (lane == 0 && !(diag & 1)) {
@@ -392,15 +400,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
           Pol::store_slab(acc, dst, c0w, g, t, lane);
         }
-        cur = rd ^ 1;
       } else {
         if (!(diag & 4)) {
           // op 0 writes the buffer the previous item's last op read: the half must be past it
-          if (q == 0) named_sync(hbar, NACTH * 32);
+          if (q == 0 && sl == 0) named_sync(hbar, NACTH * 32);
           E* dst = winbuf + other(rd) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
           Pol::store_slab(acc, dst, c0w, g, t, lane);
-          // the next (pair) op reads other slots: their writes must be visible
-          named_sync(hbar, NACTH * 32);
         } else if (diag & 8) {  // profiling: epilogue stores without the barriers
           E* dst = winbuf + other(rd) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
           Pol::store_slab(acc, dst, c0w, g, t, lane);
@@ -409,8 +414,15 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           acc.each(g, t, [&](int r, int c, E v) { sink += (float)v.x; });
           if (sink == 1.2345f) winbuf[0] = E{};
         }
-        rd = other(rd);
       }
+      }  // slots of the warp
+      if (leaf_out_done || last) {
+        cur = rd ^ 1;
+        continue;
+      }
+      // the next (pair) op reads other slots: their writes must be visible
+      if (!(diag & 4)) named_sync(hbar, NACTH * 32);
+      rd = other(rd);
     }
   }
 }
@@ -420,8 +432,8 @@ const char* fast_kernel_name(int dtype) { return dtype == BF_C128 ? "k_bf_pass<c
 template <class Pol, int D>
 static void launch_one(const FastArgs& a, unsigned grid, cudaStream_t st) {
   static bool attr = false;
-  const size_t smem = PassCfg<Pol>::smem();
-  static_assert(PassCfg<Pol>::smem() <= 227 * 1024, "pass kernel shared memory");
+  const size_t smem = PassCfg<Pol, D>::smem();
+  static_assert(PassCfg<Pol, D>::smem() <= 227 * 1024, "pass kernel shared memory");
   if (!attr) {
     cudaFuncSetAttribute(k_bf_pass<Pol, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
@@ -444,7 +456,8 @@ void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
     else if (d == 2) launch_one<PolC128<2>, 2>(a, grid, st);  // 8 warps x 16 columns: 3 % faster than 16 x 8
     else launch_one<PolC128<1>, 1>(a, grid, st);
   } else {
-    if (d == 3) launch_one<PolC64T<2>, 3>(a, grid, st);
+    if (d == 4) launch_one<PolC64T<2>, 4>(a, grid, st);
+    else if (d == 3) launch_one<PolC64T<2>, 3>(a, grid, st);
     else if (d == 2) launch_one<PolC64T<1>, 2>(a, grid, st);
     else launch_one<PolC64T<1>, 1>(a, grid, st);
   }

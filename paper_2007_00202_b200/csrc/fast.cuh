@@ -29,7 +29,8 @@ namespace bfa {
 enum FastKind : int32_t { FK_LEAF_IN = 0, FK_PAIR_DOWN = 1, FK_PAIR_UP = 2, FK_DIAG = 3, FK_LEAF_OUT = 4 };
 constexpr int FAST_RANK = 16;                   // r: slab rows
 constexpr int FAST_NB = 32;                     // right-hand sides per work item (slab columns)
-constexpr int FAST_DMAX = 3;                    // window levels per pass
+constexpr int FAST_DMAX = 3;                    // window levels per pass (complex128)
+constexpr int FAST_DMAX_C64 = 4;                // complex64: 16-slot windows fit next to the ring
 constexpr int FAST_MAXOPS = 8;
 constexpr int FAST_MAXPEER = 8;                 // ranks the fused peer-memory exchange addresses
 constexpr int FAST_SLAB = FAST_RANK * FAST_NB;  // complex entries per slab (512)

@@ -472,8 +472,11 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   const bool split = dp >= 0;
   const int ks = fast_ks((int)sizeof(CT));
   std::vector<int> lv;  // level boundaries of the window passes
-  auto chunk = [&](int lo, int hi) {  // split [lo, hi] into near-equal passes of <= FAST_DMAX levels
-    const int n = hi - lo, k = (n + FAST_DMAX - 1) / FAST_DMAX;
+  // window levels per pass: 3 (complex128), 4 (complex64; env BF_C64_DMAX = 3 for A/B)
+  int dmax = sizeof(CT) == 16 ? FAST_DMAX : FAST_DMAX_C64;
+  if (sizeof(CT) == 8 && getenv("BF_C64_DMAX")) dmax = std::max(1, std::min(FAST_DMAX_C64, atoi(getenv("BF_C64_DMAX"))));
+  auto chunk = [&](int lo, int hi) {  // split [lo, hi] into near-equal passes of <= dmax levels
+    const int n = hi - lo, k = (n + dmax - 1) / dmax;
     for (int p = 0, at = lo; p < k; ++p) {
       at += n / k + (p < n % k ? 1 : 0);
       lv.push_back(at);
