@@ -49,6 +49,22 @@ def test_fast_layouts(L, leaf, lc, dtype):
 
 
 @pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("L,leaf", [(2, 256), (3, 128), (4, 256), (8, 16)])
+@pytest.mark.parametrize("nrhs", [1, 33])
+def test_fast_large_leaves_and_thin_blocks(L, leaf, nrhs, dtype):
+    """The largest fast-path leaves (128, 256: several chunks per leaf item in both leaf
+    kernels), a single right-hand side and one column past a tile boundary."""
+    bf = random_butterfly(L=L, leaf=leaf, r=16, seed=7 * L + leaf, dtype=dtype)
+    h = pkg.BFHandle(bf)
+    assert h.rounds("N")[0]["name"].startswith("k_leaf"), "expected the fused path"
+    K = oracle.bf_dense(bf)
+    for op in "NCT":
+        X = random_rhs(bf.n if op == "N" else bf.m, nrhs, seed=L + nrhs, dtype=dtype)
+        err = oracle.rel_err(host(h.apply(dev(X), op)), oracle.apply_op(K, X, op))
+        assert err <= TOL[dtype], (op, err)
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
 @pytest.mark.parametrize("L,nrhs,leaf", [(6, 1000, 16), (7, 700, 16), (5, 64 * 32 + 5, 16), (6, 1000, 64), (7, 640, 32)])
 def test_fast_many_items(L, nrhs, leaf, dtype):
     """More work items (windows x rhs tiles) than SMs: each persistent CTA loops over
