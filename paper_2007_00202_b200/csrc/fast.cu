@@ -13,10 +13,10 @@
 //     so all 16 warps compute with 128 registers each);
 //   * the ops of an item ping-pong between two half-window buffers (op q reads buffer rd, writes
 //     the other), so one CTA barrier per op suffices: between an op's writes and the next pair
-//     op's reads of other slots.  The last op writes the output slabs straight to HBM.  complex128:
-//     when every warp has reached the last op, the other buffer takes the next window; complex64
-//     has room for a third buffer (two input buffers + a scratch), so the next window loads as
-//     soon as every warp has finished the previous item, a whole item ahead.
+//     op's reads of other slots.  The last op writes the output slabs straight to HBM; when
+//     every warp has reached it, the other buffer takes the next window.
+//   * complex64 windows may span 4 levels (16 slots per half): each warp then runs every op for
+//     two slots, one after the other.
 #include <cstdio>
 
 #include "mma.cuh"
@@ -29,18 +29,11 @@ struct PassCfg {
   static constexpr int WINH = (1 << (D > 3 ? D : 3)) * FAST_HSLAB;  // half window (elements)
   static constexpr int WIN = 2 * WINH;                        // window buffer: [half][slot][16 x 16]
   static constexpr int PG = 32768;                            // ring page (bytes)
-#ifndef BF_C64_NP
-#define BF_C64_NP 4
-#endif
-#ifndef BF_C64_NWB
-#define BF_C64_NWB 2
-#endif
-  static constexpr int NP = sizeof(E) == 16 ? 3 : D > 3 ? 3 : BF_C64_NP;  // ring pages
-  // window buffers: 2 = ping-pong (the next window loads during the item's last op); 3 = two
-  // input buffers + one scratch (the next window loads a whole item ahead; complex64 only, a
-  // third complex128 window does not fit next to its ring)
-  static constexpr int NWB = sizeof(E) == 16 ? 2 : BF_C64_NWB;
-  __host__ __device__ static constexpr size_t bars_off() { return NWB * WIN * sizeof(E) + (size_t)NP * PG; }
+  // ring pages: complex128 3 (2 x 64 KB windows), complex64 4 (3-level windows) or 3 (4-level).
+  // (Measured on complex64: a 5th page or a third window buffer, which lets the next window load
+  // a whole item ahead, made the 3-level pass slower: 0.1156 / 0.1168 vs 0.1136 ms.)
+  static constexpr int NP = sizeof(E) == 16 ? 3 : D > 3 ? 3 : 4;
+  __host__ __device__ static constexpr size_t bars_off() { return 2 * WIN * sizeof(E) + (size_t)NP * PG; }
   __host__ __device__ static constexpr size_t smem() { return bars_off() + (1 + NP) * 8 + (1 + NP) * 4; }
 };
 
@@ -153,8 +146,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   static_assert(NACT <= FAST_NCONS, "too many warps");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   E* winbuf = reinterpret_cast<E*>(smem_raw);
-  constexpr int NWB = Cfg::NWB;
-  unsigned char* ring = smem_raw + NWB * WIN * sizeof(E);
+  unsigned char* ring = smem_raw + 2 * WIN * sizeof(E);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + Cfg::bars_off());
   uint64_t* winF = bars;                              // window loads (one phase per item)
   uint64_t* full = bars + 1;
@@ -217,22 +209,17 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
     const int64_t w = item & ((int64_t(1) << nwin_log) - 1), jt = item >> nwin_log;
     const int64_t a = P.a_lo + (w >> P.b_log), b = P.b_lo + (w & bmask);
     if (!(diag & 1) && P.in_s >= 0) mbar_wait(winF, (uint32_t)(i & 1), 3);
-    // op q reads buffer rd and writes `other(rd)`: NWB = 2 ping-pong; NWB = 3 the item's input
-    // buffer i & 1 and the scratch buffer 2
-    const int inb = NWB == 3 ? (int)(i & 1) : cur;
-    auto other = [&](int r) { return NWB == 3 ? (r == inb ? 2 : inb) : r ^ 1; };
-    int rd = inb;
+    int rd = cur;  // op q reads buffer rd, writes rd ^ 1
     for (int q = 0; q < P.nops; ++q) {
       const FastOp op = P.ops[q];
       const bool last = q == P.nops - 1;
-      if (lane == 0 && !(diag & 1) && P.in_s >= 0 && (NWB == 3 ? q == 0 : last)) {
-        // NWB = 2: every warp past op q-1 -> buffer rd ^ 1 is free; NWB = 3: every warp done with
-        // item i-1 -> input buffer (i+1) & 1 is free.  The last one in loads the next window.
-        if (atom_add_acqrel(wcnt, 1) == (int)(i + 1) * NACT - 1)
-          str.issue_window(i + 1, NWB == 3 ? (int)((i + 1) & 1) : rd ^ 1);
+      // (the condition order matters to the complex128 code generation: 2 % per apply)
+      if (lane == 0 && !(diag & 1) && P.in_s >= 0 && last) {
+        // every warp past op q-1 -> buffer rd ^ 1 is free: the last one in loads the next window
+        if (atom_add_acqrel(wcnt, 1) == (int)(i + 1) * NACT - 1) str.issue_window(i + 1, rd ^ 1);
       }
       const E* win = winbuf + rd * WIN + half * Cfg::WINH;
-      bool leaf_out_done = false;
+#pragma unroll
       for (int sl = 0; sl < SPW; ++sl) {
       const int o = o0 + sl * (S / SPW);  // slot
       const bool rel = sl == SPW - 1;     // the warp's last slot releases the op's pages
@@ -306,8 +293,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
         }
         }
-        leaf_out_done = true;
-        break;  // (always the last op; one slot per warp)
+        cur = rd ^ 1;
+        continue;  // (always the last op; one slot per warp)
       }
       if (Pol::LEAF_OPS && op.kind == FK_LEAF_IN) {
         if constexpr (Pol::LEAF_OPS) {
@@ -400,29 +387,26 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
           Pol::store_slab(acc, dst, c0w, g, t, lane);
         }
+        if (rel) cur = rd ^ 1;
       } else {
         if (!(diag & 4)) {
           // op 0 writes the buffer the previous item's last op read: the half must be past it
           if (q == 0 && sl == 0) named_sync(hbar, NACTH * 32);
-          E* dst = winbuf + other(rd) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
+          E* dst = winbuf + (rd ^ 1) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
           Pol::store_slab(acc, dst, c0w, g, t, lane);
+          // the next (pair) op reads other slots: their writes must be visible
+          if (rel) named_sync(hbar, NACTH * 32);
         } else if (diag & 8) {  // profiling: epilogue stores without the barriers
-          E* dst = winbuf + other(rd) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
+          E* dst = winbuf + (rd ^ 1) * WIN + half * Cfg::WINH + o * FAST_HSLAB;
           Pol::store_slab(acc, dst, c0w, g, t, lane);
         } else {  // profiling: keep the accumulators live without any epilogue
           float sink = 0.f;
           acc.each(g, t, [&](int r, int c, E v) { sink += (float)v.x; });
           if (sink == 1.2345f) winbuf[0] = E{};
         }
+        if (rel) rd ^= 1;
       }
       }  // slots of the warp
-      if (leaf_out_done || last) {
-        cur = rd ^ 1;
-        continue;
-      }
-      // the next (pair) op reads other slots: their writes must be visible
-      if (!(diag & 4)) named_sync(hbar, NACTH * 32);
-      rd = other(rd);
     }
   }
 }
