@@ -1133,7 +1133,9 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
         emit_C(pb, G, F, S, o);
       upload_plan(h->plan[k], pb, 0, (int)pb.tasks.size(), &h->device_bytes);
     }
-    if (fast_eligible(G, d->dtype) && !getenv("BF_DISABLE_FAST")) {
+    // the fused kernels use the 3M product; selection factors (every entry 0 / +-1 / +-i, the
+    // identity pin) stay on the generic path, whose 4M product keeps their apply exact
+    if (fast_eligible(G, d->dtype) && h->m3 && !getenv("BF_DISABLE_FAST")) {
       const bool cc = leaves_contiguous(d->col_perm, d->n, G.nv(0));
       const bool rc = leaves_contiguous(d->row_perm, d->m, G.mt(0));
       if (d->dtype == BF_C128) {
@@ -1881,7 +1883,10 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
     local_pool(*d, G, own, host, F, cs);
     h->factor_entries = (int64_t)(host.size() / cs);
     if (!host.empty()) h->pool = upload(host.data(), host.size(), &h->device_bytes);
-    h->m3 = !selection_only(host.data(), (int64_t)(host.size() / cs), cs);
+    // decided on the full factors, so that every rank takes the same path (and slab format)
+    h->m3 = !(selection_only(d->U, G0.len_U, cs) && selection_only(d->R, G0.len_R, cs) &&
+              selection_only(d->B, G0.len_B, cs) && selection_only(d->W, G0.len_W, cs) &&
+              selection_only(d->Vt, G0.len_Vt, cs));
     const int L = G.L, lc = G.lc;
     const int64_t P = nranks, g = rank;
     // local row ranges (tree positions) and local perms
@@ -1988,7 +1993,7 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
     h->slab_rows = max_rows;
     // fused fast path for uniform rank-16 butterflies: the same split with the window-pass and
     // leaf kernels; the generic plans above remain the fallback
-    if (fast_eligible(G0, d->dtype) && G0.lc >= 1 && G0.L - G0.lc >= 1 && !getenv("BF_DISABLE_FAST")) {
+    if (fast_eligible(G0, d->dtype) && G0.lc >= 1 && G0.L - G0.lc >= 1 && h->m3 && !getenv("BF_DISABLE_FAST")) {
       auto build = [&](auto* tag) {
         using CT = std::remove_pointer_t<decltype(tag)>;
         HostFactors<CT> HF{static_cast<const CT*>(d->U), static_cast<const CT*>(d->R), static_cast<const CT*>(d->B),

@@ -59,6 +59,21 @@ def test_identity_exact(L, m0):
     np.testing.assert_array_equal(run(h, X, "C"), X)
 
 
+@pytest.mark.parametrize("L", [3, 5])
+def test_identity_exact_fast_shape(L):
+    """A rank-16, leaf-16 identity has the fused path's shape, but selection factors take the
+    generic path (4M product), so the apply stays exact (pin P1); random factors of the same
+    shape take the fused kernels."""
+    bf = identity_butterfly(L, 16)
+    h = pkg.BFHandle(bf)
+    assert all(r["name"].startswith("k_stage_tile") for r in h.rounds("N")), h.rounds("N")
+    X = random_rhs(bf.n, 33, seed=2)
+    np.testing.assert_array_equal(run(h, X, "N"), X)
+    np.testing.assert_array_equal(run(h, X, "C"), X)
+    hr = pkg.BFHandle(random_butterfly(L=L, leaf=16, r=16, seed=L))
+    assert hr.rounds("N")[0]["name"].startswith("k_leaf")
+
+
 @pytest.mark.parametrize("L", [4, 10, 15])
 def test_dft_vs_numpy_fft(L):
     bf = dft_butterfly(L)
