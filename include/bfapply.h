@@ -208,6 +208,14 @@ int bf_dist_apply_pre_p2p(bf_handle h, int op, int64_t nrhs, const void* X_loc, 
 int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy,
                        void* work, size_t work_bytes, bf_stream_t stream);
 
+/* Y += A on a column-major rows x nrhs complex block (device pointers, ld >= rows): the sum of
+ * the HOD-BF contributions of a tree-partitioned apply ("Y(T_tau) += B_tau X(...)"; the
+ * row-side posts of the off-diagonal butterflies at the distributed levels write a scratch block
+ * that this adds into the rank's local result).  A and Y must not overlap.  BF_ERR_ARG on NULL
+ * pointers, a negative size, ld < rows or an unknown dtype; an asynchronous launch on `stream`. */
+int bf_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,
+                  bf_stream_t stream);
+
 /* ---- introspection / in-situ timing ------------------------------------------------------
  * An apply is a fixed sequence of kernel launches ("rounds").  bf_round_info describes round
  * `round` of op `op`: the kernel variant, the number of independent block products, and the

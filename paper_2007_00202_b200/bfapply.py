@@ -101,6 +101,8 @@ _SIGS = [
                                     C.c_void_p, C.c_size_t, C.c_void_p]),
     ("bf_dist_apply_post", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64,
                                      C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("bf_accumulate", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                C.c_void_p]),
     ("bf_rounds", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
     ("bf_round_info", C.c_int, [C.c_void_p, C.c_int, C.c_int32, C.POINTER(bf_round_info_t)]),
     ("bf_apply_op_events", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,

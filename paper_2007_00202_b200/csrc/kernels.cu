@@ -228,6 +228,42 @@ static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
     launch_tile<PolC64<2>>(grid, a, st);
 }
 
+// Y += A, column-major rows x nrhs (bf_accumulate): grid-stride over the block, one complex
+// element per thread and step (HBM-bound elementwise work; coalesced along the rows)
+template <typename V>
+__global__ void k_accumulate(int64_t rows, int64_t nrhs, const V* __restrict__ A, int64_t lda, V* __restrict__ Y,
+                             int64_t ldy) {
+  const int64_t total = rows * nrhs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / rows, r = i - c * rows;
+    const V a = A[r + c * lda];
+    V y = Y[r + c * ldy];
+    y.x += a.x;
+    y.y += a.y;
+    Y[r + c * ldy] = y;
+  }
+}
+
+void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,
+                       cudaStream_t st) {
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t total = rows * nrhs;
+  if (total == 0) return;
+  const int64_t want = (total + 255) / 256;
+  const unsigned grid = (unsigned)(want < 8LL * nsm ? want : 8LL * nsm);
+  if (dtype == BF_C128)
+    k_accumulate<double2><<<grid, 256, 0, st>>>(rows, nrhs, static_cast<const double2*>(A), lda,
+                                                static_cast<double2*>(Y), ldy);
+  else
+    k_accumulate<float2><<<grid, 256, 0, st>>>(rows, nrhs, static_cast<const float2*>(A), lda,
+                                               static_cast<float2*>(Y), ldy);
+}
+
 const char* round_kernel_name(int dtype, const Round& r, int* id) {
   (void)r;
   if (id) *id = 3;

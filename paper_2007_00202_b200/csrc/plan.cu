@@ -2168,4 +2168,20 @@ int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t l
   return dist_run(h, op, nrhs, nullptr, 0, Y_loc, ldy, work, work_bytes, stream, false);
 }
 
+int bf_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,
+                  bf_stream_t stream) {
+  try {
+    require(dtype == BF_C128 || dtype == BF_C64, BF_ERR_ARG, "unknown dtype");
+    require(rows >= 0 && nrhs >= 0, BF_ERR_ARG, "negative size");
+    if (rows == 0 || nrhs == 0) return BF_OK;
+    require(A != nullptr && Y != nullptr, BF_ERR_ARG, "NULL block");
+    require(lda >= rows && ldy >= rows, BF_ERR_ARG, "leading dimension < rows");
+    launch_accumulate(dtype, rows, nrhs, A, lda, Y, ldy, static_cast<cudaStream_t>(stream));
+    BF_CK(cudaGetLastError());
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
 }  // extern "C"

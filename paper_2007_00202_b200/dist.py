@@ -261,3 +261,153 @@ class ShardedHODBF:
 
     def apply(self, Xloc: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None) -> torch.Tensor:
         return self.h.apply(Xloc, op, out=out)
+
+
+def sub_hodbf(H, p: int, g: int):
+    """The HOD-BF of T_H subtree g at level p (P:542 restricted to the rows and columns of that
+    node): its 2^(LH-p) dense leaves and its butterflies at levels p+1..LH, re-indexed as levels
+    1..LH-p, in tree order (identity perm)."""
+    from bfinputs.factors import HODBF, Stage
+    lo, hi = H.node_range(p, g)
+    w = 1 << (H.LH - p)
+    leaf_ptr = np.asarray(H.leaf_ptr[g * w:(g + 1) * w + 1], dtype=np.int64) - lo
+    D = Stage.from_blocks([H.D.block(i) for i in range(g * w, (g + 1) * w)], H.D.data.dtype)
+    off = [[H.offdiag[l - 1][t] for t in range(g << (l - p), (g + 1) << (l - p))] for l in range(p + 1, H.LH + 1)]
+    return HODBF(hi - lo, H.LH - p, leaf_ptr, np.arange(hi - lo, dtype=np.int64), D, off, H.dtype)
+
+
+class TreeHODBF:
+    """HOD-BF apply distributed by tree node.  P = 2^p ranks; rank g owns
+    the T_H node g at level p: the rows and columns of A in it (X and Y rows in HOD-BF tree
+    order, positions ``rows()``).
+
+    * The dense leaves and the sibling butterflies at levels l > p lie inside the node: a local
+      HOD-BF (``sub_hodbf``) applies them, no communication.
+    * A sibling pair (a, b) at level l <= p spans 2^(p-l) ranks on each side.  Its butterflies
+      B_a = A(T_a, T_b) and B_b = A(T_b, T_a) run as the bf_dist split over 2^(p-l) virtual
+      ranks (``DistBFHandle``), virtual rank v of a node being physical rank node * 2^(p-l) + v:
+      op N runs the column side (leaf V, W stages, centre B) of B_b and the row side (R stages,
+      leaf U) of B_a on the ranks of node a (op C the column side of B_a^H and the row side of
+      B_b^H), so every centre slab travels from the ranks of one node to the ranks of its
+      sibling.
+    * All levels' centre slabs move in one grouped send / receive per apply
+      (``torch.distributed.batch_isend_irecv``: NCCL over NVLink / NVSwitch, gloo on CPU); the
+      row sides then write scratch blocks that ``bf_accumulate`` adds into the local result.
+
+    Every arithmetic step runs in libbfapply's kernels; this class is marshalling.  With
+    ``device=None`` only the host-side plans exist (layouts, exchange maps: the gloo tests)."""
+
+    def __init__(self, H, rank: int, world: int, device: Optional[int] = 0, group=None):
+        p = world.bit_length() - 1
+        if (1 << p) != world or p > H.LH - 1:
+            raise ValueError("TreeHODBF needs a power-of-two world of at most 2^(LH-1) ranks")
+        from .bfapply import HODBFHandle
+        self.p, self.rank, self.world, self.device, self.group = p, rank, world, device, group
+        self.lo, self.hi = H.node_range(p, rank)
+        self.local = HODBFHandle(sub_hodbf(H, p, rank), device) if device is not None else None
+        self.levels = []
+        for l in range(1, p + 1):
+            a = rank >> (p - l)
+            b = a ^ 1
+            Pv = 1 << (p - l)
+            v = rank - (a << (p - l))
+            Ha = DistBFHandle(H.offdiag[l - 1][a], v, Pv, device)  # rows T_a (this rank's), cols T_b
+            Hb = DistBFHandle(H.offdiag[l - 1][b], v, Pv, device)  # rows T_b, cols T_a (this rank's)
+            a0 = H.node_range(l, a)[0]
+            # the virtual rank's slices are this rank's node: same rows in both butterflies
+            assert Ha.local_rows("N")[1] == self.hi - self.lo and Ha.local_rows("N")[3] == self.lo - a0
+            assert Hb.local_rows("N")[0] == self.hi - self.lo and Hb.local_rows("N")[2] == self.lo - a0
+            self.levels.append({"l": l, "Ha": Ha, "Hb": Hb, "peers": [(b << (p - l)) + q for q in range(Pv)],
+                                "work": {}})
+        self.code = self.levels[0]["Ha"].code if self.levels else None
+        self.cs = 16 if H.dtype == np.complex128 else 8
+
+    def rows(self):
+        """[lo, hi): this rank's positions in the HOD-BF tree order (X_loc / Y_loc rows)."""
+        return self.lo, self.hi
+
+    def _sides(self, lev, op: str):
+        """(column-side handle, row-side handle) of level `lev` for op."""
+        return (lev["Hb"], lev["Ha"]) if op == "N" else (lev["Ha"], lev["Hb"])
+
+    def exchange_plan(self, op: str, nrhs: int):
+        """Per level: the byte ranges of the column side's send region (one per sibling-node
+        peer) and of the row side's recv region, with the physical peer ranks."""
+        plan = []
+        for lev in self.levels:
+            Hc, Hr = self._sides(lev, op)
+            wbc, so, _, sc, _ = Hc.layout(op, nrhs)
+            wbr, _, ro, _, rc = Hr.layout(op, nrhs)
+            sends, recvs, s_at, r_at = [], [], so, ro
+            for q, peer in enumerate(lev["peers"]):
+                sends.append((peer, s_at, sc[q] * self.cs))
+                recvs.append((peer, r_at, rc[q] * self.cs))
+                s_at += sc[q] * self.cs
+                r_at += rc[q] * self.cs
+            plan.append({"l": lev["l"], "Hc": Hc, "Hr": Hr, "work_bytes": (wbc, wbr), "sends": sends, "recvs": recvs})
+        return plan
+
+    def _works(self, lev, op, nrhs, wbc, wbr):
+        key = (op, nrhs)
+        if key not in lev["work"]:
+            dev = torch.device("cuda", self.device) if self.device is not None else "cpu"
+            lev["work"][key] = (torch.zeros(max(wbc, 1), dtype=torch.uint8, device=dev),
+                                torch.zeros(max(wbr, 1), dtype=torch.uint8, device=dev))
+        return lev["work"][key]
+
+    def pre(self, Xloc: torch.Tensor, op: str = "N", stream=None):
+        """Every level's column side on this rank's X rows (send regions filled)."""
+        nrhs = Xloc.shape[0]
+        st = _stream_handle(stream)
+        for lev, pl in zip(self.levels, self.exchange_plan(op, nrhs)):
+            wc, _ = self._works(lev, op, nrhs, *pl["work_bytes"])
+            Hc = pl["Hc"]
+            ldx = _check_rhs(Xloc, self.hi - self.lo, self.code, "X_loc")
+            _check("bf_dist_apply_pre", lib().bf_dist_apply_pre(Hc.h, OPS[op], nrhs, C.c_void_p(Xloc.data_ptr()), ldx,
+                                                                 C.c_void_p(wc.data_ptr()), wc.numel(), st))
+
+    def buffers(self, op: str, nrhs: int):
+        """Per level: [(peer, send view)], [(peer, recv view)] (float views of the work buffers)."""
+        rdt = torch.float64 if self.cs == 16 else torch.float32
+        out = []
+        for lev, pl in zip(self.levels, self.exchange_plan(op, nrhs)):
+            wc, wr = self._works(lev, op, nrhs, *pl["work_bytes"])
+            sv = [(peer, wc[o:o + n].view(rdt)) for peer, o, n in pl["sends"]]
+            rv = [(peer, wr[o:o + n].view(rdt)) for peer, o, n in pl["recvs"]]
+            out.append((sv, rv))
+        return out
+
+    def exchange(self, op: str, nrhs: int):
+        """One grouped send / receive of every level's centre slabs between sibling nodes."""
+        ops = []
+        for sv, rv in self.buffers(op, nrhs):
+            ops += [dist.P2POp(dist.isend, t, peer, group=self.group) for peer, t in sv if t.numel()]
+            ops += [dist.P2POp(dist.irecv, t, peer, group=self.group) for peer, t in rv if t.numel()]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def post(self, Yloc: torch.Tensor, op: str = "N", stream=None):
+        """Every level's row side from its recv region, accumulated into Y_loc (bf_accumulate)."""
+        nrhs = Yloc.shape[0]
+        rows = self.hi - self.lo
+        ldy = _check_rhs(Yloc, rows, self.code, "Y_loc")
+        st = _stream_handle(stream)
+        tmp = torch.empty_like(Yloc)
+        for lev, pl in zip(self.levels, self.exchange_plan(op, nrhs)):
+            _, wr = self._works(lev, op, nrhs, *pl["work_bytes"])
+            Hr = pl["Hr"]
+            _check("bf_dist_apply_post", lib().bf_dist_apply_post(Hr.h, OPS[op], nrhs, C.c_void_p(tmp.data_ptr()), ldy,
+                                                                   C.c_void_p(wr.data_ptr()), wr.numel(), st))
+            _check("bf_accumulate", lib().bf_accumulate(self.code, rows, nrhs, C.c_void_p(tmp.data_ptr()), ldy,
+                                                        C.c_void_p(Yloc.data_ptr()), ldy, st))
+
+    def apply(self, Xloc: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Y_loc = (A X)_loc (op N) or (A^H X)_loc (op C) for this rank's rows (tree order)."""
+        if self.local is None:
+            raise BFError("hodbf_apply", -8, "host-only plan cannot apply")
+        Y = self.local.apply(Xloc, op, out=out)
+        self.pre(Xloc, op)
+        self.exchange(op, Xloc.shape[0])  # NCCL's stream waits for the current one (the send regions)
+        self.post(Y, op)
+        return Y
