@@ -208,6 +208,17 @@ int bf_dist_apply_pre_p2p(bf_handle h, int op, int64_t nrhs, const void* X_loc, 
 int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy,
                        void* work, size_t work_bytes, bf_stream_t stream);
 
+/* Sub-matrix extraction (Alg. 3 extract_BF): out(i, j) =
+ * K(rows[i], cols[j]) for user row / column indices (HOST arrays of nI / nJ int64, any order,
+ * repeats allowed), out a DEVICE column-major nI x nJ block with ldo >= nI.  Computed as a
+ * partial matvec: K E_J on the blocks (l, tau, nu) whose tau is an ancestor of a requested
+ * row's leaf and whose nu is an ancestor of a requested column's leaf, then the requested rows.
+ * Single-device handles only (BF_ERR_ARG for a bf_dist handle).  Synchronous: allocates and frees
+ * its temporaries (slab space of nJ columns, the plan of the touched blocks) and returns after
+ * the work on `stream` completed.  BF_ERR_ARG on out-of-range indices or NULL arguments. */
+int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
+               int64_t ldo, bf_stream_t stream);
+
 /* Y += A on a column-major rows x nrhs complex block (device pointers, ld >= rows): the sum of
  * the HOD-BF contributions of a tree-partitioned apply ("Y(T_tau) += B_tau X(...)"; the
  * row-side posts of the off-diagonal butterflies at the distributed levels write a scratch block

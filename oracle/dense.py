@@ -333,3 +333,17 @@ def rel_err(Y, Yref) -> float:
     Yref = np.asarray(Yref, dtype=C128)
     nrm = np.linalg.norm(Yref)
     return float(np.linalg.norm(np.asarray(Y, dtype=C128) - Yref) / (nrm if nrm > 0 else 1.0))
+
+
+def bf_extract(bf, user_rows, user_cols) -> np.ndarray:
+    """K_user(user_rows, user_cols): the sub-matrix extract_BF returns (Alg. 3, P:472-526;
+    SURVEY 8(f) NEXT-1), by its plain definition -- the entries of K (Eq. 3.1-3.2) at the requested
+    rows and columns.  Rows of K through bf_rows_apply (Eq. 3.2 restricted to those rows) times
+    unit columns; repeated indices allowed."""
+    rows = np.asarray(user_rows, dtype=np.int64)
+    cols = np.asarray(user_cols, dtype=np.int64)
+    ur, inv = np.unique(rows, return_inverse=True)
+    E = np.zeros((bf.n, len(cols)), dtype=C128)
+    E[cols, np.arange(len(cols))] = 1.0
+    return bf_rows_apply(bf, ur, E)[inv]
+

@@ -101,6 +101,8 @@ _SIGS = [
                                     C.c_void_p, C.c_size_t, C.c_void_p]),
     ("bf_dist_apply_post", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64,
                                      C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("bf_extract", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                             C.c_void_p]),
     ("bf_accumulate", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                 C.c_void_p]),
     ("bf_rounds", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
@@ -254,6 +256,17 @@ class BFHandle:
         s = C.c_size_t()
         _check("bf_workspace_size", lib().bf_workspace_size(self.h, nrhs, C.byref(s)))
         return s.value
+
+    def extract(self, rows, cols, stream=None) -> torch.Tensor:
+        """K(rows, cols) as an (len(rows), len(cols)) device tensor (bf_extract: the sub-matrix
+        as a partial matvec over the touched blocks; synchronous).  rows / cols: user indices."""
+        r = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+        c = np.ascontiguousarray(np.asarray(cols, dtype=np.int64))
+        out = torch.zeros((len(c), len(r)), dtype=_torch_dtype(self.code), device=torch.device("cuda", self.device))
+        _check("bf_extract", lib().bf_extract(self.h, len(r), r.ctypes.data_as(C.c_void_p), len(c),
+                                              c.ctypes.data_as(C.c_void_p), C.c_void_p(out.data_ptr()),
+                                              max(len(r), 1), _stream_handle(stream)))
+        return out.T
 
     def apply(self, X: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None,
               work: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

@@ -8,6 +8,7 @@
 // described by Task / Term tables built once at create time (plan.cu).  This generic path
 // serves ragged ranks (kernel-compressed butterflies, HOD-BF, the distributed split); the
 // uniform rank-16 case has its own fused kernels (fast.cu, leaf.cu).
+#include <algorithm>
 #include <type_traits>
 
 #include "mma.cuh"
@@ -262,6 +263,30 @@ void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int
   else
     k_accumulate<float2><<<grid, 256, 0, st>>>(rows, nrhs, static_cast<const float2*>(A), lda,
                                                static_cast<float2*>(Y), ldy);
+}
+
+// out(i, j) = Y(rowidx[i], j), column-major (bf_extract's final gather of the requested rows)
+template <typename V>
+__global__ void k_gather_rows(int64_t nI, int64_t nJ, const V* __restrict__ Y, int64_t ldy,
+                              const int64_t* __restrict__ rowidx, V* __restrict__ out, int64_t ldo) {
+  const int64_t total = nI * nJ;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / nI, r = i - c * nI;
+    out[r + c * ldo] = Y[rowidx[r] + c * ldy];
+  }
+}
+
+void launch_gather_rows(int dtype, int64_t nI, int64_t nJ, const void* Y, int64_t ldy, const int64_t* rowidx,
+                        void* out, int64_t ldo, cudaStream_t st) {
+  const int64_t total = nI * nJ;
+  if (total == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 4096);
+  if (dtype == BF_C128)
+    k_gather_rows<double2><<<grid, 256, 0, st>>>(nI, nJ, static_cast<const double2*>(Y), ldy, rowidx,
+                                                 static_cast<double2*>(out), ldo);
+  else
+    k_gather_rows<float2><<<grid, 256, 0, st>>>(nI, nJ, static_cast<const float2*>(Y), ldy, rowidx,
+                                                static_cast<float2*>(out), ldo);
 }
 
 const char* round_kernel_name(int dtype, const Round& r, int* id) {

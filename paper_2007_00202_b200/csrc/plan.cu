@@ -252,10 +252,23 @@ static Term mk(int64_t a_off, int a_rs, int a_cs, int64_t k, int64_t in_row, int
   return t;
 }
 
+// Blocks an extraction touches (Alg. 3): (l, tau, nu) with tau at T_O level l an
+// ancestor of a requested row's leaf and nu at T_S level L - l an ancestor of a requested
+// column's leaf.  Every other block of K E_J restricted to the rows I is zero or unused.
+struct Touch {
+  std::vector<std::vector<uint8_t>> row;  // [l][tau], l = 0..L
+  std::vector<std::vector<uint8_t>> col;  // [l][nu],  nu at T_S level L - l
+  bool r(int l, int64_t tau) const { return row[l][tau] != 0; }
+  bool c(int l, int64_t nu) const { return col[l][nu] != 0; }
+};
+
 struct EmitOpts {
   bool leaf_in = true, leaf_out = true;  // emit the V / U leaf stages (HOD-BF fuses them)
   int64_t x_base = 0, y_base = 0;        // tree position of local X / Y row 0
   Own own;
+  const Touch* touch = nullptr;          // extraction: emit only the touched blocks (op N)
+  bool tr(int l, int64_t tau) const { return !touch || touch->r(l, tau); }
+  bool tc(int l, int64_t nu) const { return !touch || touch->c(l, nu); }
 };
 
 // op N rounds: 0 leaf V, 1..lc W, lc+1 B, lc+2.. R, L+2 leaf U
@@ -263,7 +276,7 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
   const int L = G.L, lc = G.lc;
   if (o.leaf_in)
     for (int64_t nu = 0; nu < G.nb; ++nu) {
-      if (!o.own.col(G, 0, nu)) continue;
+      if (!o.own.col(G, 0, nu) || !o.tc(0, nu)) continue;
       const int c = G.c(0, nu);
       Term t = mk(F.vt + G.vt_off[nu], 1, c, G.nv(nu), G.clp[nu] - o.x_base, 1, 0);
       pb.add(0, 0, S.col_out(G, 0, nu), c, &t, 1);
@@ -271,13 +284,17 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
   for (int l = 1; l <= lc; ++l)
     for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
       for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
-        if (!o.own.col(G, l, nu)) continue;
+        if (!o.own.col(G, l, nu) || !o.tr(l, tau) || !o.tc(l, nu)) continue;
         const int64_t i = G.idx(l, tau, nu);
         const int64_t i1 = G.idx(l - 1, tau >> 1, 2 * nu), i2 = i1 + 1;
         const int c = G.c(l, i), c1 = G.c(l - 1, i1), c2 = G.c(l - 1, i2);
         Term t[2] = {mk(F.w + G.w_off[l][i], 1, c, c1, S.col_in(G, l - 1, i1), 0, 0),
                      mk(F.w + G.w_off[l][i] + int64_t(c1) * c, 1, c, c2, S.col_in(G, l - 1, i2), 0, 0)};
-        if (c1 > 0 && c2 > 0 && t[1].in_row == t[0].in_row + c1) {  // adjacent inputs: one term
+        // extraction: an untouched child holds no requested column (its product is zero, its
+        // slab is never written): drop its term
+        if (!o.tc(l - 1, 2 * nu)) t[0].k = 0;
+        if (!o.tc(l - 1, 2 * nu + 1)) t[1].k = 0;
+        if (t[0].k > 0 && t[1].k > 0 && t[1].in_row == t[0].in_row + c1) {  // adjacent inputs: one term
           t[0].k = c1 + c2;
           pb.add(l, 0, S.col_out(G, l, i), c, t, 1);
         } else {
@@ -286,7 +303,7 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
       }
   for (int64_t i = 0; i < G.nb; ++i) {
     const int64_t nu = i & ((int64_t(1) << (L - lc)) - 1);
-    if (!o.own.col(G, lc, nu)) continue;
+    if (!o.own.col(G, lc, nu) || !o.tr(lc, i >> (L - lc)) || !o.tc(lc, nu)) continue;
     const int r = G.r(lc, i), c = G.c(lc, i);
     Term t = mk(F.b + G.b_off[i], 1, r, c, S.col_in(G, lc, i), 0, 0);
     pb.add(lc + 1, 0, S.row_out(G, lc, i), r, &t, 1);
@@ -294,7 +311,7 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
   for (int l = lc; l < L; ++l)
     for (int64_t tp = 0; tp < (int64_t(1) << (l + 1)); ++tp)
       for (int64_t np = 0; np < (int64_t(1) << (L - l - 1)); ++np) {
-        if (!o.own.row(l + 1, tp)) continue;
+        if (!o.own.row(l + 1, tp) || !o.tr(l + 1, tp) || !o.tc(l + 1, np)) continue;
         const int64_t a = tp >> 1;
         const int part = (int)(tp & 1);
         const int rt = G.r(l + 1, G.idx(l + 1, 2 * a, np)), rb = G.r(l + 1, G.idx(l + 1, 2 * a + 1, np));
@@ -302,13 +319,14 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
         for (int s = 0; s < 2; ++s) {
           const int64_t i = G.idx(l, a, 2 * np + s);
           t[s] = mk(F.r + G.r_off[l][i] + (part ? rt : 0), 1, rt + rb, G.r(l, i), S.row_in(G, l, i), 0, 0);
+          if (!o.tc(l, 2 * np + s)) t[s].k = 0;  // extraction: untouched input (zero, never written)
         }
         const int64_t io = G.idx(l + 1, tp, np);
         pb.add(lc + 2 + (l - lc), 0, S.row_out(G, l + 1, io), G.r(l + 1, io), t, 2);
       }
   if (o.leaf_out)
     for (int64_t tau = 0; tau < G.nb; ++tau) {
-      if (!o.own.row(L, tau)) continue;
+      if (!o.own.row(L, tau) || !o.tr(L, tau)) continue;
       Term t = mk(F.u + G.u_off[tau], 1, (int)G.mt(tau), G.r(L, tau), S.row_in(G, L, tau), 0, 0);
       pb.add(L + 2, 1, G.rlp[tau] - o.y_base, G.mt(tau), &t, 1);
     }
@@ -946,6 +964,7 @@ struct bf_s {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
   int64_t hcalls = 0;
+  std::vector<int64_t> h_rinv, h_cinv;  // bf_extract: user index -> tree position (filled on first use)
   ~bf_s() {
     if (host_only) return;
     cudaSetDevice(device);
@@ -1037,6 +1056,28 @@ static Slabs canonical_slabs(const Geom& G, int64_t& cursor) {
       S.row[(size_t)(l - G.lc) * G.nb + i] = cursor;
       cursor += G.r(l, i);
     }
+  return S;
+}
+
+// slab rows of the touched blocks only (bf_extract): untouched blocks get none (no term reads
+// them -- emit_N drops their terms)
+static Slabs touched_slabs(const Geom& G, const Touch& T, int64_t& cursor) {
+  Slabs S;
+  S.col.assign((size_t)(G.lc + 1) * G.nb, -1);
+  S.row.assign((size_t)(G.L - G.lc + 1) * G.nb, -1);
+  const int L = G.L;
+  for (int l = 0; l <= G.lc; ++l)
+    for (int64_t i = 0; i < G.nb; ++i)
+      if (T.r(l, i >> (L - l)) && T.c(l, i & ((int64_t(1) << (L - l)) - 1))) {
+        S.col[(size_t)l * G.nb + i] = cursor;
+        cursor += G.c(l, i);
+      }
+  for (int l = G.lc; l <= L; ++l)
+    for (int64_t i = 0; i < G.nb; ++i)
+      if (T.r(l, i >> (L - l)) && T.c(l, i & ((int64_t(1) << (L - l)) - 1))) {
+        S.row[(size_t)(l - G.lc) * G.nb + i] = cursor;
+        cursor += G.r(l, i);
+      }
   return S;
 }
 
@@ -2166,6 +2207,149 @@ int bf_dist_apply_pre_p2p(bf_handle h, int op, int64_t nrhs, const void* X_loc, 
 int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy, void* work, size_t work_bytes,
                        bf_stream_t stream) {
   return dist_run(h, op, nrhs, nullptr, 0, Y_loc, ldy, work, work_bytes, stream, false);
+}
+
+// K(I, J) as a partial matvec (Alg. 3 extract_BF): K E_J evaluated only on the
+// blocks a requested row and column touch, through the generic tile kernel.  The requested
+// columns enter as unit vectors (X_small: one row per position of a touched column leaf), the
+// touched row leaves' outputs land in a scratch block, and the requested rows are gathered.
+int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
+               int64_t ldo, bf_stream_t stream) {
+  try {
+    require(h != nullptr, BF_ERR_ARG, "NULL handle");
+    require(!h->dist, BF_ERR_ARG, "bf_extract needs a single-device handle");
+    require(nI >= 0 && nJ >= 0, BF_ERR_ARG, "negative size");
+    if (nI == 0 || nJ == 0) return BF_OK;
+    require(rows != nullptr && cols != nullptr && out != nullptr, BF_ERR_ARG, "NULL argument");
+    require(ldo >= nI, BF_ERR_ARG, "ldo < number of rows");
+    require(nJ <= (int64_t)65535 * 32, BF_ERR_ARG, "too many columns for one launch");
+    const Geom& G = h->G;
+    const int L = G.L;
+    for (int64_t i = 0; i < nI; ++i) require(rows[i] >= 0 && rows[i] < G.m, BF_ERR_ARG, "row index out of range");
+    for (int64_t j = 0; j < nJ; ++j) require(cols[j] >= 0 && cols[j] < G.n, BF_ERR_ARG, "column index out of range");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t cs = csize(h->dtype);
+    // tree positions of the requested rows / columns (inverse perms, cached on the host)
+    {
+      std::lock_guard<std::mutex> lk(h->hmu);
+      if (h->h_rinv.empty()) {
+        std::vector<int64_t> rp(G.m), cp(G.n);
+        if (h->d_rperm) BF_CK(cudaMemcpy(rp.data(), h->d_rperm, G.m * 8, cudaMemcpyDeviceToHost));
+        else for (int64_t i = 0; i < G.m; ++i) rp[i] = i;
+        if (h->d_cperm) BF_CK(cudaMemcpy(cp.data(), h->d_cperm, G.n * 8, cudaMemcpyDeviceToHost));
+        else for (int64_t i = 0; i < G.n; ++i) cp[i] = i;
+        h->h_rinv.assign(G.m, 0);
+        h->h_cinv.assign(G.n, 0);
+        for (int64_t p = 0; p < G.m; ++p) h->h_rinv[rp[p]] = p;
+        for (int64_t p = 0; p < G.n; ++p) h->h_cinv[cp[p]] = p;
+      }
+    }
+    auto leaf_of = [](const std::vector<int64_t>& lp, int64_t p) {
+      return (int64_t)(std::upper_bound(lp.begin(), lp.end(), p) - lp.begin()) - 1;
+    };
+    Touch T;
+    T.row.resize(L + 1);
+    T.col.resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      T.row[l].assign((size_t)1 << l, 0);
+      T.col[l].assign((size_t)1 << (L - l), 0);
+    }
+    std::vector<int64_t> pr(nI), pc(nJ);
+    for (int64_t i = 0; i < nI; ++i) {
+      pr[i] = h->h_rinv[rows[i]];
+      const int64_t tau = leaf_of(G.rlp, pr[i]);
+      for (int l = 0; l <= L; ++l) T.row[l][tau >> (L - l)] = 1;
+    }
+    for (int64_t j = 0; j < nJ; ++j) {
+      pc[j] = h->h_cinv[cols[j]];
+      const int64_t nu = leaf_of(G.clp, pc[j]);
+      for (int l = 0; l <= L; ++l) T.col[l][nu >> l] = 1;
+    }
+    // X_small: one row per position of a touched column leaf, unit entries at the requested
+    // columns; Y_ext: one row per position of a touched row leaf
+    std::vector<int64_t> xperm(G.n, 0), yperm(G.m, 0);
+    int64_t nx = 0, ny = 0;
+    for (int64_t nu = 0; nu < G.nb; ++nu)
+      if (T.c(0, nu))
+        for (int64_t p = G.clp[nu]; p < G.clp[nu + 1]; ++p) xperm[p] = nx++;
+    for (int64_t tau = 0; tau < G.nb; ++tau)
+      if (T.r(L, tau))
+        for (int64_t p = G.rlp[tau]; p < G.rlp[tau + 1]; ++p) yperm[p] = ny++;
+    nx = std::max<int64_t>(nx, 1);
+    ny = std::max<int64_t>(ny, 1);
+    std::vector<char> Xs((size_t)(nx * nJ) * cs, 0);
+    for (int64_t j = 0; j < nJ; ++j) {
+      char* e = Xs.data() + (size_t)(xperm[pc[j]] + j * nx) * cs;
+      if (cs == 16) reinterpret_cast<double2*>(e)->x = 1.0;
+      else reinterpret_cast<float2*>(e)->x = 1.f;
+    }
+    std::vector<int64_t> rowidx(nI);
+    for (int64_t i = 0; i < nI; ++i) rowidx[i] = yperm[pr[i]];
+    // the touched blocks' plan
+    FBase F;
+    F.u = 0;
+    F.r = G.len_U;
+    F.b = F.r + G.len_R;
+    F.w = F.b + G.len_B;
+    F.vt = F.w + G.len_W;
+    int64_t cursor = 0;
+    Slabs S = touched_slabs(G, T, cursor);
+    PlanBuilder pb;
+    EmitOpts o;
+    o.touch = &T;
+    emit_N(pb, G, F, S, o);
+    Plan P;
+    size_t pbytes = 0;
+    upload_plan(P, pb, 0, (int)pb.tasks.size(), &pbytes);
+    // device temporaries: slab space, X_small, Y_ext, perms, row map (freed after the call)
+    std::vector<void*> tmp;
+    auto dalloc = [&](size_t b) {
+      void* p = nullptr;
+      BF_CK(cudaMalloc(&p, std::max<size_t>(b, 256)));
+      tmp.push_back(p);
+      return p;
+    };
+    try {
+      void* dS = dalloc((size_t)cursor * (size_t)nJ * cs);
+      void* dX = dalloc(Xs.size());
+      void* dY = dalloc((size_t)(ny * nJ) * cs);
+      int64_t* dxp = static_cast<int64_t*>(dalloc(xperm.size() * 8));
+      int64_t* dyp = static_cast<int64_t*>(dalloc(yperm.size() * 8));
+      int64_t* dri = static_cast<int64_t*>(dalloc(rowidx.size() * 8));
+      BF_CK(cudaMemcpyAsync(dX, Xs.data(), Xs.size(), cudaMemcpyHostToDevice, st));
+      BF_CK(cudaMemcpyAsync(dxp, xperm.data(), xperm.size() * 8, cudaMemcpyHostToDevice, st));
+      BF_CK(cudaMemcpyAsync(dyp, yperm.data(), yperm.size() * 8, cudaMemcpyHostToDevice, st));
+      BF_CK(cudaMemcpyAsync(dri, rowidx.data(), rowidx.size() * 8, cudaMemcpyHostToDevice, st));
+      StageArgs a{};
+      a.pool = h->pool;
+      a.m3 = h->m3;
+      a.X = dX;
+      a.ldx = nx;
+      a.xperm = dxp;
+      a.S = dS;
+      a.ldS = nJ;
+      a.Y = dY;
+      a.ldy = ny;
+      a.yperm = dyp;
+      a.conj_flip = 0;
+      a.nrhs = (int32_t)nJ;
+      run_plan(h->dtype, P, a, st);
+      launch_gather_rows(h->dtype, nI, nJ, dY, ny, dri, out, ldo, st);
+      BF_CK(cudaGetLastError());
+      BF_CK(cudaStreamSynchronize(st));  // the host buffers above and the temporaries end here
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      for (void* p : tmp) cudaFree(p);
+      free_plan(P);
+      throw;
+    }
+    for (void* p : tmp) cudaFree(p);
+    free_plan(P);
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
 }
 
 int bf_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,

@@ -1,0 +1,67 @@
+"""GPU parity of bf_extract (Alg. 3 extract_BF; the sub-matrix
+K(I, J) as a partial matvec over the touched blocks) against the CPU oracle's entries of K:
+random uniform-rank butterflies (fused-path shapes; extraction runs the generic kernel),
+ragged ranks, permuted rows / columns, repeated and scattered indices, single entries, whole
+leaf blocks, both dtypes; the closed-form identity extracts exactly."""
+import numpy as np
+import pytest
+
+import oracle
+from bfinputs import identity_butterfly, random_butterfly, random_ranks_butterfly
+import paper_2007_00202_b200 as pkg
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.complex128: 1e-12, np.complex64: 1e-5}
+
+
+def _get(h, I, J):
+    return h.extract(I, J).cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("L,leaf,r", [(6, 16, 16), (9, 16, 16), (5, 32, 8)])
+def test_extract_random(L, leaf, r, dtype):
+    bf = random_butterfly(L=L, leaf=leaf, r=r, seed=L + r, dtype=dtype)
+    rng = np.random.default_rng(L)
+    bf.row_perm = rng.permutation(bf.m).astype(np.int64)
+    bf.col_perm = rng.permutation(bf.n).astype(np.int64)
+    h = pkg.BFHandle(bf)
+    cases = [
+        (rng.integers(0, bf.m, 37), rng.integers(0, bf.n, 29)),          # scattered, repeats
+        (np.arange(leaf, 3 * leaf), np.arange(bf.n - 2 * leaf, bf.n)),    # contiguous user ranges
+        ([5], [bf.n - 1]),                                                # one entry
+        (rng.integers(0, bf.m, 300), rng.integers(0, bf.n, 70)),         # many leaves
+    ]
+    for I, J in cases:
+        got = _get(h, I, J)
+        ref = oracle.bf_extract(bf, I, J)
+        assert got.shape == (len(I), len(J))
+        assert oracle.rel_err(got, ref) <= TOL[dtype], (len(I), len(J))
+
+
+def test_extract_ragged_ranks():
+    rng = np.random.default_rng(4)
+    bf = random_ranks_butterfly(6, rng.integers(1, 9, 64), rng.integers(1, 9, 64), seed=4, rmin=1, rmax=7)
+    h = pkg.BFHandle(bf)
+    I, J = rng.integers(0, bf.m, 41), rng.integers(0, bf.n, 23)
+    assert oracle.rel_err(_get(h, I, J), oracle.bf_extract(bf, I, J)) <= 1e-12
+
+
+def test_extract_identity_exact():
+    bf = identity_butterfly(6, 4)
+    h = pkg.BFHandle(bf)
+    rng = np.random.default_rng(1)
+    I = rng.integers(0, bf.m, 50)
+    J = np.concatenate([I[:20], rng.integers(0, bf.n, 30)])
+    np.testing.assert_array_equal(_get(h, I, J), (I[:, None] == J[None, :]).astype(np.complex128))
+
+
+def test_extract_errors():
+    bf = random_butterfly(L=3, leaf=8, r=4, seed=2)
+    h = pkg.BFHandle(bf)
+    with pytest.raises(pkg.BFError):
+        h.extract([bf.m], [0])
+    with pytest.raises(pkg.BFError):
+        h.extract([0], [-1])
+    assert h.extract([], [1, 2]).shape == (0, 2)

@@ -277,3 +277,27 @@ def test_ID_exact_on_low_rank():
     assert Vt.shape[0] == 6
     np.testing.assert_allclose(Vt[:, J], np.eye(6), atol=0)
     assert np.linalg.norm(M[:, J] @ Vt - M) < 1e-11 * np.linalg.norm(M)
+
+
+# ------------------------------------------------------------------ extraction (NEXT-1)
+@pytest.mark.parametrize("L,m0", [(4, 2), (3, 3)])
+def test_extract_identity_closed_form(L, m0):
+    """extract_BF of the closed-form identity butterfly (P1) is the Kronecker delta of the
+    requested indices (repeats included)."""
+    bf = identity_butterfly(L, m0)
+    rng = np.random.default_rng(L)
+    I = rng.integers(0, bf.m, 9)
+    J = np.concatenate([I[:4], rng.integers(0, bf.n, 5)])
+    E = oracle.bf_extract(bf, I, J)
+    assert np.array_equal(E, (I[:, None] == J[None, :]).astype(np.complex128))
+
+
+def test_extract_dft_closed_form():
+    """extract_BF of the closed-form DFT butterfly (P3) is omega^(i j), omega = e^(-2 pi i / n)."""
+    L = 8
+    bf = dft_butterfly(L)
+    n = bf.n
+    rng = np.random.default_rng(3)
+    I, J = rng.integers(0, n, 11), rng.integers(0, n, 7)
+    ref = np.exp(-2j * np.pi * ((I[:, None] * J[None, :]) % n) / n)
+    assert np.abs(oracle.bf_extract(bf, I, J) - ref).max() < 1e-13
