@@ -265,28 +265,62 @@ void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int
                                                static_cast<float2*>(Y), ldy);
 }
 
-// out(i, j) = Y(rowidx[i], j), column-major (bf_extract's final gather of the requested rows)
+// bf_extract, first round (the column leaves on unit vectors, Eq. 3.3's V^0 applied to E_J):
+// z^0 slab column j of leaf nu(j) = Vt_nu(:, local column of j).  jmap[j] = {slab row of the
+// leaf's z^0, rank c, pool offset of that Vt column}; the slabs were zeroed before.
 template <typename V>
-__global__ void k_gather_rows(int64_t nI, int64_t nJ, const V* __restrict__ Y, int64_t ldy,
-                              const int64_t* __restrict__ rowidx, V* __restrict__ out, int64_t ldo) {
-  const int64_t total = nI * nJ;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = i / nI, r = i - c * nI;
-    out[r + c * ldo] = Y[rowidx[r] + c * ldy];
+__global__ void k_extract_vt_cols(int64_t nJ, const int64_t* __restrict__ jmap, const V* __restrict__ pool,
+                                  V* __restrict__ S) {
+  for (int64_t j = blockIdx.x; j < nJ; j += gridDim.x) {
+    const int64_t row0 = jmap[3 * j], c = jmap[3 * j + 1], off = jmap[3 * j + 2];
+    for (int64_t r = threadIdx.x; r < c; r += blockDim.x) S[(row0 + r) * nJ + j] = pool[off + r];
   }
 }
 
-void launch_gather_rows(int dtype, int64_t nI, int64_t nJ, const void* Y, int64_t ldy, const int64_t* rowidx,
-                        void* out, int64_t ldo, cudaStream_t st) {
+// bf_extract, last round (Eq. 3.3's U^L restricted to the requested rows): out(i, :) =
+// U_tau(row i, :) y^L_tau (1 x r times r x nJ, slab rows nJ wide).  imap[i] = {pool offset of
+// U_tau's row (stride m_tau), m_tau, rank r, slab row of y^L_tau}.
+template <typename V>
+__global__ void k_extract_u_rows(int64_t nI, int64_t nJ, const int64_t* __restrict__ imap,
+                                 const V* __restrict__ pool, const V* __restrict__ S, V* __restrict__ out,
+                                 int64_t ldo) {
+  const int64_t total = nI * nJ;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q % nI, j = q / nI;
+    const int64_t off = imap[4 * i], mt = imap[4 * i + 1], r = imap[4 * i + 2], row0 = imap[4 * i + 3];
+    decltype(V::x) re = 0, im = 0;
+    for (int64_t k = 0; k < r; ++k) {
+      const V u = pool[off + k * mt], y = S[(row0 + k) * nJ + j];
+      re += u.x * y.x - u.y * y.y;
+      im += u.x * y.y + u.y * y.x;
+    }
+    V o;
+    o.x = re;
+    o.y = im;
+    out[i + j * ldo] = o;
+  }
+}
+
+void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const void* pool, void* S, cudaStream_t st) {
+  if (nJ == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(nJ, 65535);
+  if (dtype == BF_C128)
+    k_extract_vt_cols<double2><<<grid, 64, 0, st>>>(nJ, jmap, static_cast<const double2*>(pool), static_cast<double2*>(S));
+  else
+    k_extract_vt_cols<float2><<<grid, 64, 0, st>>>(nJ, jmap, static_cast<const float2*>(pool), static_cast<float2*>(S));
+}
+
+void launch_extract_u_rows(int dtype, int64_t nI, int64_t nJ, const int64_t* imap, const void* pool, const void* S,
+                           void* out, int64_t ldo, cudaStream_t st) {
   const int64_t total = nI * nJ;
   if (total == 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 4096);
   if (dtype == BF_C128)
-    k_gather_rows<double2><<<grid, 256, 0, st>>>(nI, nJ, static_cast<const double2*>(Y), ldy, rowidx,
-                                                 static_cast<double2*>(out), ldo);
+    k_extract_u_rows<double2><<<grid, 256, 0, st>>>(nI, nJ, imap, static_cast<const double2*>(pool),
+                                                    static_cast<const double2*>(S), static_cast<double2*>(out), ldo);
   else
-    k_gather_rows<float2><<<grid, 256, 0, st>>>(nI, nJ, static_cast<const float2*>(Y), ldy, rowidx,
-                                                static_cast<float2*>(out), ldo);
+    k_extract_u_rows<float2><<<grid, 256, 0, st>>>(nI, nJ, imap, static_cast<const float2*>(pool),
+                                                   static_cast<const float2*>(S), static_cast<float2*>(out), ldo);
 }
 
 const char* round_kernel_name(int dtype, const Round& r, int* id) {

@@ -1,3 +1,4 @@
+#include <chrono>
 // Host side of libbfapply: descriptor validation, device upload, and the per-op plans
 // (Task / Term tables) that turn Eq. (3.3) into a short sequence of batched launches.
 //
@@ -258,6 +259,7 @@ static Term mk(int64_t a_off, int a_rs, int a_cs, int64_t k, int64_t in_row, int
 struct Touch {
   std::vector<std::vector<uint8_t>> row;  // [l][tau], l = 0..L
   std::vector<std::vector<uint8_t>> col;  // [l][nu],  nu at T_S level L - l
+  std::vector<std::vector<int64_t>> rows, cols;  // the same as ascending lists
   bool r(int l, int64_t tau) const { return row[l][tau] != 0; }
   bool c(int l, int64_t nu) const { return col[l][nu] != 0; }
 };
@@ -266,9 +268,6 @@ struct EmitOpts {
   bool leaf_in = true, leaf_out = true;  // emit the V / U leaf stages (HOD-BF fuses them)
   int64_t x_base = 0, y_base = 0;        // tree position of local X / Y row 0
   Own own;
-  const Touch* touch = nullptr;          // extraction: emit only the touched blocks (op N)
-  bool tr(int l, int64_t tau) const { return !touch || touch->r(l, tau); }
-  bool tc(int l, int64_t nu) const { return !touch || touch->c(l, nu); }
 };
 
 // op N rounds: 0 leaf V, 1..lc W, lc+1 B, lc+2.. R, L+2 leaf U
@@ -276,7 +275,7 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
   const int L = G.L, lc = G.lc;
   if (o.leaf_in)
     for (int64_t nu = 0; nu < G.nb; ++nu) {
-      if (!o.own.col(G, 0, nu) || !o.tc(0, nu)) continue;
+      if (!o.own.col(G, 0, nu)) continue;
       const int c = G.c(0, nu);
       Term t = mk(F.vt + G.vt_off[nu], 1, c, G.nv(nu), G.clp[nu] - o.x_base, 1, 0);
       pb.add(0, 0, S.col_out(G, 0, nu), c, &t, 1);
@@ -284,17 +283,13 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
   for (int l = 1; l <= lc; ++l)
     for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
       for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
-        if (!o.own.col(G, l, nu) || !o.tr(l, tau) || !o.tc(l, nu)) continue;
+        if (!o.own.col(G, l, nu)) continue;
         const int64_t i = G.idx(l, tau, nu);
         const int64_t i1 = G.idx(l - 1, tau >> 1, 2 * nu), i2 = i1 + 1;
         const int c = G.c(l, i), c1 = G.c(l - 1, i1), c2 = G.c(l - 1, i2);
         Term t[2] = {mk(F.w + G.w_off[l][i], 1, c, c1, S.col_in(G, l - 1, i1), 0, 0),
                      mk(F.w + G.w_off[l][i] + int64_t(c1) * c, 1, c, c2, S.col_in(G, l - 1, i2), 0, 0)};
-        // extraction: an untouched child holds no requested column (its product is zero, its
-        // slab is never written): drop its term
-        if (!o.tc(l - 1, 2 * nu)) t[0].k = 0;
-        if (!o.tc(l - 1, 2 * nu + 1)) t[1].k = 0;
-        if (t[0].k > 0 && t[1].k > 0 && t[1].in_row == t[0].in_row + c1) {  // adjacent inputs: one term
+        if (c1 > 0 && c2 > 0 && t[1].in_row == t[0].in_row + c1) {  // adjacent inputs: one term
           t[0].k = c1 + c2;
           pb.add(l, 0, S.col_out(G, l, i), c, t, 1);
         } else {
@@ -303,7 +298,7 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
       }
   for (int64_t i = 0; i < G.nb; ++i) {
     const int64_t nu = i & ((int64_t(1) << (L - lc)) - 1);
-    if (!o.own.col(G, lc, nu) || !o.tr(lc, i >> (L - lc)) || !o.tc(lc, nu)) continue;
+    if (!o.own.col(G, lc, nu)) continue;
     const int r = G.r(lc, i), c = G.c(lc, i);
     Term t = mk(F.b + G.b_off[i], 1, r, c, S.col_in(G, lc, i), 0, 0);
     pb.add(lc + 1, 0, S.row_out(G, lc, i), r, &t, 1);
@@ -311,7 +306,7 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
   for (int l = lc; l < L; ++l)
     for (int64_t tp = 0; tp < (int64_t(1) << (l + 1)); ++tp)
       for (int64_t np = 0; np < (int64_t(1) << (L - l - 1)); ++np) {
-        if (!o.own.row(l + 1, tp) || !o.tr(l + 1, tp) || !o.tc(l + 1, np)) continue;
+        if (!o.own.row(l + 1, tp)) continue;
         const int64_t a = tp >> 1;
         const int part = (int)(tp & 1);
         const int rt = G.r(l + 1, G.idx(l + 1, 2 * a, np)), rb = G.r(l + 1, G.idx(l + 1, 2 * a + 1, np));
@@ -319,17 +314,57 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
         for (int s = 0; s < 2; ++s) {
           const int64_t i = G.idx(l, a, 2 * np + s);
           t[s] = mk(F.r + G.r_off[l][i] + (part ? rt : 0), 1, rt + rb, G.r(l, i), S.row_in(G, l, i), 0, 0);
-          if (!o.tc(l, 2 * np + s)) t[s].k = 0;  // extraction: untouched input (zero, never written)
         }
         const int64_t io = G.idx(l + 1, tp, np);
         pb.add(lc + 2 + (l - lc), 0, S.row_out(G, l + 1, io), G.r(l + 1, io), t, 2);
       }
   if (o.leaf_out)
     for (int64_t tau = 0; tau < G.nb; ++tau) {
-      if (!o.own.row(L, tau) || !o.tr(L, tau)) continue;
+      if (!o.own.row(L, tau)) continue;
       Term t = mk(F.u + G.u_off[tau], 1, (int)G.mt(tau), G.r(L, tau), S.row_in(G, L, tau), 0, 0);
       pb.add(L + 2, 1, G.rlp[tau] - o.y_base, G.mt(tau), &t, 1);
     }
+}
+
+// bf_extract: the inner op-N rounds of emit_N (W stages, centre, R stages) over the touched
+// blocks only (O(touched) work per query); the two leaf rounds are bf_extract's own kernels
+// (Vt columns of the requested columns, U rows of the requested rows)
+static void emit_N_touched(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& S, const Touch& T) {
+  const int L = G.L, lc = G.lc;
+  for (int l = 1; l <= lc; ++l)
+    for (int64_t tau : T.rows[l])
+      for (int64_t nu : T.cols[l]) {
+        const int64_t i = G.idx(l, tau, nu);
+        const int64_t i1 = G.idx(l - 1, tau >> 1, 2 * nu), i2 = i1 + 1;
+        const int c = G.c(l, i), c1 = G.c(l - 1, i1), c2 = G.c(l - 1, i2);
+        Term t[2] = {mk(F.w + G.w_off[l][i], 1, c, c1, S.col_in(G, l - 1, i1), 0, 0),
+                     mk(F.w + G.w_off[l][i] + int64_t(c1) * c, 1, c, c2, S.col_in(G, l - 1, i2), 0, 0)};
+        if (!T.c(l - 1, 2 * nu)) t[0].k = 0;
+        if (!T.c(l - 1, 2 * nu + 1)) t[1].k = 0;
+        pb.add(l, 0, S.col_out(G, l, i), c, t, 2);
+      }
+  for (int64_t tau : T.rows[lc])
+    for (int64_t nu : T.cols[lc]) {
+      const int64_t i = G.idx(lc, tau, nu);
+      const int r = G.r(lc, i), c = G.c(lc, i);
+      Term t = mk(F.b + G.b_off[i], 1, r, c, S.col_in(G, lc, i), 0, 0);
+      pb.add(lc + 1, 0, S.row_out(G, lc, i), r, &t, 1);
+    }
+  for (int l = lc; l < L; ++l)
+    for (int64_t tp : T.rows[l + 1])
+      for (int64_t np : T.cols[l + 1]) {
+        const int64_t a = tp >> 1;
+        const int part = (int)(tp & 1);
+        const int rt = G.r(l + 1, G.idx(l + 1, 2 * a, np)), rb = G.r(l + 1, G.idx(l + 1, 2 * a + 1, np));
+        Term t[2];
+        for (int s = 0; s < 2; ++s) {
+          const int64_t i = G.idx(l, a, 2 * np + s);
+          t[s] = mk(F.r + G.r_off[l][i] + (part ? rt : 0), 1, rt + rb, G.r(l, i), S.row_in(G, l, i), 0, 0);
+          if (!T.c(l, 2 * np + s)) t[s].k = 0;
+        }
+        const int64_t io = G.idx(l + 1, tp, np);
+        pb.add(lc + 2 + (l - lc), 0, S.row_out(G, l + 1, io), G.r(l + 1, io), t, 2);
+      }
 }
 
 // op C rounds: 0 leaf U^H, 1..L-lc R^H, L-lc+1 B^H, .. W^H, L+2 leaf Vt^H
@@ -965,6 +1000,9 @@ struct bf_s {
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
   int64_t hcalls = 0;
   std::vector<int64_t> h_rinv, h_cinv;  // bf_extract: user index -> tree position (filled on first use)
+  std::mutex xmu;                       // bf_extract: its scratch
+  void* xbuf = nullptr;
+  size_t xbuf_bytes = 0;
   ~bf_s() {
     if (host_only) return;
     cudaSetDevice(device);
@@ -991,6 +1029,7 @@ struct bf_s {
     if (pool) cudaFree(pool);
     if (d_rperm) cudaFree(d_rperm);
     if (d_cperm) cudaFree(d_cperm);
+    if (xbuf) cudaFree(xbuf);
   }
 };
 
@@ -1065,16 +1104,17 @@ static Slabs touched_slabs(const Geom& G, const Touch& T, int64_t& cursor) {
   Slabs S;
   S.col.assign((size_t)(G.lc + 1) * G.nb, -1);
   S.row.assign((size_t)(G.L - G.lc + 1) * G.nb, -1);
-  const int L = G.L;
   for (int l = 0; l <= G.lc; ++l)
-    for (int64_t i = 0; i < G.nb; ++i)
-      if (T.r(l, i >> (L - l)) && T.c(l, i & ((int64_t(1) << (L - l)) - 1))) {
+    for (int64_t tau : T.rows[l])
+      for (int64_t nu : T.cols[l]) {
+        const int64_t i = G.idx(l, tau, nu);
         S.col[(size_t)l * G.nb + i] = cursor;
         cursor += G.c(l, i);
       }
-  for (int l = G.lc; l <= L; ++l)
-    for (int64_t i = 0; i < G.nb; ++i)
-      if (T.r(l, i >> (L - l)) && T.c(l, i & ((int64_t(1) << (L - l)) - 1))) {
+  for (int l = G.lc; l <= G.L; ++l)
+    for (int64_t tau : T.rows[l])
+      for (int64_t nu : T.cols[l]) {
+        const int64_t i = G.idx(l, tau, nu);
         S.row[(size_t)(l - G.lc) * G.nb + i] = cursor;
         cursor += G.r(l, i);
       }
@@ -2230,6 +2270,14 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
     DeviceGuard dg(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t cs = csize(h->dtype);
+    static const bool tdbg = getenv("BF_EXTRACT_TIMING") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {
+      if (!tdbg) return;
+      auto t1 = std::chrono::steady_clock::now();
+      fprintf(stderr, "bf_extract %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+      t0 = t1;
+    };
     // tree positions of the requested rows / columns (inverse perms, cached on the host)
     {
       std::lock_guard<std::mutex> lk(h->hmu);
@@ -2266,26 +2314,14 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
       const int64_t nu = leaf_of(G.clp, pc[j]);
       for (int l = 0; l <= L; ++l) T.col[l][nu >> l] = 1;
     }
-    // X_small: one row per position of a touched column leaf, unit entries at the requested
-    // columns; Y_ext: one row per position of a touched row leaf
-    std::vector<int64_t> xperm(G.n, 0), yperm(G.m, 0);
-    int64_t nx = 0, ny = 0;
-    for (int64_t nu = 0; nu < G.nb; ++nu)
-      if (T.c(0, nu))
-        for (int64_t p = G.clp[nu]; p < G.clp[nu + 1]; ++p) xperm[p] = nx++;
-    for (int64_t tau = 0; tau < G.nb; ++tau)
-      if (T.r(L, tau))
-        for (int64_t p = G.rlp[tau]; p < G.rlp[tau + 1]; ++p) yperm[p] = ny++;
-    nx = std::max<int64_t>(nx, 1);
-    ny = std::max<int64_t>(ny, 1);
-    std::vector<char> Xs((size_t)(nx * nJ) * cs, 0);
-    for (int64_t j = 0; j < nJ; ++j) {
-      char* e = Xs.data() + (size_t)(xperm[pc[j]] + j * nx) * cs;
-      if (cs == 16) reinterpret_cast<double2*>(e)->x = 1.0;
-      else reinterpret_cast<float2*>(e)->x = 1.f;
+    T.rows.resize(L + 1);
+    T.cols.resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      for (size_t k = 0; k < T.row[l].size(); ++k)
+        if (T.row[l][k]) T.rows[l].push_back((int64_t)k);
+      for (size_t k = 0; k < T.col[l].size(); ++k)
+        if (T.col[l][k]) T.cols[l].push_back((int64_t)k);
     }
-    std::vector<int64_t> rowidx(nI);
-    for (int64_t i = 0; i < nI; ++i) rowidx[i] = yperm[pr[i]];
     // the touched blocks' plan
     FBase F;
     F.u = 0;
@@ -2295,57 +2331,73 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
     F.vt = F.w + G.len_W;
     int64_t cursor = 0;
     Slabs S = touched_slabs(G, T, cursor);
+    tick("touched sets + inputs");
     PlanBuilder pb;
-    EmitOpts o;
-    o.touch = &T;
-    emit_N(pb, G, F, S, o);
+    emit_N_touched(pb, G, F, S, T);
+    tick("plan");
     Plan P;
     size_t pbytes = 0;
+    std::lock_guard<std::mutex> lk(h->xmu);  // one extraction at a time uses the handle's scratch
     upload_plan(P, pb, 0, (int)pb.tasks.size(), &pbytes);
-    // device temporaries: slab space, X_small, Y_ext, perms, row map (freed after the call)
-    std::vector<void*> tmp;
-    auto dalloc = [&](size_t b) {
-      void* p = nullptr;
-      BF_CK(cudaMalloc(&p, std::max<size_t>(b, 256)));
-      tmp.push_back(p);
-      return p;
-    };
+    tick("plan upload");
     try {
-      void* dS = dalloc((size_t)cursor * (size_t)nJ * cs);
-      void* dX = dalloc(Xs.size());
-      void* dY = dalloc((size_t)(ny * nJ) * cs);
-      int64_t* dxp = static_cast<int64_t*>(dalloc(xperm.size() * 8));
-      int64_t* dyp = static_cast<int64_t*>(dalloc(yperm.size() * 8));
-      int64_t* dri = static_cast<int64_t*>(dalloc(rowidx.size() * 8));
-      BF_CK(cudaMemcpyAsync(dX, Xs.data(), Xs.size(), cudaMemcpyHostToDevice, st));
-      BF_CK(cudaMemcpyAsync(dxp, xperm.data(), xperm.size() * 8, cudaMemcpyHostToDevice, st));
-      BF_CK(cudaMemcpyAsync(dyp, yperm.data(), yperm.size() * 8, cudaMemcpyHostToDevice, st));
-      BF_CK(cudaMemcpyAsync(dri, rowidx.data(), rowidx.size() * 8, cudaMemcpyHostToDevice, st));
+      // the leaf maps: per requested column its Vt column, per requested row its U row
+      std::vector<int64_t> jmap(3 * nJ), imap(4 * nI);
+      for (int64_t j = 0; j < nJ; ++j) {
+        const int64_t nu = leaf_of(G.clp, pc[j]);
+        const int c = G.c(0, nu);
+        jmap[3 * j] = S.col_out(G, 0, nu);
+        jmap[3 * j + 1] = c;
+        jmap[3 * j + 2] = F.vt + G.vt_off[nu] + (pc[j] - G.clp[nu]) * c;
+      }
+      for (int64_t i = 0; i < nI; ++i) {
+        const int64_t tau = leaf_of(G.rlp, pr[i]);
+        imap[4 * i] = F.u + G.u_off[tau] + (pr[i] - G.rlp[tau]);
+        imap[4 * i + 1] = G.mt(tau);
+        imap[4 * i + 2] = G.r(L, tau);
+        imap[4 * i + 3] = S.row_in(G, L, tau);
+      }
+      int64_t rows0 = 0;  // z^0 slabs come first in the touched slab space
+      for (int64_t nu : T.cols[0]) rows0 += G.c(0, nu);
+      // device scratch (grow-only, handle-owned): slab space | column map | row map
+      const size_t bS = align256((size_t)cursor * (size_t)nJ * cs), bJ = align256(jmap.size() * 8),
+                   bI = align256(imap.size() * 8);
+      const size_t need = bS + bJ + bI;
+      if (h->xbuf_bytes < need) {
+        if (h->xbuf) cudaFree(h->xbuf);
+        h->xbuf = nullptr;
+        h->xbuf_bytes = 0;
+        BF_CK(cudaMalloc(&h->xbuf, need));
+        h->xbuf_bytes = need;
+      }
+      char* base = static_cast<char*>(h->xbuf);
+      void* dS = base;
+      int64_t* dj = reinterpret_cast<int64_t*>(base + bS);
+      int64_t* di = reinterpret_cast<int64_t*>(base + bS + bJ);
+      BF_CK(cudaMemcpyAsync(dj, jmap.data(), jmap.size() * 8, cudaMemcpyHostToDevice, st));
+      BF_CK(cudaMemcpyAsync(di, imap.data(), imap.size() * 8, cudaMemcpyHostToDevice, st));
+      BF_CK(cudaMemsetAsync(dS, 0, (size_t)rows0 * (size_t)nJ * cs, st));
+      tick("scratch + copies");
       StageArgs a{};
       a.pool = h->pool;
       a.m3 = h->m3;
-      a.X = dX;
-      a.ldx = nx;
-      a.xperm = dxp;
       a.S = dS;
       a.ldS = nJ;
-      a.Y = dY;
-      a.ldy = ny;
-      a.yperm = dyp;
       a.conj_flip = 0;
       a.nrhs = (int32_t)nJ;
+      launch_extract_vt_cols(h->dtype, nJ, dj, h->pool, dS, st);
       run_plan(h->dtype, P, a, st);
-      launch_gather_rows(h->dtype, nI, nJ, dY, ny, dri, out, ldo, st);
+      launch_extract_u_rows(h->dtype, nI, nJ, di, h->pool, dS, out, ldo, st);
       BF_CK(cudaGetLastError());
-      BF_CK(cudaStreamSynchronize(st));  // the host buffers above and the temporaries end here
+      BF_CK(cudaStreamSynchronize(st));  // the host buffers above and the plan end here
+      tick("kernels");
     } catch (...) {
       cudaStreamSynchronize(st);
-      for (void* p : tmp) cudaFree(p);
       free_plan(P);
       throw;
     }
-    for (void* p : tmp) cudaFree(p);
     free_plan(P);
+    tick("free");
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
