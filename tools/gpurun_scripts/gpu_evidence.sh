@@ -7,6 +7,7 @@ mkdir -p gpurun_out/ev
 O=gpurun_out/ev
 timeout 1500 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
 timeout 600 python bench.py > $O/bench_c128.json 2> $O/bench_c128.err
 timeout 600 python bench.py --dtype c64 > $O/bench_c64.json 2> $O/bench_c64.err
 timeout 600 python bench.py --op C --no-cpu-baseline > $O/bench_c128_C.json 2> $O/bench_c128_C.err
@@ -23,4 +24,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_st
 timeout 900 python tools/time_split.py c128 > $O/split_c128.txt 2>&1
 timeout 900 python tools/time_split.py c64 > $O/split_c64.txt 2>&1
 for dt in c128 c64; do timeout 120 python tools/time_apply.py $dt >> $O/apply_plain.txt 2>&1; done
+timeout 600 python tools/time_extract.py c128 > $O/extract_c128.txt 2>&1
 echo done
