@@ -107,6 +107,18 @@ def cpu_threads():
         return len(os.sched_getaffinity(0))
 
 
+def cpu_model():
+    """The host CPU's model name (SURVEY 8(d) timing protocol: cores and model with the oracle)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def oracle_sample(bf, X, nrows=(16, 128), centre=3):
     """Time the CPU oracle (sampled-row reconstruction) on rows of one
     centre node and extrapolate to the full apply with a two-point model
@@ -200,7 +212,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": WORKLOAD, "op": args.op, "nrhs": args.nrhs},
-            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                              "sample": sample + " (each step one such sample; value from the median extrapolation)"},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -360,7 +372,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         full, spent, sample = oracle_sample(bf, X)
-        cpu = {"value": ab / full / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
+        cpu = {"value": ab / full / 1e9, "unit": "GB/s", "cores": cpu_threads(), "cpu_model": cpu_model(), "kind": "oracle",
                "sample": sample}
 
     if rank == 0:
