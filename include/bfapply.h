@@ -219,6 +219,14 @@ int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t l
 int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
                int64_t ldo, bf_stream_t stream);
 
+/* HOD-BF sub-matrix extraction (extract_HODBF): out(i, j) =
+ * A(rows[i], cols[j]) for user indices, as bf_extract: the entries inside one leaf from D_t,
+ * every other one from the sibling butterfly of the level where the row's and the column's
+ * tree nodes split, each butterfly's share as a partial matvec over its touched blocks.
+ * Same arguments, errors and synchronous behaviour as bf_extract. */
+int hodbf_extract(hodbf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
+                  int64_t ldo, bf_stream_t stream);
+
 /* Y += A on a column-major rows x nrhs complex block (device pointers, ld >= rows): the sum of
  * the HOD-BF contributions of a tree-partitioned apply ("Y(T_tau) += B_tau X(...)"; the
  * row-side posts of the off-diagonal butterflies at the distributed levels write a scratch block

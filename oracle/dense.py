@@ -347,3 +347,10 @@ def bf_extract(bf, user_rows, user_cols) -> np.ndarray:
     E[cols, np.arange(len(cols))] = 1.0
     return bf_rows_apply(bf, ur, E)[inv]
 
+
+def hodbf_extract(H, user_rows, user_cols) -> np.ndarray:
+    """A(user_rows, user_cols) of an HOD-BF (extract_HODBF) by its
+    plain definition: the entries of the assembled matrix."""
+    A = hodbf_dense(H)
+    return A[np.ix_(np.asarray(user_rows, dtype=np.int64), np.asarray(user_cols, dtype=np.int64))]
+

@@ -103,6 +103,8 @@ _SIGS = [
                                      C.c_void_p, C.c_size_t, C.c_void_p]),
     ("bf_extract", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
                              C.c_void_p]),
+    ("hodbf_extract", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                C.c_void_p]),
     ("bf_accumulate", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                 C.c_void_p]),
     ("bf_rounds", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
@@ -422,6 +424,16 @@ class HODBFHandle:
         s = C.c_size_t()
         _check("hodbf_workspace_size", lib().hodbf_workspace_size(self.h, nrhs, C.byref(s)))
         return s.value
+
+    def extract(self, rows, cols, stream=None) -> torch.Tensor:
+        """A(rows, cols) as an (len(rows), len(cols)) device tensor (hodbf_extract; synchronous)."""
+        r = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+        c = np.ascontiguousarray(np.asarray(cols, dtype=np.int64))
+        out = torch.zeros((len(c), len(r)), dtype=_torch_dtype(self.code), device=torch.device("cuda", self.device))
+        _check("hodbf_extract", lib().hodbf_extract(self.h, len(r), r.ctypes.data_as(C.c_void_p), len(c),
+                                                    c.ctypes.data_as(C.c_void_p), C.c_void_p(out.data_ptr()),
+                                                    max(len(r), 1), _stream_handle(stream)))
+        return out.T
 
     def apply(self, X: torch.Tensor, op: str = "N", out=None, work=None, stream=None) -> torch.Tensor:
         ldx = _check_rhs(X, self.n, self.code, "X")

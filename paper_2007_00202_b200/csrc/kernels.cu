@@ -277,17 +277,18 @@ __global__ void k_extract_vt_cols(int64_t nJ, const int64_t* __restrict__ jmap, 
   }
 }
 
-// bf_extract, last round (Eq. 3.3's U^L restricted to the requested rows): out(i, :) =
-// U_tau(row i, :) y^L_tau (1 x r times r x nJ, slab rows nJ wide).  imap[i] = {pool offset of
-// U_tau's row (stride m_tau), m_tau, rank r, slab row of y^L_tau}.
+// bf_extract, last round (Eq. 3.3's U^L restricted to the requested rows): out(orow_i, ocol_j) =
+// U_tau(row i, :) y^L_tau(:, j) (1 x r times r x nJ, slab rows nJ wide).  imap[i] = {pool offset
+// of U_tau's row, its stride (m_tau), rank r, slab row of y^L_tau, output row}; ocol[j] = output
+// column.
 template <typename V>
 __global__ void k_extract_u_rows(int64_t nI, int64_t nJ, const int64_t* __restrict__ imap,
-                                 const V* __restrict__ pool, const V* __restrict__ S, V* __restrict__ out,
-                                 int64_t ldo) {
+                                 const int64_t* __restrict__ ocol, const V* __restrict__ pool,
+                                 const V* __restrict__ S, V* __restrict__ out, int64_t ldo) {
   const int64_t total = nI * nJ;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = q % nI, j = q / nI;
-    const int64_t off = imap[4 * i], mt = imap[4 * i + 1], r = imap[4 * i + 2], row0 = imap[4 * i + 3];
+    const int64_t off = imap[5 * i], mt = imap[5 * i + 1], r = imap[5 * i + 2], row0 = imap[5 * i + 3];
     decltype(V::x) re = 0, im = 0;
     for (int64_t k = 0; k < r; ++k) {
       const V u = pool[off + k * mt], y = S[(row0 + k) * nJ + j];
@@ -297,8 +298,25 @@ __global__ void k_extract_u_rows(int64_t nI, int64_t nJ, const int64_t* __restri
     V o;
     o.x = re;
     o.y = im;
-    out[i + j * ldo] = o;
+    out[imap[5 * i + 4] + ocol[j] * ldo] = o;
   }
+}
+
+// hodbf_extract: the dense-leaf entries, out[pairs[2q]] = pool[pairs[2q + 1]]
+template <typename V>
+__global__ void k_extract_gather(int64_t n, const int64_t* __restrict__ pairs, const V* __restrict__ pool,
+                                 V* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[pairs[2 * q]] = pool[pairs[2 * q + 1]];
+}
+
+void launch_extract_gather(int dtype, int64_t n, const int64_t* pairs, const void* pool, void* out, cudaStream_t st) {
+  if (n == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
+  if (dtype == BF_C128)
+    k_extract_gather<double2><<<grid, 256, 0, st>>>(n, pairs, static_cast<const double2*>(pool), static_cast<double2*>(out));
+  else
+    k_extract_gather<float2><<<grid, 256, 0, st>>>(n, pairs, static_cast<const float2*>(pool), static_cast<float2*>(out));
 }
 
 void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const void* pool, void* S, cudaStream_t st) {
@@ -310,16 +328,16 @@ void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const vo
     k_extract_vt_cols<float2><<<grid, 64, 0, st>>>(nJ, jmap, static_cast<const float2*>(pool), static_cast<float2*>(S));
 }
 
-void launch_extract_u_rows(int dtype, int64_t nI, int64_t nJ, const int64_t* imap, const void* pool, const void* S,
-                           void* out, int64_t ldo, cudaStream_t st) {
+void launch_extract_u_rows(int dtype, int64_t nI, int64_t nJ, const int64_t* imap, const int64_t* ocol,
+                           const void* pool, const void* S, void* out, int64_t ldo, cudaStream_t st) {
   const int64_t total = nI * nJ;
   if (total == 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 4096);
   if (dtype == BF_C128)
-    k_extract_u_rows<double2><<<grid, 256, 0, st>>>(nI, nJ, imap, static_cast<const double2*>(pool),
+    k_extract_u_rows<double2><<<grid, 256, 0, st>>>(nI, nJ, imap, ocol, static_cast<const double2*>(pool),
                                                     static_cast<const double2*>(S), static_cast<double2*>(out), ldo);
   else
-    k_extract_u_rows<float2><<<grid, 256, 0, st>>>(nI, nJ, imap, static_cast<const float2*>(pool),
+    k_extract_u_rows<float2><<<grid, 256, 0, st>>>(nI, nJ, imap, ocol, static_cast<const float2*>(pool),
                                                    static_cast<const float2*>(S), static_cast<float2*>(out), ldo);
 }
 

@@ -1,3 +1,4 @@
+#include <map>
 #include <chrono>
 // Host side of libbfapply: descriptor validation, device upload, and the per-op plans
 // (Task / Term tables) that turn Eq. (3.3) into a short sequence of batched launches.
@@ -262,6 +263,26 @@ struct Touch {
   std::vector<std::vector<int64_t>> rows, cols;  // the same as ascending lists
   bool r(int l, int64_t tau) const { return row[l][tau] != 0; }
   bool c(int l, int64_t nu) const { return col[l][nu] != 0; }
+};
+
+// grow-only device scratch of the extraction calls of one handle
+struct XScratch {
+  std::mutex mu;
+  void* buf = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (bytes < need) {
+      if (buf) cudaFree(buf);
+      buf = nullptr;
+      bytes = 0;
+      BF_CK(cudaMalloc(&buf, need));
+      bytes = need;
+    }
+    return buf;
+  }
+  ~XScratch() {
+    if (buf) cudaFree(buf);
+  }
 };
 
 struct EmitOpts {
@@ -1000,9 +1021,7 @@ struct bf_s {
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
   int64_t hcalls = 0;
   std::vector<int64_t> h_rinv, h_cinv;  // bf_extract: user index -> tree position (filled on first use)
-  std::mutex xmu;                       // bf_extract: its scratch
-  void* xbuf = nullptr;
-  size_t xbuf_bytes = 0;
+  XScratch xs;                          // bf_extract's device scratch
   ~bf_s() {
     if (host_only) return;
     cudaSetDevice(device);
@@ -1029,7 +1048,6 @@ struct bf_s {
     if (pool) cudaFree(pool);
     if (d_rperm) cudaFree(d_rperm);
     if (d_cperm) cudaFree(d_cperm);
-    if (xbuf) cudaFree(xbuf);
   }
 };
 
@@ -1040,6 +1058,13 @@ struct hodbf_s {
   int LH = 0;
   void* pool = nullptr;
   int32_t m3 = 1;  // as bf_s::m3
+  // hodbf_extract: tree geometry and pool layout kept from create
+  std::vector<int64_t> lp, inv;              // leaf offsets; user index -> tree position
+  std::vector<Geom> G;                       // every off-diagonal butterfly (level-major)
+  std::vector<FBase> F;                      // their R / B / W pool offsets
+  std::vector<int64_t> M_off, SV_off, sumc;  // per leaf: [D | U^(1..LH)] and stacked Vt
+  std::vector<int64_t> ustart, vstart;       // [leaf][l]: first U column / Vt row of level l
+  XScratch xs;
   int64_t* d_perm = nullptr;
   int64_t slab_rows = 0;
   int64_t factor_entries = 0;
@@ -1677,6 +1702,28 @@ int hodbf_create(const hodbf_desc* d, int device, hodbf_handle* out) {
     }
     if (pool_len) h->pool = upload(hp, (size_t)pool_len * cs, &h->device_bytes);
     h->m3 = !selection_only(hp, pool_len, cs);
+    h->lp.assign(lp, lp + nleaf + 1);
+    h->inv.resize(d->n);
+    for (int64_t p = 0; p < d->n; ++p) h->inv[d->perm ? d->perm[p] : p] = p;
+    h->G = G;
+    h->F = F;
+    h->M_off = M_off;
+    h->SV_off = SV_off;
+    h->sumc = sumc;
+    h->ustart.assign((size_t)nleaf * (LH + 1), 0);
+    h->vstart.assign((size_t)nleaf * (LH + 1), 0);
+    for (int64_t t = 0; t < nleaf; ++t) {
+      int64_t uc = 0, vr = 0;
+      for (int l = 1; l <= LH; ++l) {
+        h->ustart[(size_t)t * (LH + 1) + l] = uc;
+        h->vstart[(size_t)t * (LH + 1) + l] = vr;
+        int64_t k, loc;
+        bf_of_row_leaf(l, t, &k, &loc);
+        uc += G[k].r(G[k].L, loc);
+        bf_of_col_leaf(l, t, &k, &loc);
+        vr += G[k].c(0, loc);
+      }
+    }
     if (d->perm) h->d_perm = (int64_t*)upload(d->perm, d->n * 8, &h->device_bytes);
     // ---- slab space: per leaf the z^0 group and the y^L group, then each bf's inner levels
     std::vector<Slabs> S(nbf);
@@ -2249,10 +2296,120 @@ int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t l
   return dist_run(h, op, nrhs, nullptr, 0, Y_loc, ldy, work, work_bytes, stream, false);
 }
 
-// K(I, J) as a partial matvec (Alg. 3 extract_BF): K E_J evaluated only on the
-// blocks a requested row and column touch, through the generic tile kernel.  The requested
-// columns enter as unit vectors (X_small: one row per position of a touched column leaf), the
-// touched row leaves' outputs land in a scratch block, and the requested rows are gathered.
+}  // extern "C"
+
+namespace bfa {
+
+// One butterfly's sub-matrix request: the requested rows / columns as tree positions of that
+// butterfly, where their U rows / Vt columns live in the pool, and where they go in `out`.
+struct XQuery {
+  std::vector<int64_t> pr, pc;      // tree positions (butterfly-local)
+  std::vector<int64_t> vtoff;       // per column: pool offset of its Vt column (c contiguous entries)
+  std::vector<int64_t> uoff, ustr;  // per row: pool offset of its U row, the row's stride
+  std::vector<int64_t> orow, ocol;  // output row / column of each request
+};
+
+static int64_t leaf_of(const std::vector<int64_t>& lp, int64_t p) {
+  return (int64_t)(std::upper_bound(lp.begin(), lp.end(), p) - lp.begin()) - 1;
+}
+
+// K(I, J) of one butterfly as a partial matvec (Alg. 3 extract_BF): K E_J evaluated
+// only on the blocks (l, tau, nu) with tau an ancestor of a requested row's leaf and nu an
+// ancestor of a requested column's leaf.  Leaf rounds: the requested Vt columns gathered into
+// zeroed z^0 slabs, the requested U rows times y^L; the inner rounds through the generic tile
+// kernel on a per-query plan.  Synchronous on `st` (the host buffers and the plan end here).
+static void extract_core(int dtype, const void* pool, int32_t m3, const Geom& G, const FBase& F, const XQuery& q,
+                         void* out, int64_t ldo, cudaStream_t st, XScratch& xs) {
+  const int L = G.L;
+  const int64_t nI = (int64_t)q.pr.size(), nJ = (int64_t)q.pc.size();
+  if (nI == 0 || nJ == 0) return;
+  const size_t cs = csize(dtype);
+  Touch T;
+  T.row.resize(L + 1);
+  T.col.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    T.row[l].assign((size_t)1 << l, 0);
+    T.col[l].assign((size_t)1 << (L - l), 0);
+  }
+  std::vector<int64_t> ti(nI), tj(nJ);
+  for (int64_t i = 0; i < nI; ++i) {
+    ti[i] = leaf_of(G.rlp, q.pr[i]);
+    for (int l = 0; l <= L; ++l) T.row[l][ti[i] >> (L - l)] = 1;
+  }
+  for (int64_t j = 0; j < nJ; ++j) {
+    tj[j] = leaf_of(G.clp, q.pc[j]);
+    for (int l = 0; l <= L; ++l) T.col[l][tj[j] >> l] = 1;
+  }
+  T.rows.resize(L + 1);
+  T.cols.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    for (size_t k = 0; k < T.row[l].size(); ++k)
+      if (T.row[l][k]) T.rows[l].push_back((int64_t)k);
+    for (size_t k = 0; k < T.col[l].size(); ++k)
+      if (T.col[l][k]) T.cols[l].push_back((int64_t)k);
+  }
+  int64_t cursor = 0;
+  Slabs S = touched_slabs(G, T, cursor);
+  PlanBuilder pb;
+  emit_N_touched(pb, G, F, S, T);
+  std::vector<int64_t> jmap(3 * nJ), imap(5 * nI);
+  for (int64_t j = 0; j < nJ; ++j) {
+    jmap[3 * j] = S.col_out(G, 0, tj[j]);
+    jmap[3 * j + 1] = G.c(0, tj[j]);
+    jmap[3 * j + 2] = q.vtoff[j];
+  }
+  for (int64_t i = 0; i < nI; ++i) {
+    imap[5 * i] = q.uoff[i];
+    imap[5 * i + 1] = q.ustr[i];
+    imap[5 * i + 2] = G.r(L, ti[i]);
+    imap[5 * i + 3] = S.row_in(G, L, ti[i]);
+    imap[5 * i + 4] = q.orow[i];
+  }
+  int64_t rows0 = 0;  // the z^0 slabs come first in the touched slab space
+  for (int64_t nu : T.cols[0]) rows0 += G.c(0, nu);
+  std::lock_guard<std::mutex> lk(xs.mu);
+  Plan P;
+  size_t pbytes = 0;
+  upload_plan(P, pb, 0, (int)pb.tasks.size(), &pbytes);
+  try {
+    // scratch: slab space | column map | row map | output columns
+    const size_t bS = align256((size_t)cursor * (size_t)nJ * cs), bJ = align256(jmap.size() * 8),
+                 bI = align256(imap.size() * 8), bC = align256(q.ocol.size() * 8);
+    char* base = static_cast<char*>(xs.get(bS + bJ + bI + bC));
+    void* dS = base;
+    int64_t* dj = reinterpret_cast<int64_t*>(base + bS);
+    int64_t* di = reinterpret_cast<int64_t*>(base + bS + bJ);
+    int64_t* dc = reinterpret_cast<int64_t*>(base + bS + bJ + bI);
+    BF_CK(cudaMemcpyAsync(dj, jmap.data(), jmap.size() * 8, cudaMemcpyHostToDevice, st));
+    BF_CK(cudaMemcpyAsync(di, imap.data(), imap.size() * 8, cudaMemcpyHostToDevice, st));
+    BF_CK(cudaMemcpyAsync(dc, q.ocol.data(), q.ocol.size() * 8, cudaMemcpyHostToDevice, st));
+    BF_CK(cudaMemsetAsync(dS, 0, (size_t)rows0 * (size_t)nJ * cs, st));
+    StageArgs a{};
+    a.pool = pool;
+    a.m3 = m3;
+    a.S = dS;
+    a.ldS = nJ;
+    a.conj_flip = 0;
+    a.nrhs = (int32_t)nJ;
+    launch_extract_vt_cols(dtype, nJ, dj, pool, dS, st);
+    run_plan(dtype, P, a, st);
+    launch_extract_u_rows(dtype, nI, nJ, di, dc, pool, dS, out, ldo, st);
+    BF_CK(cudaGetLastError());
+    BF_CK(cudaStreamSynchronize(st));
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    free_plan(P);
+    throw;
+  }
+  free_plan(P);
+}
+
+}  // namespace bfa
+
+extern "C" {
+
+// K(I, J) (bf_extract): the user indices to tree positions, the standalone pool's U / Vt
+// locations, then extract_core.
 int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
                int64_t ldo, bf_stream_t stream) {
   try {
@@ -2264,22 +2421,10 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
     require(ldo >= nI, BF_ERR_ARG, "ldo < number of rows");
     require(nJ <= (int64_t)65535 * 32, BF_ERR_ARG, "too many columns for one launch");
     const Geom& G = h->G;
-    const int L = G.L;
     for (int64_t i = 0; i < nI; ++i) require(rows[i] >= 0 && rows[i] < G.m, BF_ERR_ARG, "row index out of range");
     for (int64_t j = 0; j < nJ; ++j) require(cols[j] >= 0 && cols[j] < G.n, BF_ERR_ARG, "column index out of range");
     DeviceGuard dg(h->device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t cs = csize(h->dtype);
-    static const bool tdbg = getenv("BF_EXTRACT_TIMING") != nullptr;
-    auto t0 = std::chrono::steady_clock::now();
-    auto tick = [&](const char* what) {
-      if (!tdbg) return;
-      auto t1 = std::chrono::steady_clock::now();
-      fprintf(stderr, "bf_extract %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
-      t0 = t1;
-    };
-    // tree positions of the requested rows / columns (inverse perms, cached on the host)
-    {
+    {  // user index -> tree position, cached on the host on first use
       std::lock_guard<std::mutex> lk(h->hmu);
       if (h->h_rinv.empty()) {
         std::vector<int64_t> rp(G.m), cp(G.n);
@@ -2293,111 +2438,118 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
         for (int64_t p = 0; p < G.n; ++p) h->h_cinv[cp[p]] = p;
       }
     }
-    auto leaf_of = [](const std::vector<int64_t>& lp, int64_t p) {
-      return (int64_t)(std::upper_bound(lp.begin(), lp.end(), p) - lp.begin()) - 1;
-    };
-    Touch T;
-    T.row.resize(L + 1);
-    T.col.resize(L + 1);
-    for (int l = 0; l <= L; ++l) {
-      T.row[l].assign((size_t)1 << l, 0);
-      T.col[l].assign((size_t)1 << (L - l), 0);
-    }
-    std::vector<int64_t> pr(nI), pc(nJ);
-    for (int64_t i = 0; i < nI; ++i) {
-      pr[i] = h->h_rinv[rows[i]];
-      const int64_t tau = leaf_of(G.rlp, pr[i]);
-      for (int l = 0; l <= L; ++l) T.row[l][tau >> (L - l)] = 1;
-    }
-    for (int64_t j = 0; j < nJ; ++j) {
-      pc[j] = h->h_cinv[cols[j]];
-      const int64_t nu = leaf_of(G.clp, pc[j]);
-      for (int l = 0; l <= L; ++l) T.col[l][nu >> l] = 1;
-    }
-    T.rows.resize(L + 1);
-    T.cols.resize(L + 1);
-    for (int l = 0; l <= L; ++l) {
-      for (size_t k = 0; k < T.row[l].size(); ++k)
-        if (T.row[l][k]) T.rows[l].push_back((int64_t)k);
-      for (size_t k = 0; k < T.col[l].size(); ++k)
-        if (T.col[l][k]) T.cols[l].push_back((int64_t)k);
-    }
-    // the touched blocks' plan
     FBase F;
     F.u = 0;
     F.r = G.len_U;
     F.b = F.r + G.len_R;
     F.w = F.b + G.len_B;
     F.vt = F.w + G.len_W;
-    int64_t cursor = 0;
-    Slabs S = touched_slabs(G, T, cursor);
-    tick("touched sets + inputs");
-    PlanBuilder pb;
-    emit_N_touched(pb, G, F, S, T);
-    tick("plan");
-    Plan P;
-    size_t pbytes = 0;
-    std::lock_guard<std::mutex> lk(h->xmu);  // one extraction at a time uses the handle's scratch
-    upload_plan(P, pb, 0, (int)pb.tasks.size(), &pbytes);
-    tick("plan upload");
-    try {
-      // the leaf maps: per requested column its Vt column, per requested row its U row
-      std::vector<int64_t> jmap(3 * nJ), imap(4 * nI);
-      for (int64_t j = 0; j < nJ; ++j) {
-        const int64_t nu = leaf_of(G.clp, pc[j]);
-        const int c = G.c(0, nu);
-        jmap[3 * j] = S.col_out(G, 0, nu);
-        jmap[3 * j + 1] = c;
-        jmap[3 * j + 2] = F.vt + G.vt_off[nu] + (pc[j] - G.clp[nu]) * c;
-      }
-      for (int64_t i = 0; i < nI; ++i) {
-        const int64_t tau = leaf_of(G.rlp, pr[i]);
-        imap[4 * i] = F.u + G.u_off[tau] + (pr[i] - G.rlp[tau]);
-        imap[4 * i + 1] = G.mt(tau);
-        imap[4 * i + 2] = G.r(L, tau);
-        imap[4 * i + 3] = S.row_in(G, L, tau);
-      }
-      int64_t rows0 = 0;  // z^0 slabs come first in the touched slab space
-      for (int64_t nu : T.cols[0]) rows0 += G.c(0, nu);
-      // device scratch (grow-only, handle-owned): slab space | column map | row map
-      const size_t bS = align256((size_t)cursor * (size_t)nJ * cs), bJ = align256(jmap.size() * 8),
-                   bI = align256(imap.size() * 8);
-      const size_t need = bS + bJ + bI;
-      if (h->xbuf_bytes < need) {
-        if (h->xbuf) cudaFree(h->xbuf);
-        h->xbuf = nullptr;
-        h->xbuf_bytes = 0;
-        BF_CK(cudaMalloc(&h->xbuf, need));
-        h->xbuf_bytes = need;
-      }
-      char* base = static_cast<char*>(h->xbuf);
-      void* dS = base;
-      int64_t* dj = reinterpret_cast<int64_t*>(base + bS);
-      int64_t* di = reinterpret_cast<int64_t*>(base + bS + bJ);
-      BF_CK(cudaMemcpyAsync(dj, jmap.data(), jmap.size() * 8, cudaMemcpyHostToDevice, st));
-      BF_CK(cudaMemcpyAsync(di, imap.data(), imap.size() * 8, cudaMemcpyHostToDevice, st));
-      BF_CK(cudaMemsetAsync(dS, 0, (size_t)rows0 * (size_t)nJ * cs, st));
-      tick("scratch + copies");
-      StageArgs a{};
-      a.pool = h->pool;
-      a.m3 = h->m3;
-      a.S = dS;
-      a.ldS = nJ;
-      a.conj_flip = 0;
-      a.nrhs = (int32_t)nJ;
-      launch_extract_vt_cols(h->dtype, nJ, dj, h->pool, dS, st);
-      run_plan(h->dtype, P, a, st);
-      launch_extract_u_rows(h->dtype, nI, nJ, di, h->pool, dS, out, ldo, st);
-      BF_CK(cudaGetLastError());
-      BF_CK(cudaStreamSynchronize(st));  // the host buffers above and the plan end here
-      tick("kernels");
-    } catch (...) {
-      cudaStreamSynchronize(st);
-      free_plan(P);
-      throw;
+    XQuery q;
+    q.pr.resize(nI);
+    q.uoff.resize(nI);
+    q.ustr.resize(nI);
+    q.orow.resize(nI);
+    q.pc.resize(nJ);
+    q.vtoff.resize(nJ);
+    q.ocol.resize(nJ);
+    for (int64_t i = 0; i < nI; ++i) {
+      q.pr[i] = h->h_rinv[rows[i]];
+      const int64_t tau = leaf_of(G.rlp, q.pr[i]);
+      q.uoff[i] = F.u + G.u_off[tau] + (q.pr[i] - G.rlp[tau]);
+      q.ustr[i] = G.mt(tau);
+      q.orow[i] = i;
     }
-    free_plan(P);
-    tick("free");
+    for (int64_t j = 0; j < nJ; ++j) {
+      q.pc[j] = h->h_cinv[cols[j]];
+      const int64_t nu = leaf_of(G.clp, q.pc[j]);
+      q.vtoff[j] = F.vt + G.vt_off[nu] + (q.pc[j] - G.clp[nu]) * G.c(0, nu);
+      q.ocol[j] = j;
+    }
+    extract_core(h->dtype, h->pool, h->m3, G, F, q, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+// A(I, J) of an HOD-BF (extract_HODBF): the entries inside one leaf
+// from D_t, every other entry from the sibling butterfly of the level where the row's and the
+// column's nodes split, each butterfly's share by extract_core.
+int hodbf_extract(hodbf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
+                  int64_t ldo, bf_stream_t stream) {
+  try {
+    require(h != nullptr, BF_ERR_ARG, "NULL handle");
+    require(nI >= 0 && nJ >= 0, BF_ERR_ARG, "negative size");
+    if (nI == 0 || nJ == 0) return BF_OK;
+    require(rows != nullptr && cols != nullptr && out != nullptr, BF_ERR_ARG, "NULL argument");
+    require(ldo >= nI, BF_ERR_ARG, "ldo < number of rows");
+    require(nJ <= (int64_t)65535 * 32, BF_ERR_ARG, "too many columns for one launch");
+    for (int64_t i = 0; i < nI; ++i) require(rows[i] >= 0 && rows[i] < h->n, BF_ERR_ARG, "row index out of range");
+    for (int64_t j = 0; j < nJ; ++j) require(cols[j] >= 0 && cols[j] < h->n, BF_ERR_ARG, "column index out of range");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int LH = h->LH;
+    const std::vector<int64_t>& lp = h->lp;
+    std::vector<int64_t> pi(nI), pj(nJ), ti(nI), tj(nJ);
+    for (int64_t i = 0; i < nI; ++i) {
+      pi[i] = h->inv[rows[i]];
+      ti[i] = leaf_of(lp, pi[i]);
+    }
+    for (int64_t j = 0; j < nJ; ++j) {
+      pj[j] = h->inv[cols[j]];
+      tj[j] = leaf_of(lp, pj[j]);
+    }
+    // the dense-leaf entries
+    std::vector<int64_t> pairs;
+    for (int64_t j = 0; j < nJ; ++j)
+      for (int64_t i = 0; i < nI; ++i)
+        if (ti[i] == tj[j]) {
+          const int64_t t = ti[i], mt = lp[t + 1] - lp[t];
+          pairs.push_back(i + j * ldo);
+          pairs.push_back(h->M_off[t] + (pi[i] - lp[t]) + (pj[j] - lp[t]) * mt);
+        }
+    if (!pairs.empty()) {
+      std::lock_guard<std::mutex> lk(h->xs.mu);
+      int64_t* dp = static_cast<int64_t*>(h->xs.get(pairs.size() * 8));
+      BF_CK(cudaMemcpyAsync(dp, pairs.data(), pairs.size() * 8, cudaMemcpyHostToDevice, st));
+      launch_extract_gather(h->dtype, (int64_t)pairs.size() / 2, dp, h->pool, out, st);
+      BF_CK(cudaGetLastError());
+      BF_CK(cudaStreamSynchronize(st));
+    }
+    // every sibling butterfly a requested row and column meet in: B_a = A(T_a, T_{a^1}) at level l
+    for (int l = 1; l <= LH; ++l) {
+      const int sh = LH - l;
+      const int64_t w = int64_t(1) << sh;
+      std::map<int64_t, std::vector<int64_t>> rows_of, cols_of;  // node a -> requests under it
+      for (int64_t i = 0; i < nI; ++i) rows_of[ti[i] >> sh].push_back(i);
+      for (int64_t j = 0; j < nJ; ++j) cols_of[tj[j] >> sh].push_back(j);
+      for (auto& ra : rows_of) {
+        const int64_t a = ra.first, b = a ^ 1;
+        auto cb = cols_of.find(b);
+        if (cb == cols_of.end()) continue;
+        // only pairs whose nodes split at level l: their level l-1 ancestors agree (a, b siblings)
+        const int64_t k = (int64_t(1) << l) - 2 + a;
+        const Geom& G = h->G[k];
+        const int64_t r0 = lp[a * w], c0 = lp[b * w];
+        XQuery q;
+        for (int64_t i : ra.second) {
+          const int64_t p = pi[i] - r0, t = ti[i], tau = t - a * w, mt = lp[t + 1] - lp[t];
+          q.pr.push_back(p);
+          q.uoff.push_back(h->M_off[t] + mt * (mt + h->ustart[(size_t)t * (LH + 1) + l]) + (pi[i] - lp[t]));
+          q.ustr.push_back(mt);
+          q.orow.push_back(i);
+          (void)tau;
+        }
+        for (int64_t j : cb->second) {
+          const int64_t p = pj[j] - c0, t = tj[j], nu = t - b * w;
+          q.pc.push_back(p);
+          q.vtoff.push_back(h->SV_off[t] + (pj[j] - lp[t]) * h->sumc[t] + h->vstart[(size_t)t * (LH + 1) + l]);
+          q.ocol.push_back(j);
+          (void)nu;
+        }
+        extract_core(h->dtype, h->pool, h->m3, G, h->F[k], q, out, ldo, st, h->xs);
+      }
+    }
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);

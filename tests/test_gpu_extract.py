@@ -65,3 +65,24 @@ def test_extract_errors():
     with pytest.raises(pkg.BFError):
         h.extract([0], [-1])
     assert h.extract([], [1, 2]).shape == (0, 2)
+
+
+# ------------------------------------------------------------------ extract_HODBF
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_hodbf_extract(dtype):
+    """hodbf_extract: dense-leaf entries plus, for every other entry, the sibling
+    butterfly of the level where its row's and column's nodes split."""
+    from bfinputs.configs import helmholtz_plane_hodbf
+    H = helmholtz_plane_hodbf(32, 16, 10.0, 1e-4).astype(dtype)
+    h = pkg.HODBFHandle(H)
+    rng = np.random.default_rng(2)
+    t = H.perm[int(H.leaf_ptr[5]):int(H.leaf_ptr[6])]  # the user indices of one leaf
+    cases = [
+        (rng.integers(0, H.n, 57), rng.integers(0, H.n, 33)),   # scattered, every level, repeats
+        (t, t),                                                  # one dense leaf block
+        (t, H.perm[int(H.leaf_ptr[40]):int(H.leaf_ptr[44])]),   # a far off-diagonal block
+        ([3], [H.n - 1]),
+    ]
+    for I, J in cases:
+        got = h.extract(I, J).cpu().numpy()
+        assert oracle.rel_err(got, oracle.hodbf_extract(H, I, J)) <= TOL[dtype], (len(I), len(J))

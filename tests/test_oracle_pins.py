@@ -249,6 +249,21 @@ def test_P8_hodbf_two_by_two_block_matrix():
         assert oracle.rel_err(oracle.hodbf_apply(H, X, op), oracle.apply_op(Ad, X, op)) < 1e-15
 
 
+def test_hodbf_extract_two_by_two_block_matrix():
+    """extract_HODBF of the L_H = 1 HOD-BF whose blocks are an arbitrary 2x2 block matrix (P8):
+    exactly the entries of that matrix, under a permutation, repeats included."""
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((9, 9)) + 1j * rng.standard_normal((9, 9))
+    lp = np.array([0, 4, 9])
+    perm = rng.permutation(9)
+    D = Stage.from_blocks([A[:4, :4], A[4:, 4:]], np.complex128)
+    H = HODBF(9, 1, lp, perm, D, [[_lowrank_bf_L0(A[:4, 4:]), _lowrank_bf_L0(A[4:, :4])]])
+    Ad = np.zeros_like(A)
+    Ad[np.ix_(perm, perm)] = A
+    I, J = rng.integers(0, 9, 7), rng.integers(0, 9, 5)
+    np.testing.assert_array_equal(oracle.hodbf_extract(H, I, J), Ad[np.ix_(I, J)])
+
+
 def test_P8_hodbf_zero_offdiag_is_blockdiag():
     rng = np.random.default_rng(1)
     LH, leaf = 3, 3

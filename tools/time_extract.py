@@ -1,6 +1,7 @@
-"""bf_extract (extract_BF as a partial matvec) on the config-5 butterfly: wall time
-per call (synchronous: host planning of the touched blocks + uploads + kernels) for typical
-sub-block shapes, next to the full apply.   python tools/time_extract.py [c128|c64]"""
+"""bf_extract (extract_BF as a partial matvec) on the config-5 butterfly and
+hodbf_extract on the config-3 HOD-BF: wall time per call (synchronous: host planning of
+the touched blocks + uploads + kernels) for typical sub-block shapes, next to the full apply.
+    python tools/time_extract.py [c128|c64]"""
 import json
 import os
 import sys
@@ -33,6 +34,25 @@ def main():
         for _ in range(5):
             t0 = time.perf_counter()
             h.extract(I, J)
+            t.append(time.perf_counter() - t0)
+        res[name] = {"ms": 1e3 * float(np.median(t)), "entries": len(I) * len(J)}
+        print(name, json.dumps(res[name]), flush=True)
+    # extract_HODBF on config 3 (c128): a leaf block, a 256 x 256 block of 4 x 4 leaves, scattered
+    from bfinputs.configs import cfg3
+    H, _ = cfg3(np.complex128)
+    hh = pkg.HODBFHandle(H)
+    lp = H.leaf_ptr
+    hcases = {
+        "cfg3 HOD-BF one leaf block 64x64": (H.perm[lp[7]:lp[8]], H.perm[lp[7]:lp[8]]),
+        "cfg3 HOD-BF 4 x 4 leaves off-diagonal (256 x 256)": (H.perm[lp[0]:lp[4]], H.perm[lp[200]:lp[204]]),
+        "cfg3 HOD-BF 256 x 256 scattered": (rng.integers(0, H.n, 256), rng.integers(0, H.n, 256)),
+    }
+    for name, (I, J) in hcases.items():
+        hh.extract(I, J)
+        t = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            hh.extract(I, J)
             t.append(time.perf_counter() - t0)
         res[name] = {"ms": 1e3 * float(np.median(t)), "entries": len(I) * len(J)}
         print(name, json.dumps(res[name]), flush=True)
