@@ -126,7 +126,9 @@ struct Stream {
   }
 };
 
-template <class Pol, int D>
+// HV: column halves with work (1 when nrhs <= 16, the second half of the only tile being padding;
+// a compile-time choice, so that the two-half instantiation keeps its code generation)
+template <class Pol, int D, int HV = 2>
 __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_constant__ FastArgs A) {
   using E = typename Pol::E;
   using Cfg = PassCfg<Pol, D>;
@@ -189,6 +191,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   __syncthreads();
   const int half = warp / FAST_NCONS_HALF, hw = warp % FAST_NCONS_HALF;
   if (hw >= NACTH) return;  // idle warps (d = 1)
+  // nrhs <= 16 (HV = 1): the second column half of the (only) tile is padding -- its warps skip
+  // the work, and every release count waits for the first half's warps only
+  if (half >= HV) return;
+  constexpr int nact = HV * NACTH;
 
   if (half == 1 && A.skew > 0) __nanosleep(A.skew);
   const int g = lane >> 2, t = lane & 3;
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
       // (the condition order matters to the complex128 code generation: 2 % per apply)
       if (lane == 0 && !(diag & 1) && P.in_s >= 0 && last) {
         // every warp past op q-1 -> buffer rd ^ 1 is free: the last one in loads the next window
-        if (atom_add_acqrel(wcnt, 1) == (int)(i + 1) * NACT - 1) str.issue_window(i + 1, rd ^ 1);
+        if (atom_add_acqrel(wcnt, 1) == (int)(i + 1) * nact - 1) str.issue_window(i + 1, rd ^ 1);
       }
       const E* win = winbuf + rd * WIN + half * Cfg::WINH;
 #pragma unroll
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
           __syncwarp();
           if (lane == 0 && !(diag & 1)) {
-            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * NACT - 1) str.issue_page(j + NP);
+            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
           }
           ++j;
           if (++slot == NP) {
@@ -317,7 +323,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
           __syncwarp();
           if (lane == 0 && !(diag & 1)) {
-            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * NACT - 1) str.issue_page(j + NP);
+            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
           }
           ++j;
           if (++slot == NP) {
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           // release the page; the last warp out re-arms it with page j + NP
           __syncwarp();
           if (lane == 0 && !(diag & 1)) {
-            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * NACT - 1) str.issue_page(j + NP);
+            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
           }
           ++j;
           if (++slot == NP) {
@@ -413,16 +419,22 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
 
 const char* fast_kernel_name(int dtype) { return dtype == BF_C128 ? "k_bf_pass<c128>" : "k_bf_pass<c64>"; }
 
-template <class Pol, int D>
-static void launch_one(const FastArgs& a, unsigned grid, cudaStream_t st) {
+template <class Pol, int D, int HV>
+static void launch_hv(const FastArgs& a, unsigned grid, cudaStream_t st) {
   static bool attr = false;
   const size_t smem = PassCfg<Pol, D>::smem();
   static_assert(PassCfg<Pol, D>::smem() <= 227 * 1024, "pass kernel shared memory");
   if (!attr) {
-    cudaFuncSetAttribute(k_bf_pass<Pol, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_bf_pass<Pol, D, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  launch_pdl(k_bf_pass<Pol, D>, grid, FAST_THREADS, smem, st, a);
+  launch_pdl(k_bf_pass<Pol, D, HV>, grid, FAST_THREADS, smem, st, a);
+}
+
+template <class Pol, int D>
+static void launch_one(const FastArgs& a, unsigned grid, cudaStream_t st) {
+  if (a.halves == 1) launch_hv<Pol, D, 1>(a, grid, st);
+  else launch_hv<Pol, D, 2>(a, grid, st);
 }
 
 void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {

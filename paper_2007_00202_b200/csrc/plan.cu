@@ -1365,6 +1365,7 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       a.p = P;
       a.diag = diag;
       a.skew = getenv("BF_FAST_SKEW") ? atoi(getenv("BF_FAST_SKEW")) : 0;
+      a.halves = nrhs <= FAST_HC && !getenv("BF_NO_HALF_SKIP") ? 1 : 2;
       if (peer_recv && P.xout) {  // fused peer-memory exchange
         a.p2p = 1;
         a.myrank = h->rank;

@@ -1,5 +1,5 @@
 """Plain apply loop on config 5 (no per-launch events between kernels): ms per apply, best of
-5 runs of 20 applies.   python tools/time_apply.py [c128|c64] [N|C]"""
+5 runs of 20 applies.   python tools/time_apply.py [c128|c64] [N|C] [nrhs]"""
 import os
 import sys
 
@@ -14,7 +14,8 @@ import paper_2007_00202_b200 as pkg  # noqa: E402
 def main():
     dts = sys.argv[1] if len(sys.argv) > 1 else "c128"
     op = sys.argv[2] if len(sys.argv) > 2 else "N"
-    bf, X = cfg5(np.complex128 if dts == "c128" else np.complex64)
+    nrhs = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+    bf, X = cfg5(np.complex128 if dts == "c128" else np.complex64, nrhs=nrhs)
     h = pkg.BFHandle(bf)
     Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
     Y = h.apply(Xd, op)
@@ -31,7 +32,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / 20)
-    print(f"{dts} op {op}: {best:.4f} ms/apply")
+    print(f"{dts} op {op} nrhs {nrhs}: {best:.4f} ms/apply")
 
 
 if __name__ == "__main__":
