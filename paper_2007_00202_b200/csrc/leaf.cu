@@ -27,7 +27,9 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
   using E = typename Pol::E;
   constexpr int KS = Pol::KS;
   constexpr int NT = Pol::NT;
-  static_assert(NT == 4, "a leaf warp covers the 32-column tile");
+  // NT = 4: a leaf warp covers the 32-column tile; NT = 2 (nrhs <= 16): its first half only (the
+  // second is padding: the next window pass skips it, the row leaf writes only valid columns)
+  static_assert(NT == 4 || NT == 2, "a leaf warp covers the tile or its first half");
   constexpr int KPS = FAST_RANK / KS;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -239,12 +241,23 @@ void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
   if (a.tma && a.mode == 0)
     a.tma = make_map(dtype, a.X, a.nleaf * a.leaf, a.nrhs, a.ldx, a.brows, &a.map) ? 1 : 0;
   (void)w;
+  const bool narrow = a.nrhs <= FAST_HC && !getenv("BF_NO_HALF_SKIP");  // the tile's second half is padding
   if (dtype == BF_C128) {
-    if (a.mode == 0) launch_leaf_t<PolC128<4>, 0>(a, st);
-    else launch_leaf_t<PolC128<4>, 1>(a, st);
+    if (narrow) {
+      if (a.mode == 0) launch_leaf_t<PolC128<2>, 0>(a, st);
+      else launch_leaf_t<PolC128<2>, 1>(a, st);
+    } else {
+      if (a.mode == 0) launch_leaf_t<PolC128<4>, 0>(a, st);
+      else launch_leaf_t<PolC128<4>, 1>(a, st);
+    }
   } else {
-    if (a.mode == 0) launch_leaf_t<PolC64<4>, 0>(a, st);
-    else launch_leaf_t<PolC64<4>, 1>(a, st);
+    if (narrow) {
+      if (a.mode == 0) launch_leaf_t<PolC64<2>, 0>(a, st);
+      else launch_leaf_t<PolC64<2>, 1>(a, st);
+    } else {
+      if (a.mode == 0) launch_leaf_t<PolC64<4>, 0>(a, st);
+      else launch_leaf_t<PolC64<4>, 1>(a, st);
+    }
   }
 }
 
