@@ -127,7 +127,8 @@ struct Stream {
 };
 
 // HV: column halves with work (1 when nrhs <= 16, the second half of the only tile being padding;
-// a compile-time choice, so that the two-half instantiation keeps its code generation)
+// 0 = narrow, nrhs <= 8: one half, one 8-column n-tile per warp (Pol::NT == 1), a warp per slot).
+// A compile-time choice, so that the two-half instantiation keeps its code generation.
 template <class Pol, int D, int HV = 2>
 __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_constant__ FastArgs A) {
   using E = typename Pol::E;
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   using St = Stream<Pol, D>;
   constexpr int NT = Pol::NT;
   constexpr int S = 1 << D;                          // slots of the window
-  constexpr int CT = 2 / NT;                         // column tiles per slot (in a half)
+  constexpr int CT = HV == 0 ? 1 : 2 / NT;           // column tiles per slot (in a half)
+  static_assert(HV != 0 || NT == 1, "narrow passes use one 8-column n-tile per warp");
   // slots per warp: 2 for 4-level windows (16 slots, 8 warps per half), else 1
   constexpr int SPW = S * CT > FAST_NCONS_HALF ? S * CT / FAST_NCONS_HALF : 1;
   static_assert(SPW == 1 || CT == 1, "several slots per warp need whole-slot warps");
@@ -193,8 +195,9 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   if (hw >= NACTH) return;  // idle warps (d = 1)
   // nrhs <= 16 (HV = 1): the second column half of the (only) tile is padding -- its warps skip
   // the work, and every release count waits for the first half's warps only
-  if (half >= HV) return;
-  constexpr int nact = HV * NACTH;
+  constexpr int HVN = HV == 0 ? 1 : HV;  // halves with work
+  if (half >= HVN) return;
+  constexpr int nact = HVN * NACTH;
 
   if (half == 1 && A.skew > 0) __nanosleep(A.skew);
   const int g = lane >> 2, t = lane & 3;
@@ -433,7 +436,7 @@ static void launch_hv(const FastArgs& a, unsigned grid, cudaStream_t st) {
 
 template <class Pol, int D>
 static void launch_one(const FastArgs& a, unsigned grid, cudaStream_t st) {
-  if (a.halves == 1) launch_hv<Pol, D, 1>(a, grid, st);
+  if (a.halves <= 1) launch_hv<Pol, D, 1>(a, grid, st);
   else launch_hv<Pol, D, 2>(a, grid, st);
 }
 
@@ -447,7 +450,11 @@ void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
   const int64_t items = a.p.nwin * ((a.nrhs + FAST_NB - 1) / FAST_NB);  // (window, rhs tile)
   const unsigned grid = (unsigned)(items < nsm ? items : nsm);
   const int d = a.p.d;
-  if (dtype == BF_C128) {
+  if (dtype == BF_C128 && a.halves == 0) {  // nrhs <= 8: 8 columns per warp, a warp per slot
+    if (d == 3) launch_hv<PolC128<1>, 3, 0>(a, grid, st);
+    else if (d == 2) launch_hv<PolC128<1>, 2, 0>(a, grid, st);
+    else launch_hv<PolC128<1>, 1, 0>(a, grid, st);
+  } else if (dtype == BF_C128) {
     if (d == 3) launch_one<PolC128<2>, 3>(a, grid, st);
     else if (d == 2) launch_one<PolC128<2>, 2>(a, grid, st);  // 8 warps x 16 columns: 3 % faster than 16 x 8
     else launch_one<PolC128<1>, 1>(a, grid, st);

@@ -85,7 +85,7 @@ struct FastArgs {
   int32_t nrhs;
   int32_t ntiles;  // 32-column rhs tiles (exchange layout stride)
   int32_t skew;  // ns the second column half starts late (tuning knob, env BF_FAST_SKEW)
-  int32_t halves;  // column halves with work: 1 when nrhs <= 16 (the second half is padding)
+  int32_t halves;  // column halves with work: 2; 1 when nrhs <= 16; 0 = one 8-column tile (nrhs <= 8)
   int32_t p2p;   // xout pass: write each slab straight into its receiver's recv region
   int32_t myrank;
   void* peer[FAST_MAXPEER];  // p2p: every rank's recv-region base (peer memory over NVLink)

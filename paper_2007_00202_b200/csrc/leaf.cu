@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant_
   constexpr int NT = Pol::NT;
   // NT = 4: a leaf warp covers the 32-column tile; NT = 2 (nrhs <= 16): its first half only (the
   // second is padding: the next window pass skips it, the row leaf writes only valid columns)
-  static_assert(NT == 4 || NT == 2, "a leaf warp covers the tile or its first half");
+  static_assert(NT == 4 || NT == 2 || NT == 1, "a leaf warp covers the tile, its first half or 8 columns");
   constexpr int KPS = FAST_RANK / KS;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -242,8 +242,12 @@ void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
     a.tma = make_map(dtype, a.X, a.nleaf * a.leaf, a.nrhs, a.ldx, a.brows, &a.map) ? 1 : 0;
   (void)w;
   const bool narrow = a.nrhs <= FAST_HC && !getenv("BF_NO_HALF_SKIP");  // the tile's second half is padding
+  const bool eight = narrow && a.nrhs <= 8 && !getenv("BF_NO_NARROW");   // and columns 8..15 too
   if (dtype == BF_C128) {
-    if (narrow) {
+    if (eight) {
+      if (a.mode == 0) launch_leaf_t<PolC128<1>, 0>(a, st);
+      else launch_leaf_t<PolC128<1>, 1>(a, st);
+    } else if (narrow) {
       if (a.mode == 0) launch_leaf_t<PolC128<2>, 0>(a, st);
       else launch_leaf_t<PolC128<2>, 1>(a, st);
     } else {
@@ -251,7 +255,10 @@ void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
       else launch_leaf_t<PolC128<4>, 1>(a, st);
     }
   } else {
-    if (narrow) {
+    if (eight) {
+      if (a.mode == 0) launch_leaf_t<PolC64<1>, 0>(a, st);
+      else launch_leaf_t<PolC64<1>, 1>(a, st);
+    } else if (narrow) {
       if (a.mode == 0) launch_leaf_t<PolC64<2>, 0>(a, st);
       else launch_leaf_t<PolC64<2>, 1>(a, st);
     } else {

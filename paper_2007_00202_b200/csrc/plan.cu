@@ -1365,7 +1365,8 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       a.p = P;
       a.diag = diag;
       a.skew = getenv("BF_FAST_SKEW") ? atoi(getenv("BF_FAST_SKEW")) : 0;
-      a.halves = nrhs <= FAST_HC && !getenv("BF_NO_HALF_SKIP") ? 1 : 2;
+      // column halves with work: 2; 1 when nrhs <= 16; 0 (narrow, 8 columns) when nrhs <= 8
+      a.halves = getenv("BF_NO_HALF_SKIP") ? 2 : nrhs <= 8 && !getenv("BF_NO_NARROW") ? 0 : nrhs <= FAST_HC ? 1 : 2;
       if (peer_recv && P.xout) {  // fused peer-memory exchange
         a.p2p = 1;
         a.myrank = h->rank;
