@@ -151,6 +151,12 @@ PIPE = {"c128": ("dmma_sync_tflops", 6, "FP64 tensor pipe (mma.sync.m8n8k4.f64);
                                         "= 6 flops per complex MAC"),
         "c64": ("tf32_mma_sync_tflops", 18, "TF32 tensor pipe (mma.sync.m16n8k8.tf32); 3M x 3xTF32 split = 9 real "
                                           "MACs = 18 flops per complex MAC")}
+# The peak a contraction is measured against (task rule: its own dtype's peak = another dtype's
+# measured peak x the guide's nominal ratio).  TF32: MEASURED_PEAKS bf16 x (1.1 / 2.25 PF, the
+# guide's dense tf32 / bf16 nominals) -- the tcgen05-class TF32 rate of the chip, not the
+# mma.sync rate the kernel can reach (kept beside it).  FP64: the guide states no FP64 figure,
+# so the DMMA peak measured on this pool (tools/peaks.cu) stands.
+TF32_OVER_BF16 = 1.1 / 2.25
 
 
 def dominant_roofline(dtype, name, rounds, mean, nrhs, cs, peaks):
@@ -164,12 +170,19 @@ def dominant_roofline(dtype, name, rounds, mean, nrhs, cs, peaks):
     tiles = (nrhs + 31) // 32
     key, fpc, note = PIPE[dtype]
     fl = sum(rounds[i]["factor_entries"] for i in idx) / len(idx) * tiles * 32 * fpc
-    pipe_peak = ((peaks.get("pipes") or {}).get(key) or 0.0) * 1e12
+    sync_peak = ((peaks.get("pipes") or {}).get(key) or 0.0) * 1e12   # mma.sync rate measured on this pool
+    if dtype == "c64" and peaks.get("bf16_tflops"):
+        pipe_peak = peaks["bf16_tflops"] * TF32_OVER_BF16 * 1e12
+        src = "MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (B200_PROFILING.md tf32 / bf16 dense nominals)"
+    else:
+        pipe_peak = sync_peak
+        src = "profiles/pipe_peaks.json (" + key + "; the guide states no FP64 figure)"
     hbm = {"achieved": b / t / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": b / t / 1e9 / peaks["hbm_gbs"],
            "peak_source": peaks.get("source")}
     ten = {"achieved": fl / t / 1e12, "peak": pipe_peak / 1e12, "unit": "TFLOP/s",
-           "frac": (fl / t / pipe_peak) if pipe_peak else None, "peak_source": "profiles/pipe_peaks.json (" + key + ")",
-           "work": note}
+           "frac": (fl / t / pipe_peak) if pipe_peak else None, "peak_source": src, "work": note,
+           "mma_sync_peak": sync_peak / 1e12,
+           "frac_of_mma_sync_peak": (fl / t / sync_peak) if sync_peak else None}
     t_hbm = b / (peaks["hbm_gbs"] * 1e9)
     t_pipe = fl / pipe_peak if pipe_peak else 0.0
     main, other, bound = (ten, hbm, "tensor") if t_pipe > t_hbm else (hbm, ten, "hbm")
