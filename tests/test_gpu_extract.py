@@ -86,3 +86,13 @@ def test_hodbf_extract(dtype):
     for I, J in cases:
         got = h.extract(I, J).cpu().numpy()
         assert oracle.rel_err(got, oracle.hodbf_extract(H, I, J)) <= TOL[dtype], (len(I), len(J))
+
+
+@pytest.mark.parametrize("L,lc", [(0, 0), (5, 0), (5, 5), (4, 1)])
+def test_extract_centre_edge_cases(L, lc):
+    """lc at 0 or L (no W or no R stages), and L = 0 (K = U B Vt: one dense block)."""
+    bf = random_butterfly(L=L, leaf=16, r=8, seed=3 + L + lc, lc=lc)
+    h = pkg.BFHandle(bf)
+    rng = np.random.default_rng(L + lc)
+    I, J = rng.integers(0, bf.m, 23), rng.integers(0, bf.n, 17)
+    assert oracle.rel_err(_get(h, I, J), oracle.bf_extract(bf, I, J)) <= 1e-12
