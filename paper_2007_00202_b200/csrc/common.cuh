@@ -52,6 +52,8 @@ struct Round {
   int32_t max_k;
   int32_t fast;        // specialised kernel id (0 = generic)
   int32_t pad;
+  const int2* cols;    // device, optional (bf_extract): per task the rhs-column range [x, y) it must
+                       // produce -- column tiles outside it are skipped (they stay zero)
   // algorithmic accounting (host only)
   int64_t factor_entries, user_in, user_out, slab_in, slab_out;
 };
@@ -74,6 +76,7 @@ struct StageArgs {
   int32_t conj_flip;
   int32_t nrhs;
   int32_t m3;  // 3M complex products (0: 4M, exact on selection factors)
+  const int2* cols;  // Round::cols of the launched round (nullptr: every column tile)
 };
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);

@@ -98,6 +98,10 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   const Task tk = a.tasks[un.x];
   const int r0 = un.y * TR;
   const int j0 = blockIdx.y * TC;
+  if (a.cols) {  // bf_extract: only the column tiles the task's output has nonzeros in
+    const int2 cr = a.cols[un.x];
+    if (j0 >= cr.y || j0 + TC <= cr.x) return;
+  }
   const int g = lane >> 2, t = lane & 3;
   const int wr = 16 * (w & 1), wc = 16 * (w >> 1);  // warp tile origin inside the CTA tile
   const E* __restrict__ pool = static_cast<const E*>(a.pool);
@@ -222,6 +226,7 @@ static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
   a.units = r.units;
   a.nunits = r.nunits;
   a.out_kind = r.out_kind;
+  a.cols = r.cols;
   dim3 grid(r.nunits, (a.nrhs + 63) / 64);  // CTA tile: 32 rows x 64 columns
   if (sizeof(V) == 16)
     launch_tile<PolC128<2>>(grid, a, st);

@@ -219,13 +219,18 @@ struct PlanBuilder {
   std::vector<std::vector<Task>> tasks;
   std::vector<std::vector<Term>> terms;
   std::vector<int> okind;
-  void add(int round, int out_kind, int64_t out_row, int64_t m, const Term* t, int nt) {
+  bool use_cols = false;                   // bf_extract: per-task column ranges
+  std::vector<std::vector<int2>> cols;
+  void add(int round, int out_kind, int64_t out_row, int64_t m, const Term* t, int nt,
+           int2 colr = make_int2(0, 0)) {
     if (m <= 0) return;
     if ((int)tasks.size() <= round) {
       tasks.resize(round + 1);
       terms.resize(round + 1);
       okind.resize(round + 1, -1);
+      cols.resize(round + 1);
     }
+    if (use_cols) cols[round].push_back(colr);
     require(okind[round] == -1 || okind[round] == out_kind, BF_ERR_ARG, "internal: mixed out kinds");
     okind[round] = out_kind;
     Task tk{};
@@ -261,6 +266,7 @@ struct Touch {
   std::vector<std::vector<uint8_t>> row;  // [l][tau], l = 0..L
   std::vector<std::vector<uint8_t>> col;  // [l][nu],  nu at T_S level L - l
   std::vector<std::vector<int64_t>> rows, cols;  // the same as ascending lists
+  std::vector<std::vector<int2>> crange;         // [l][nu]: requested columns (tree-sorted) under nu
   bool r(int l, int64_t tau) const { return row[l][tau] != 0; }
   bool c(int l, int64_t nu) const { return col[l][nu] != 0; }
 };
@@ -352,6 +358,8 @@ static void emit_N(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
 // (Vt columns of the requested columns, U rows of the requested rows)
 static void emit_N_touched(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& S, const Touch& T) {
   const int L = G.L, lc = G.lc;
+  // the (tree-sorted) requested columns under nu at T_S level L - l: T.crange[l][nu]
+  auto cr = [&](int l, int64_t nu) { return T.crange.empty() ? make_int2(0, 0) : T.crange[l][nu]; };
   for (int l = 1; l <= lc; ++l)
     for (int64_t tau : T.rows[l])
       for (int64_t nu : T.cols[l]) {
@@ -362,14 +370,14 @@ static void emit_N_touched(PlanBuilder& pb, const Geom& G, const FBase& F, const
                      mk(F.w + G.w_off[l][i] + int64_t(c1) * c, 1, c, c2, S.col_in(G, l - 1, i2), 0, 0)};
         if (!T.c(l - 1, 2 * nu)) t[0].k = 0;
         if (!T.c(l - 1, 2 * nu + 1)) t[1].k = 0;
-        pb.add(l, 0, S.col_out(G, l, i), c, t, 2);
+        pb.add(l, 0, S.col_out(G, l, i), c, t, 2, cr(l, nu));
       }
   for (int64_t tau : T.rows[lc])
     for (int64_t nu : T.cols[lc]) {
       const int64_t i = G.idx(lc, tau, nu);
       const int r = G.r(lc, i), c = G.c(lc, i);
       Term t = mk(F.b + G.b_off[i], 1, r, c, S.col_in(G, lc, i), 0, 0);
-      pb.add(lc + 1, 0, S.row_out(G, lc, i), r, &t, 1);
+      pb.add(lc + 1, 0, S.row_out(G, lc, i), r, &t, 1, cr(lc, nu));
     }
   for (int l = lc; l < L; ++l)
     for (int64_t tp : T.rows[l + 1])
@@ -384,7 +392,7 @@ static void emit_N_touched(PlanBuilder& pb, const Geom& G, const FBase& F, const
           if (!T.c(l, 2 * np + s)) t[s].k = 0;
         }
         const int64_t io = G.idx(l + 1, tp, np);
-        pb.add(lc + 2 + (l - lc), 0, S.row_out(G, l + 1, io), G.r(l + 1, io), t, 2);
+        pb.add(lc + 2 + (l - lc), 0, S.row_out(G, l + 1, io), G.r(l + 1, io), t, 2, cr(l + 1, np));
       }
 }
 
@@ -868,7 +876,7 @@ struct Plan {
 
 static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, size_t* bytes) {
   size_t tot = 0;
-  std::vector<size_t> toff, xoff, uoff;
+  std::vector<size_t> toff, xoff, uoff, coff;
   std::vector<std::vector<int2>> units;
   for (int r = round_lo; r < round_hi && r < (int)pb.tasks.size(); ++r) {
     toff.push_back(tot);
@@ -885,6 +893,11 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
     tot += u.size() * sizeof(int2);
     tot = (tot + 255) & ~size_t(255);
     units.push_back(std::move(u));
+    coff.push_back(tot);
+    if (pb.use_cols) {
+      tot += pb.cols[r].size() * sizeof(int2);
+      tot = (tot + 255) & ~size_t(255);
+    }
   }
   if (tot == 0) return;
   std::vector<char> host(tot);
@@ -893,6 +906,8 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
     if (!pb.tasks[r].empty()) memcpy(host.data() + toff[q], pb.tasks[r].data(), pb.tasks[r].size() * sizeof(Task));
     if (!pb.terms[r].empty()) memcpy(host.data() + xoff[q], pb.terms[r].data(), pb.terms[r].size() * sizeof(Term));
     if (!units[q].empty()) memcpy(host.data() + uoff[q], units[q].data(), units[q].size() * sizeof(int2));
+    if (pb.use_cols && !pb.cols[r].empty())
+      memcpy(host.data() + coff[q], pb.cols[r].data(), pb.cols[r].size() * sizeof(int2));
   }
   if (tot) {
     BF_CK(cudaMalloc(&P.dev, tot));
@@ -904,6 +919,7 @@ static void upload_plan(Plan& P, PlanBuilder& pb, int round_lo, int round_hi, si
     R.tasks = reinterpret_cast<const Task*>((char*)P.dev + toff[q]);
     R.terms = reinterpret_cast<const Term*>((char*)P.dev + xoff[q]);
     R.units = reinterpret_cast<const int2*>((char*)P.dev + uoff[q]);
+    R.cols = pb.use_cols ? reinterpret_cast<const int2*>((char*)P.dev + coff[q]) : nullptr;
     R.nunits = (int32_t)units[q].size();
     R.ntasks = (int32_t)pb.tasks[r].size();
     R.out_kind = pb.okind[r] < 0 ? 0 : pb.okind[r];
@@ -2320,11 +2336,24 @@ static int64_t leaf_of(const std::vector<int64_t>& lp, int64_t p) {
 // ancestor of a requested column's leaf.  Leaf rounds: the requested Vt columns gathered into
 // zeroed z^0 slabs, the requested U rows times y^L; the inner rounds through the generic tile
 // kernel on a per-query plan.  Synchronous on `st` (the host buffers and the plan end here).
-static void extract_core(int dtype, const void* pool, int32_t m3, const Geom& G, const FBase& F, const XQuery& q,
+static void extract_core(int dtype, const void* pool, int32_t m3, const Geom& G, const FBase& F, const XQuery& q0,
                          void* out, int64_t ldo, cudaStream_t st, XScratch& xs) {
   const int L = G.L;
-  const int64_t nI = (int64_t)q.pr.size(), nJ = (int64_t)q.pc.size();
+  const int64_t nI = (int64_t)q0.pr.size(), nJ = (int64_t)q0.pc.size();
   if (nI == 0 || nJ == 0) return;
+  // the columns in tree order, so that the ones under any T_S node are a contiguous range
+  // (every block then computes only the column tiles of its own range)
+  XQuery q = q0;
+  {
+    std::vector<int64_t> ord(nJ);
+    for (int64_t j = 0; j < nJ; ++j) ord[j] = j;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return q0.pc[x] < q0.pc[y]; });
+    for (int64_t j = 0; j < nJ; ++j) {
+      q.pc[j] = q0.pc[ord[j]];
+      q.vtoff[j] = q0.vtoff[ord[j]];
+      q.ocol[j] = q0.ocol[ord[j]];
+    }
+  }
   const size_t cs = csize(dtype);
   Touch T;
   T.row.resize(L + 1);
@@ -2344,15 +2373,23 @@ static void extract_core(int dtype, const void* pool, int32_t m3, const Geom& G,
   }
   T.rows.resize(L + 1);
   T.cols.resize(L + 1);
+  T.crange.resize(L + 1);
   for (int l = 0; l <= L; ++l) {
     for (size_t k = 0; k < T.row[l].size(); ++k)
       if (T.row[l][k]) T.rows[l].push_back((int64_t)k);
     for (size_t k = 0; k < T.col[l].size(); ++k)
       if (T.col[l][k]) T.cols[l].push_back((int64_t)k);
+    T.crange[l].assign(T.col[l].size(), make_int2(0, 0));
+    for (int64_t j = 0; j < nJ; ++j) {  // tj ascending (sorted columns): each node's range is contiguous
+      int2& r = T.crange[l][tj[j] >> l];
+      if (r.y == 0) r.x = (int)j;
+      r.y = (int)j + 1;
+    }
   }
   int64_t cursor = 0;
   Slabs S = touched_slabs(G, T, cursor);
   PlanBuilder pb;
+  pb.use_cols = true;
   emit_N_touched(pb, G, F, S, T);
   std::vector<int64_t> jmap(3 * nJ), imap(5 * nI);
   for (int64_t j = 0; j < nJ; ++j) {
@@ -2367,8 +2404,7 @@ static void extract_core(int dtype, const void* pool, int32_t m3, const Geom& G,
     imap[5 * i + 3] = S.row_in(G, L, ti[i]);
     imap[5 * i + 4] = q.orow[i];
   }
-  int64_t rows0 = 0;  // the z^0 slabs come first in the touched slab space
-  for (int64_t nu : T.cols[0]) rows0 += G.c(0, nu);
+  const int64_t rows0 = cursor;  // every slab starts at zero: skipped column tiles stay zero
   std::lock_guard<std::mutex> lk(xs.mu);
   Plan P;
   size_t pbytes = 0;
