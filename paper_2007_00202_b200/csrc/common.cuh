@@ -82,9 +82,10 @@ struct StageArgs {
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);
 void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,
                        cudaStream_t st);
-void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const void* pool, void* S, cudaStream_t st);
-void launch_extract_u_rows(int dtype, int64_t nI, int64_t nJ, const int64_t* imap, const int64_t* ocol,
-                           const void* pool, const void* S, void* out, int64_t ldo, cudaStream_t st);
+void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const void* pool, void* S, int64_t ldS,
+                            cudaStream_t st);
+void launch_extract_u_rows(int dtype, int64_t nE, const int64_t* imap, const int64_t* ocol, const void* pool,
+                           const void* S, int64_t ldS, void* out, int64_t ldo, cudaStream_t st);
 void launch_extract_gather(int dtype, int64_t n, const int64_t* pairs, const void* pool, void* out, cudaStream_t st);
 
 // Launch with programmatic stream serialization (PDL, see mma.cuh pdl_wait) unless env BF_NO_PDL

@@ -271,39 +271,40 @@ void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int
 }
 
 // bf_extract, first round (the column leaves on unit vectors, Eq. 3.3's V^0 applied to E_J):
-// z^0 slab column j of leaf nu(j) = Vt_nu(:, local column of j).  jmap[j] = {slab row of the
-// leaf's z^0, rank c, pool offset of that Vt column}; the slabs were zeroed before.
+// z^0 slab column of request j = the Vt column of that request.  jmap[j] = {slab row of the
+// leaf's z^0, rank c, pool offset of the Vt column, slab column}; the slabs were zeroed before.
 template <typename V>
 __global__ void k_extract_vt_cols(int64_t nJ, const int64_t* __restrict__ jmap, const V* __restrict__ pool,
-                                  V* __restrict__ S) {
+                                  V* __restrict__ S, int64_t ldS) {
   for (int64_t j = blockIdx.x; j < nJ; j += gridDim.x) {
-    const int64_t row0 = jmap[3 * j], c = jmap[3 * j + 1], off = jmap[3 * j + 2];
-    for (int64_t r = threadIdx.x; r < c; r += blockDim.x) S[(row0 + r) * nJ + j] = pool[off + r];
+    const int64_t row0 = jmap[4 * j], c = jmap[4 * j + 1], off = jmap[4 * j + 2], col = jmap[4 * j + 3];
+    for (int64_t r = threadIdx.x; r < c; r += blockDim.x) S[(row0 + r) * ldS + col] = pool[off + r];
   }
 }
 
-// bf_extract, last round (Eq. 3.3's U^L restricted to the requested rows): out(orow_i, ocol_j) =
-// U_tau(row i, :) y^L_tau(:, j) (1 x r times r x nJ, slab rows nJ wide).  imap[i] = {pool offset
-// of U_tau's row, its stride (m_tau), rank r, slab row of y^L_tau, output row}; ocol[j] = output
-// column.
+// bf_extract, last round (Eq. 3.3's U^L restricted to the requested rows): for request-row entry
+// e = {pool offset of the U row, its stride, rank r, slab row of y^L, output row, first slab
+// column, column count}: out(orow, ocol[c]) = U(row, :) y^L(:, c) for its slab columns c.
 template <typename V>
-__global__ void k_extract_u_rows(int64_t nI, int64_t nJ, const int64_t* __restrict__ imap,
-                                 const int64_t* __restrict__ ocol, const V* __restrict__ pool,
-                                 const V* __restrict__ S, V* __restrict__ out, int64_t ldo) {
-  const int64_t total = nI * nJ;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q % nI, j = q / nI;
-    const int64_t off = imap[5 * i], mt = imap[5 * i + 1], r = imap[5 * i + 2], row0 = imap[5 * i + 3];
-    decltype(V::x) re = 0, im = 0;
-    for (int64_t k = 0; k < r; ++k) {
-      const V u = pool[off + k * mt], y = S[(row0 + k) * nJ + j];
-      re += u.x * y.x - u.y * y.y;
-      im += u.x * y.y + u.y * y.x;
+__global__ void k_extract_u_rows(int64_t nE, const int64_t* __restrict__ imap, const int64_t* __restrict__ ocol,
+                                 const V* __restrict__ pool, const V* __restrict__ S, int64_t ldS,
+                                 V* __restrict__ out, int64_t ldo) {
+  for (int64_t e = blockIdx.x; e < nE; e += gridDim.x) {
+    const int64_t* m = imap + 7 * e;
+    const int64_t off = m[0], mt = m[1], r = m[2], row0 = m[3], orow = m[4], c0 = m[5], nc = m[6];
+    for (int64_t jj = threadIdx.x; jj < nc; jj += blockDim.x) {
+      const int64_t c = c0 + jj;
+      decltype(V::x) re = 0, im = 0;
+      for (int64_t k = 0; k < r; ++k) {
+        const V u = pool[off + k * mt], y = S[(row0 + k) * ldS + c];
+        re += u.x * y.x - u.y * y.y;
+        im += u.x * y.y + u.y * y.x;
+      }
+      V o;
+      o.x = re;
+      o.y = im;
+      out[orow + ocol[c] * ldo] = o;
     }
-    V o;
-    o.x = re;
-    o.y = im;
-    out[imap[5 * i + 4] + ocol[j] * ldo] = o;
   }
 }
 
@@ -315,6 +316,31 @@ __global__ void k_extract_gather(int64_t n, const int64_t* __restrict__ pairs, c
     out[pairs[2 * q]] = pool[pairs[2 * q + 1]];
 }
 
+
+void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const void* pool, void* S, int64_t ldS,
+                            cudaStream_t st) {
+  if (nJ == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(nJ, 65535);
+  if (dtype == BF_C128)
+    k_extract_vt_cols<double2><<<grid, 64, 0, st>>>(nJ, jmap, static_cast<const double2*>(pool),
+                                                    static_cast<double2*>(S), ldS);
+  else
+    k_extract_vt_cols<float2><<<grid, 64, 0, st>>>(nJ, jmap, static_cast<const float2*>(pool),
+                                                   static_cast<float2*>(S), ldS);
+}
+
+void launch_extract_u_rows(int dtype, int64_t nE, const int64_t* imap, const int64_t* ocol, const void* pool,
+                           const void* S, int64_t ldS, void* out, int64_t ldo, cudaStream_t st) {
+  if (nE == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(nE, 65535);
+  if (dtype == BF_C128)
+    k_extract_u_rows<double2><<<grid, 128, 0, st>>>(nE, imap, ocol, static_cast<const double2*>(pool),
+                                                    static_cast<const double2*>(S), ldS, static_cast<double2*>(out), ldo);
+  else
+    k_extract_u_rows<float2><<<grid, 128, 0, st>>>(nE, imap, ocol, static_cast<const float2*>(pool),
+                                                   static_cast<const float2*>(S), ldS, static_cast<float2*>(out), ldo);
+}
+
 void launch_extract_gather(int dtype, int64_t n, const int64_t* pairs, const void* pool, void* out, cudaStream_t st) {
   if (n == 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
@@ -322,28 +348,6 @@ void launch_extract_gather(int dtype, int64_t n, const int64_t* pairs, const voi
     k_extract_gather<double2><<<grid, 256, 0, st>>>(n, pairs, static_cast<const double2*>(pool), static_cast<double2*>(out));
   else
     k_extract_gather<float2><<<grid, 256, 0, st>>>(n, pairs, static_cast<const float2*>(pool), static_cast<float2*>(out));
-}
-
-void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const void* pool, void* S, cudaStream_t st) {
-  if (nJ == 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(nJ, 65535);
-  if (dtype == BF_C128)
-    k_extract_vt_cols<double2><<<grid, 64, 0, st>>>(nJ, jmap, static_cast<const double2*>(pool), static_cast<double2*>(S));
-  else
-    k_extract_vt_cols<float2><<<grid, 64, 0, st>>>(nJ, jmap, static_cast<const float2*>(pool), static_cast<float2*>(S));
-}
-
-void launch_extract_u_rows(int dtype, int64_t nI, int64_t nJ, const int64_t* imap, const int64_t* ocol,
-                           const void* pool, const void* S, void* out, int64_t ldo, cudaStream_t st) {
-  const int64_t total = nI * nJ;
-  if (total == 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 4096);
-  if (dtype == BF_C128)
-    k_extract_u_rows<double2><<<grid, 256, 0, st>>>(nI, nJ, imap, ocol, static_cast<const double2*>(pool),
-                                                    static_cast<const double2*>(S), static_cast<double2*>(out), ldo);
-  else
-    k_extract_u_rows<float2><<<grid, 256, 0, st>>>(nI, nJ, imap, ocol, static_cast<const float2*>(pool),
-                                                   static_cast<const float2*>(S), static_cast<float2*>(out), ldo);
 }
 
 const char* round_kernel_name(int dtype, const Round& r, int* id) {

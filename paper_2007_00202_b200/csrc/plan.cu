@@ -2331,88 +2331,109 @@ static int64_t leaf_of(const std::vector<int64_t>& lp, int64_t p) {
   return (int64_t)(std::upper_bound(lp.begin(), lp.end(), p) - lp.begin()) - 1;
 }
 
-// K(I, J) of one butterfly as a partial matvec (Alg. 3 extract_BF): K E_J evaluated
-// only on the blocks (l, tau, nu) with tau an ancestor of a requested row's leaf and nu an
-// ancestor of a requested column's leaf.  Leaf rounds: the requested Vt columns gathered into
-// zeroed z^0 slabs, the requested U rows times y^L; the inner rounds through the generic tile
-// kernel on a per-query plan.  Synchronous on `st` (the host buffers and the plan end here).
-static void extract_core(int dtype, const void* pool, int32_t m3, const Geom& G, const FBase& F, const XQuery& q0,
-                         void* out, int64_t ldo, cudaStream_t st, XScratch& xs) {
-  const int L = G.L;
-  const int64_t nI = (int64_t)q0.pr.size(), nJ = (int64_t)q0.pc.size();
-  if (nI == 0 || nJ == 0) return;
-  // the columns in tree order, so that the ones under any T_S node are a contiguous range
-  // (every block then computes only the column tiles of its own range)
-  XQuery q = q0;
-  {
-    std::vector<int64_t> ord(nJ);
-    for (int64_t j = 0; j < nJ; ++j) ord[j] = j;
-    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return q0.pc[x] < q0.pc[y]; });
-    for (int64_t j = 0; j < nJ; ++j) {
-      q.pc[j] = q0.pc[ord[j]];
-      q.vtoff[j] = q0.vtoff[ord[j]];
-      q.ocol[j] = q0.ocol[ord[j]];
-    }
-  }
+// One butterfly's share of an extraction (its geometry in the pool, its requests).
+struct XPart {
+  const Geom* G;
+  FBase F;
+  XQuery q;
+};
+
+// Sub-matrices of one or more butterflies stored in `pool`, as partial matvecs (Alg. 3
+// extract_BF), in ONE plan: every part's K E_J evaluated only on the blocks
+// (l, tau, nu) with tau an ancestor of a requested row's leaf and nu an ancestor of a requested
+// column's leaf.  Each part's columns are put in tree order (the ones under any T_S node are then
+// a contiguous range, which every task carries: the tile kernel skips the other column tiles)
+// and get their own block of slab columns.  Leaf rounds: the requested Vt columns gathered into
+// the zeroed z^0 slabs, the requested U rows times y^L; the inner rounds (stage s of every part
+// in round s: the parts never interact) through the generic tile kernel.  Synchronous on `st`.
+static void extract_multi(int dtype, const void* pool, int32_t m3, std::vector<XPart>& parts, void* out, int64_t ldo,
+                          cudaStream_t st, XScratch& xs) {
   const size_t cs = csize(dtype);
-  Touch T;
-  T.row.resize(L + 1);
-  T.col.resize(L + 1);
-  for (int l = 0; l <= L; ++l) {
-    T.row[l].assign((size_t)1 << l, 0);
-    T.col[l].assign((size_t)1 << (L - l), 0);
-  }
-  std::vector<int64_t> ti(nI), tj(nJ);
-  for (int64_t i = 0; i < nI; ++i) {
-    ti[i] = leaf_of(G.rlp, q.pr[i]);
-    for (int l = 0; l <= L; ++l) T.row[l][ti[i] >> (L - l)] = 1;
-  }
-  for (int64_t j = 0; j < nJ; ++j) {
-    tj[j] = leaf_of(G.clp, q.pc[j]);
-    for (int l = 0; l <= L; ++l) T.col[l][tj[j] >> l] = 1;
-  }
-  T.rows.resize(L + 1);
-  T.cols.resize(L + 1);
-  T.crange.resize(L + 1);
-  for (int l = 0; l <= L; ++l) {
-    for (size_t k = 0; k < T.row[l].size(); ++k)
-      if (T.row[l][k]) T.rows[l].push_back((int64_t)k);
-    for (size_t k = 0; k < T.col[l].size(); ++k)
-      if (T.col[l][k]) T.cols[l].push_back((int64_t)k);
-    T.crange[l].assign(T.col[l].size(), make_int2(0, 0));
-    for (int64_t j = 0; j < nJ; ++j) {  // tj ascending (sorted columns): each node's range is contiguous
-      int2& r = T.crange[l][tj[j] >> l];
-      if (r.y == 0) r.x = (int)j;
-      r.y = (int)j + 1;
-    }
-  }
+  int64_t W = 0;  // slab columns over all parts
+  for (XPart& pt : parts) W += (int64_t)pt.q.pc.size();
+  if (W == 0) return;
+  require(W <= (int64_t)65535 * 32, BF_ERR_ARG, "too many columns for one extraction launch");
   int64_t cursor = 0;
-  Slabs S = touched_slabs(G, T, cursor);
   PlanBuilder pb;
   pb.use_cols = true;
-  emit_N_touched(pb, G, F, S, T);
-  std::vector<int64_t> jmap(3 * nJ), imap(5 * nI);
-  for (int64_t j = 0; j < nJ; ++j) {
-    jmap[3 * j] = S.col_out(G, 0, tj[j]);
-    jmap[3 * j + 1] = G.c(0, tj[j]);
-    jmap[3 * j + 2] = q.vtoff[j];
+  std::vector<int64_t> jmap, imap, ocol(W);
+  int64_t cb = 0;  // first slab column of the part
+  for (XPart& pt : parts) {
+    const Geom& G = *pt.G;
+    const int L = G.L;
+    const int64_t nI = (int64_t)pt.q.pr.size(), nJ = (int64_t)pt.q.pc.size();
+    if (nI == 0 || nJ == 0) continue;
+    XQuery& q = pt.q;
+    {  // the part's columns in tree order
+      std::vector<int64_t> ord(nJ);
+      for (int64_t j = 0; j < nJ; ++j) ord[j] = j;
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return q.pc[x] < q.pc[y]; });
+      XQuery s = q;
+      for (int64_t j = 0; j < nJ; ++j) {
+        q.pc[j] = s.pc[ord[j]];
+        q.vtoff[j] = s.vtoff[ord[j]];
+        q.ocol[j] = s.ocol[ord[j]];
+      }
+    }
+    Touch T;
+    T.row.resize(L + 1);
+    T.col.resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      T.row[l].assign((size_t)1 << l, 0);
+      T.col[l].assign((size_t)1 << (L - l), 0);
+    }
+    std::vector<int64_t> ti(nI), tj(nJ);
+    for (int64_t i = 0; i < nI; ++i) {
+      ti[i] = leaf_of(G.rlp, q.pr[i]);
+      for (int l = 0; l <= L; ++l) T.row[l][ti[i] >> (L - l)] = 1;
+    }
+    for (int64_t j = 0; j < nJ; ++j) {
+      tj[j] = leaf_of(G.clp, q.pc[j]);
+      for (int l = 0; l <= L; ++l) T.col[l][tj[j] >> l] = 1;
+    }
+    T.rows.resize(L + 1);
+    T.cols.resize(L + 1);
+    T.crange.resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      for (size_t k = 0; k < T.row[l].size(); ++k)
+        if (T.row[l][k]) T.rows[l].push_back((int64_t)k);
+      for (size_t k = 0; k < T.col[l].size(); ++k)
+        if (T.col[l][k]) T.cols[l].push_back((int64_t)k);
+      T.crange[l].assign(T.col[l].size(), make_int2(0, 0));
+      for (int64_t j = 0; j < nJ; ++j) {  // tj ascending: each node's columns are contiguous
+        int2& r = T.crange[l][tj[j] >> l];
+        if (r.y == 0) r.x = (int)(cb + j);
+        r.y = (int)(cb + j) + 1;
+      }
+    }
+    Slabs S = touched_slabs(G, T, cursor);  // appends to the shared slab space
+    emit_N_touched(pb, G, pt.F, S, T);
+    for (int64_t j = 0; j < nJ; ++j) {
+      jmap.push_back(S.col_out(G, 0, tj[j]));
+      jmap.push_back(G.c(0, tj[j]));
+      jmap.push_back(q.vtoff[j]);
+      jmap.push_back(cb + j);
+      ocol[cb + j] = q.ocol[j];
+    }
+    for (int64_t i = 0; i < nI; ++i) {
+      imap.push_back(q.uoff[i]);
+      imap.push_back(q.ustr[i]);
+      imap.push_back(G.r(L, ti[i]));
+      imap.push_back(S.row_in(G, L, ti[i]));
+      imap.push_back(q.orow[i]);
+      imap.push_back(cb);
+      imap.push_back(nJ);
+    }
+    cb += nJ;
   }
-  for (int64_t i = 0; i < nI; ++i) {
-    imap[5 * i] = q.uoff[i];
-    imap[5 * i + 1] = q.ustr[i];
-    imap[5 * i + 2] = G.r(L, ti[i]);
-    imap[5 * i + 3] = S.row_in(G, L, ti[i]);
-    imap[5 * i + 4] = q.orow[i];
-  }
-  const int64_t rows0 = cursor;  // every slab starts at zero: skipped column tiles stay zero
   std::lock_guard<std::mutex> lk(xs.mu);
   Plan P;
   size_t pbytes = 0;
   upload_plan(P, pb, 0, (int)pb.tasks.size(), &pbytes);
   try {
-    // scratch: slab space | column map | row map | output columns
-    const size_t bS = align256((size_t)cursor * (size_t)nJ * cs), bJ = align256(jmap.size() * 8),
-                 bI = align256(imap.size() * 8), bC = align256(q.ocol.size() * 8);
+    // scratch: slab space (every slab starts at zero: skipped column tiles stay zero) | maps
+    const size_t bS = align256((size_t)cursor * (size_t)W * cs), bJ = align256(jmap.size() * 8),
+                 bI = align256(imap.size() * 8), bC = align256(ocol.size() * 8);
     char* base = static_cast<char*>(xs.get(bS + bJ + bI + bC));
     void* dS = base;
     int64_t* dj = reinterpret_cast<int64_t*>(base + bS);
@@ -2420,18 +2441,18 @@ static void extract_core(int dtype, const void* pool, int32_t m3, const Geom& G,
     int64_t* dc = reinterpret_cast<int64_t*>(base + bS + bJ + bI);
     BF_CK(cudaMemcpyAsync(dj, jmap.data(), jmap.size() * 8, cudaMemcpyHostToDevice, st));
     BF_CK(cudaMemcpyAsync(di, imap.data(), imap.size() * 8, cudaMemcpyHostToDevice, st));
-    BF_CK(cudaMemcpyAsync(dc, q.ocol.data(), q.ocol.size() * 8, cudaMemcpyHostToDevice, st));
-    BF_CK(cudaMemsetAsync(dS, 0, (size_t)rows0 * (size_t)nJ * cs, st));
+    BF_CK(cudaMemcpyAsync(dc, ocol.data(), ocol.size() * 8, cudaMemcpyHostToDevice, st));
+    BF_CK(cudaMemsetAsync(dS, 0, (size_t)cursor * (size_t)W * cs, st));
     StageArgs a{};
     a.pool = pool;
     a.m3 = m3;
     a.S = dS;
-    a.ldS = nJ;
+    a.ldS = W;
     a.conj_flip = 0;
-    a.nrhs = (int32_t)nJ;
-    launch_extract_vt_cols(dtype, nJ, dj, pool, dS, st);
+    a.nrhs = (int32_t)W;
+    launch_extract_vt_cols(dtype, (int64_t)jmap.size() / 4, dj, pool, dS, W, st);
     run_plan(dtype, P, a, st);
-    launch_extract_u_rows(dtype, nI, nJ, di, dc, pool, dS, out, ldo, st);
+    launch_extract_u_rows(dtype, (int64_t)imap.size() / 7, di, dc, pool, dS, W, out, ldo, st);
     BF_CK(cudaGetLastError());
     BF_CK(cudaStreamSynchronize(st));
   } catch (...) {
@@ -2503,7 +2524,11 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
       q.vtoff[j] = F.vt + G.vt_off[nu] + (q.pc[j] - G.clp[nu]) * G.c(0, nu);
       q.ocol[j] = j;
     }
-    extract_core(h->dtype, h->pool, h->m3, G, F, q, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
+    std::vector<XPart> parts(1);
+    parts[0].G = &G;
+    parts[0].F = F;
+    parts[0].q = std::move(q);
+    extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
@@ -2554,7 +2579,9 @@ int hodbf_extract(hodbf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, c
       BF_CK(cudaGetLastError());
       BF_CK(cudaStreamSynchronize(st));
     }
-    // every sibling butterfly a requested row and column meet in: B_a = A(T_a, T_{a^1}) at level l
+    // every sibling butterfly a requested row and column meet in: B_a = A(T_a, T_{a^1}) at level
+    // l -- all of them in one extraction plan
+    std::vector<XPart> parts;
     for (int l = 1; l <= LH; ++l) {
       const int sh = LH - l;
       const int64_t w = int64_t(1) << sh;
@@ -2585,9 +2612,10 @@ int hodbf_extract(hodbf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, c
           q.ocol.push_back(j);
           (void)nu;
         }
-        extract_core(h->dtype, h->pool, h->m3, G, h->F[k], q, out, ldo, st, h->xs);
+        parts.push_back(XPart{&G, h->F[k], std::move(q)});
       }
     }
+    extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, st, h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
