@@ -95,10 +95,10 @@ inline bool pdl_enabled() {
   return on;
 }
 template <typename Arg>
-inline void launch_pdl(void (*kernel)(Arg), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                       const Arg& a) {
+inline void launch_pdl(void (*kernel)(Arg), unsigned grid, unsigned grid_y, unsigned block, size_t smem,
+                       cudaStream_t st, const Arg& a) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(grid, grid_y);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -108,6 +108,11 @@ inline void launch_pdl(void (*kernel)(Arg), unsigned grid, unsigned block, size_
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kernel, a);
+}
+template <typename Arg>
+inline void launch_pdl(void (*kernel)(Arg), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       const Arg& a) {
+  launch_pdl(kernel, grid, 1u, block, smem, st, a);
 }
 const char* round_kernel_name(int dtype, const Round& r, int* id);
 

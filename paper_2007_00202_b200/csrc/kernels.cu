@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   E* sm = reinterpret_cast<E*>(sm_raw);  // C::NST stages of [A: KC x SA][B: KC x SB]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int2 un = a.units[blockIdx.x];
+  const int2 un = a.units[blockIdx.x];  // plan tables: immutable, read before the PDL wait
   const Task tk = a.tasks[un.x];
+  pdl_wait();  // slabs / X / Y of the previous rounds (programmatic dependent launch)
   const int r0 = un.y * TR;
   const int j0 = blockIdx.y * TC;
   if (a.cols) {  // bf_extract: only the column tiles the task's output has nonzeros in
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
     }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
+  pdl_trigger();  // the next round's CTAs may launch once every CTA of this one is storing
   const int rb = r0 + wr, cb = j0 + wc;
   if (a.out_kind == 0) {
     E* Sd = static_cast<E*>(a.S);
@@ -211,7 +213,7 @@ static void launch_tile_t(dim3 grid, const StageArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(k_stage_tile<Pol, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_stage_tile<Pol, M3><<<grid, 256, smem, st>>>(a);
+  launch_pdl(k_stage_tile<Pol, M3>, grid.x, grid.y, 256, smem, st, a);
 }
 template <class Pol>
 static void launch_tile(dim3 grid, const StageArgs& a, cudaStream_t st) {
