@@ -160,13 +160,95 @@ def bf_apply(bf, X, op: str = "N") -> np.ndarray:
 # ----------------------------------------------------------------------------------
 # sampled rows / columns (C2 step 5)
 # ----------------------------------------------------------------------------------
-def bf_rows_apply(bf, user_rows, X) -> np.ndarray:
-    """(K_user X)[user_rows, :] without forming K: rows of Eq. (3.1) blocks.
+def _ranks(bf):
+    """r^l (row side, l = lc..L) and c^l (column side, l = 0..lc) per canonical index."""
+    L, lc = bf.L, bf.lc
+    r = {L: np.asarray(bf.U.cols)}
+    for l in range(lc, L):
+        r[l] = np.asarray(bf.R[l - lc].cols)
+    c = {0: np.asarray(bf.Vt.rows)}
+    for l in range(1, lc + 1):
+        c[l] = np.asarray(bf.W[l - 1].rows)
+    return r, c
 
-    For each sampled row i (tree position p) in centre node tau_c, row p of
-    Uhat_{tau_c,nu} follows Eq. (3.2) restricted to that row; Vthat_{tau_c,nu} is
-    formed in full; the K row block over S_nu is (Uhat[p] B) Vthat, then times X(S_nu).
-    """
+
+def _row_chains(bf, tree_rows):
+    """Row p of Uhat_{tau_c(p), nu} for every nu at level lc (Eq. 3.2 left, restricted
+    to one row): Uhat_{tau,nu}[p] = Uhat_{child,nu>>1}[p] R_{tau,nu}[rows of that child], where
+    child = 2tau or 2tau+1 is the one containing p.  Rows are processed in groups that share
+    their level-l node tau; returns {tau_c: (row positions, [per nu: s x r^lc_{tau_c,nu}])}."""
+    L, lc = bf.L, bf.lc
+    r, _ = _ranks(bf)
+    leaf = np.searchsorted(bf.row_leaf_ptr, tree_rows, side="right") - 1
+    groups = {}
+    for tau in np.unique(leaf):
+        sel = np.nonzero(leaf == tau)[0]
+        o0 = int(bf.row_leaf_ptr[tau])
+        groups[int(tau)] = (sel, [np.asarray(bf.Ub(int(tau)), dtype=C128)[tree_rows[sel] - o0, :]])
+    for l in range(L - 1, lc - 1, -1):
+        nxt = {}
+        for tau in sorted({t >> 1 for t in groups}):
+            sels, vecs = [], []
+            for ch in (0, 1):
+                g = groups.get(2 * tau + ch)
+                if g is None:
+                    continue
+                sel, v = g
+                out = []
+                for nu in range(1 << (L - l)):
+                    Rb = np.asarray(bf.Rb(l, tau, nu), dtype=C128)
+                    rt = int(r[l + 1][bf.idx(l + 1, 2 * tau, nu >> 1)])
+                    part = Rb[:rt, :] if ch == 0 else Rb[rt:, :]
+                    out.append(v[nu >> 1] @ part)
+                sels.append(sel)
+                vecs.append(out)
+            sel = np.concatenate(sels)
+            v = [np.vstack([vv[nu] for vv in vecs]) for nu in range(1 << (L - l))]
+            nxt[tau] = (sel, v)
+        groups = nxt
+    return groups
+
+
+def _col_descend(bf, groups):
+    """Push row vectors u (one per centre block (tau_c, nu), s x c^lc) down the column-side
+    recursion Eq. (3.2) right: u Vthat_{tau,nu} = [(u W_{tau,nu})[:, :c_left]
+    Vthat_{tau>>1,2nu}, (u W_{tau,nu})[:, c_left:] Vthat_{tau>>1,2nu+1}], down to the leaves,
+    where u Vthat_{0,nu} = u Vt_nu.  Returns (row positions, [per leaf nu: s x n_nu])."""
+    L, lc = bf.L, bf.lc
+    _, c = _ranks(bf)
+    for l in range(lc, 0, -1):
+        nxt = {}
+        for tau in sorted({t >> 1 for t in groups}):
+            sels, vecs = [], []
+            for ch in (0, 1):
+                g = groups.get(2 * tau + ch)
+                if g is None:
+                    continue
+                sel, u = g
+                t = 2 * tau + ch
+                out = [None] * (1 << (L - l + 1))
+                for nu in range(1 << (L - l)):
+                    P = u[nu] @ np.asarray(bf.Wb(l, t, nu), dtype=C128)
+                    cl = int(c[l - 1][bf.idx(l - 1, tau, 2 * nu)])
+                    out[2 * nu], out[2 * nu + 1] = P[:, :cl], P[:, cl:]
+                sels.append(sel)
+                vecs.append(out)
+            sel = np.concatenate(sels)
+            u = [np.vstack([vv[nu] for vv in vecs]) for nu in range(1 << (L - l + 1))]
+            nxt[tau] = (sel, u)
+        groups = nxt
+    sel, u = groups[0]
+    return sel, [u[nu] @ np.asarray(bf.Vtb(nu), dtype=C128) for nu in range(1 << L)]
+
+
+def bf_rows_apply(bf, user_rows, X) -> np.ndarray:
+    """(K_user X)[user_rows, :] without forming K: rows of Eq. (3.1) blocks (SURVEY C2 step 5).
+
+    Row p (tree position) of the centre block K(O_tau_c, S_nu) is Uhat_{tau_c,nu}[p] B_{tau_c,nu}
+    Vthat_{tau_c,nu} (Eq. 3.1): the row of Uhat by Eq. (3.2) left restricted to that
+    row (_row_chains), times B, then pushed as a row vector through Eq. (3.2) right down to the
+    column leaves (_col_descend) -- the nested bases of P:302-317 evaluated from the row side,
+    never forming any Vthat.  The K row segment over leaf S_nu0 then multiplies X(S_nu0)."""
     L, lc = bf.L, bf.lc
     assert len(np.unique(user_rows)) == len(user_rows), "sampled rows must be unique"
     X = np.asarray(X, dtype=C128)
@@ -175,41 +257,95 @@ def bf_rows_apply(bf, user_rows, X) -> np.ndarray:
     tree_rows = inv_row[np.asarray(user_rows, dtype=np.int64)]
     Xt = X[bf.col_perm, :]                     # X in column-tree order
     out = np.zeros((len(tree_rows), X.shape[1]), dtype=C128)
-    w_c = 1 << (L - lc)
-    centre = np.searchsorted(bf.row_leaf_ptr, tree_rows, side="right") - 1
-    centre = centre // w_c
-    for tau_c in np.unique(centre):
-        sel = np.nonzero(centre == tau_c)[0]
-        order = np.argsort(tree_rows[sel], kind="stable")
-        sel = sel[order]
-        rows = tree_rows[sel]                   # sorted, unique (caller's rows are unique)
-        bases = _Bases(bf)
-
-        def urows(l, tau, nu):
-            """(rows of O_tau among `rows`, Uhat_{tau,nu}[those rows, :])."""
-            o0, o1 = _O(bf, l, tau)
-            mine = rows[(rows >= o0) & (rows < o1)]
-            if l == L:
-                return mine, np.asarray(bf.Ub(tau), dtype=C128)[mine - o0, :]
-            R = np.asarray(bf.Rb(l, tau, nu), dtype=C128)
-            mt, ut = urows(l + 1, 2 * tau, nu >> 1)
-            mb, ub = urows(l + 1, 2 * tau + 1, nu >> 1)
-            # rows of diag(Uhat_top, Uhat_bot) R
-            full = sla.block_diag(ut, ub) @ R
-            return np.concatenate([mt, mb]), full
-
-        for nu in range(1 << (L - lc)):
-            c0, c1 = _S(bf, L - lc, nu)
-            rr, ur = urows(lc, int(tau_c), nu)
-            Krow = ur @ np.asarray(bf.Bb(int(tau_c), nu), dtype=C128) @ bases.Vthat(lc, int(tau_c), nu)
-            out[sel[np.searchsorted(rows, rr)], :] += Krow @ Xt[c0:c1, :]
-            # drop memoised bases of this nu's column chain to bound memory
-            bases.Vm.clear()
+    if len(tree_rows) == 0:
+        return out
+    groups = _row_chains(bf, tree_rows)
+    # centre: u_{tau_c,nu} = Uhat[p] B_{tau_c,nu}
+    cen = {tau: (sel, [v[nu] @ np.asarray(bf.Bb(tau, nu), dtype=C128) for nu in range(1 << (L - lc))])
+           for tau, (sel, v) in groups.items()}
+    sel, seg = _col_descend(bf, cen)
+    acc = np.zeros((len(sel), X.shape[1]), dtype=C128)
+    for nu in range(1 << L):
+        c0, c1 = int(bf.col_leaf_ptr[nu]), int(bf.col_leaf_ptr[nu + 1])
+        acc += seg[nu] @ Xt[c0:c1, :]
+    out[sel] = acc
     return out
 
 
+def _col_chains(bf, tree_cols):
+    """Column q of Vthat_{tau,nu_c(q)} for every tau at level lc (Eq. 3.2 right, P:312-316,
+    restricted to one column): Vthat_{tau,nu}[:, q] = W_{tau,nu}[:, cols of the child holding q]
+    Vthat_{tau>>1,child}[:, q].  Groups share their T_S node; returns
+    {nu_c: (column positions, [per tau: c^lc_{tau,nu_c} x s])}."""
+    L, lc = bf.L, bf.lc
+    _, c = _ranks(bf)
+    leaf = np.searchsorted(bf.col_leaf_ptr, tree_cols, side="right") - 1
+    groups = {}
+    for nu in np.unique(leaf):
+        sel = np.nonzero(leaf == nu)[0]
+        s0 = int(bf.col_leaf_ptr[nu])
+        groups[int(nu)] = (sel, [np.asarray(bf.Vtb(int(nu)), dtype=C128)[:, tree_cols[sel] - s0]])
+    for l in range(1, lc + 1):
+        nxt = {}
+        for nu in sorted({v >> 1 for v in groups}):
+            sels, vecs = [], []
+            for ch in (0, 1):
+                g = groups.get(2 * nu + ch)
+                if g is None:
+                    continue
+                sel, v = g
+                out = []
+                for tau in range(1 << l):
+                    Wb = np.asarray(bf.Wb(l, tau, nu), dtype=C128)
+                    cl = int(c[l - 1][bf.idx(l - 1, tau >> 1, 2 * nu)])
+                    part = Wb[:, :cl] if ch == 0 else Wb[:, cl:]
+                    out.append(part @ v[tau >> 1])
+                sels.append(sel)
+                vecs.append(out)
+            sel = np.concatenate(sels)
+            v = [np.hstack([vv[tau] for vv in vecs]) for tau in range(1 << l)]
+            nxt[nu] = (sel, v)
+        groups = nxt
+    return groups
+
+
+def _row_ascend(bf, groups):
+    """Push column vectors w (one per centre block (tau, nu_c), r^lc x s) up the row-side
+    recursion Eq. (3.2) left (P:303-309): Uhat_{tau,nu} w = [Uhat_{2tau,nu>>1} (R w)[:r_top];
+    Uhat_{2tau+1,nu>>1} (R w)[r_top:]], up to the row leaves, where Uhat_{tau,0} = U_tau.
+    Returns (column positions, [per leaf tau: m_tau x s])."""
+    L, lc = bf.L, bf.lc
+    r, _ = _ranks(bf)
+    for l in range(lc, L):
+        nxt = {}
+        for nu in sorted({v >> 1 for v in groups}):
+            sels, vecs = [], []
+            for ch in (0, 1):
+                g = groups.get(2 * nu + ch)
+                if g is None:
+                    continue
+                sel, w = g
+                v = 2 * nu + ch
+                out = [None] * (1 << (l + 1))
+                for tau in range(1 << l):
+                    P = np.asarray(bf.Rb(l, tau, v), dtype=C128) @ w[tau]
+                    rt = int(r[l + 1][bf.idx(l + 1, 2 * tau, nu)])
+                    out[2 * tau], out[2 * tau + 1] = P[:rt], P[rt:]
+                sels.append(sel)
+                vecs.append(out)
+            sel = np.concatenate(sels)
+            w = [np.hstack([vv[tau] for vv in vecs]) for tau in range(1 << (l + 1))]
+            nxt[nu] = (sel, w)
+        groups = nxt
+    sel, w = groups[0]
+    return sel, [np.asarray(bf.Ub(tau), dtype=C128) @ w[tau] for tau in range(1 << L)]
+
+
 def bf_cols_apply_adj(bf, user_cols, X) -> np.ndarray:
-    """(K_user^H X)[user_cols, :] via sampled columns of Eq. (3.1) blocks."""
+    """(K_user^H X)[user_cols, :] via sampled columns of Eq. (3.1) blocks: column q of the centre
+    block K(O_tau, S_nu_c) is Uhat_{tau,nu_c} B_{tau,nu_c} Vthat_{tau,nu_c}[:, q] -- the column of
+    Vthat by Eq. (3.2) right restricted to q (_col_chains), times B, pushed up Eq. (3.2) left to
+    the row leaves (_row_ascend); then (K^H X)[q] = sum over row leaves K(O_tau, q)^H X(O_tau)."""
     L, lc = bf.L, bf.lc
     assert len(np.unique(user_cols)) == len(user_cols), "sampled columns must be unique"
     X = np.asarray(X, dtype=C128)
@@ -218,32 +354,17 @@ def bf_cols_apply_adj(bf, user_cols, X) -> np.ndarray:
     tree_cols = inv_col[np.asarray(user_cols, dtype=np.int64)]
     Xt = X[bf.row_perm, :]                     # X in row-tree order
     out = np.zeros((len(tree_cols), X.shape[1]), dtype=C128)
-    w_c = 1 << lc                               # leaves per T_S node at level L - lc
-    centre = (np.searchsorted(bf.col_leaf_ptr, tree_cols, side="right") - 1) // w_c
-    for nu_c in np.unique(centre):
-        sel = np.nonzero(centre == nu_c)[0]
-        order = np.argsort(tree_cols[sel], kind="stable")
-        sel = sel[order]
-        cols = tree_cols[sel]                   # sorted, unique
-        bases = _Bases(bf)
-
-        def vcols(l, tau, nu):
-            """(cols of S_nu among `cols`, Vthat_{tau,nu}[:, those cols])."""
-            s0, s1 = _S(bf, L - l, nu)
-            mine = cols[(cols >= s0) & (cols < s1)]
-            if l == 0:
-                return mine, np.asarray(bf.Vtb(nu), dtype=C128)[:, mine - s0]
-            Wb = np.asarray(bf.Wb(l, tau, nu), dtype=C128)
-            ml, vl = vcols(l - 1, tau >> 1, 2 * nu)
-            mr, vr = vcols(l - 1, tau >> 1, 2 * nu + 1)
-            return np.concatenate([ml, mr]), Wb @ sla.block_diag(vl, vr)
-
-        for tau in range(1 << lc):
-            r0, r1 = _O(bf, lc, tau)
-            cc, vc = vcols(lc, tau, int(nu_c))
-            Kcol = bases.Uhat(lc, tau, int(nu_c)) @ np.asarray(bf.Bb(tau, int(nu_c)), dtype=C128) @ vc
-            out[sel[np.searchsorted(cols, cc)], :] += Kcol.conj().T @ Xt[r0:r1, :]
-            bases.Um.clear()
+    if len(tree_cols) == 0:
+        return out
+    groups = _col_chains(bf, tree_cols)
+    cen = {nu: (sel, [np.asarray(bf.Bb(tau, nu), dtype=C128) @ v[tau] for tau in range(1 << lc)])
+           for nu, (sel, v) in groups.items()}
+    sel, seg = _row_ascend(bf, cen)
+    acc = np.zeros((len(sel), X.shape[1]), dtype=C128)
+    for tau in range(1 << L):
+        r0, r1 = int(bf.row_leaf_ptr[tau]), int(bf.row_leaf_ptr[tau + 1])
+        acc += seg[tau].conj().T @ Xt[r0:r1, :]
+    out[sel] = acc
     return out
 
 
