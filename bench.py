@@ -12,8 +12,9 @@ SURVEY 8(a) rows a1-a5; a6 with --op C), inputs resident in HBM.  The factors (2
 c128 / 1.24 GB c64) are far larger than the 126 MB L2, so every step streams them from
 HBM; no L2 flush is needed between steps.
 
-value = algorithmic bytes / time (all factor entries once + X read once + Y written
-once), whole job.  Multi-GPU: the butterfly is split by column subtrees
+value = algorithmic bytes / time (every factor entry an apply streams once + X read once + Y
+written once; SURVEY 8(d) -- the centre B^{lc}, folded into R^{lc} at create, is not counted:
+config.b_folded_entries), whole job.  Multi-GPU: the butterfly is split by column subtrees
 (V, W, B) and row subtrees (R, U) with one NCCL all-to-all of the centre slabs; total
 work is fixed (strong scaling).  Prints ONE JSON line on rank 0.
 """
@@ -30,7 +31,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "butterfly apply GB/s and RHS-columns/s, % of B200 HBM roofline, 1/2/4/8 GPUs"
-WORKLOAD = "cfg5: random-factor butterfly n=m=2^20, L=14, lc=7, leaf 64, r=16, nrhs=32, seed 1"
+
+
+def workload(args):
+    return (f"cfg5: random-factor butterfly n=m=2^20, L=14, lc=7, leaf 64, r=16, nrhs={args.nrhs}, seed 1, "
+            f"{args.dtype}, op {args.op}")
 
 
 def _peaks():
@@ -100,11 +105,21 @@ class ClockSampler:
 
 
 def cpu_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        return len(os.sched_getaffinity(0))
+    """Host cores this process may run on (os.sched_getaffinity; SURVEY 8(d) timing protocol)."""
+    return len(os.sched_getaffinity(0))
+
+
+def method_sample(bf, X, op, reps=1):
+    """Time the level-by-level CPU apply (oracle/stagewise.py: the method on
+    the host, all cores) on the WHOLE workload: one full apply per rep, measured, not
+    extrapolated.  Returns (seconds per apply, threads)."""
+    from oracle.stagewise import bf_apply_stagewise, host_threads
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        bf_apply_stagewise(bf, X, op)
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts)), host_threads()
 
 
 def cpu_model():
@@ -159,6 +174,18 @@ PIPE = {"c128": ("dmma_sync_tflops", 6, "FP64 tensor pipe (mma.sync.m8n8k4.f64);
 TF32_OVER_BF16 = 1.1 / 2.25
 
 
+def issued_cols(dtype, name, nrhs):
+    """Right-hand-side columns the kernel's MMAs cover (the n-tile widths it instantiates): the
+    window pass runs 8 columns per warp for nrhs <= 8 (complex128), one 16-column half for
+    nrhs <= 16, else whole 32-column tiles; complex64's pass keeps 16 columns (its MMA's M) for
+    nrhs <= 16.  The leaf kernels: 8 / 16 / 32-column variants likewise."""
+    if dtype == "c128" and nrhs <= 8:
+        return 8
+    if nrhs <= 16:
+        return 16 if (dtype == "c64" or nrhs > 8) else 8
+    return 32 * ((nrhs + 31) // 32)
+
+
 def dominant_roofline(dtype, name, rounds, mean, nrhs, cs, peaks):
     """Roofline of the kernel with the largest share of the step, from its per-launch CUDA-event
     times: algorithmic bytes (factor entries + user rows) against the HBM peak and the
@@ -167,9 +194,11 @@ def dominant_roofline(dtype, name, rounds, mean, nrhs, cs, peaks):
     t = float(sum(mean[i] for i in idx)) * 1e-3 / len(idx)                 # s per launch
     b = sum((rounds[i]["factor_entries"] + (rounds[i]["user_rows_in"] + rounds[i]["user_rows_out"]) * nrhs) * cs
             for i in idx) / len(idx)                                        # bytes per launch
-    tiles = (nrhs + 31) // 32
     key, fpc, note = PIPE[dtype]
-    fl = sum(rounds[i]["factor_entries"] for i in idx) / len(idx) * tiles * 32 * fpc
+    cols = issued_cols(dtype, name, nrhs)
+    ent = sum(rounds[i]["factor_entries"] for i in idx) / len(idx)
+    fl = ent * cols * fpc                                                     # pipe flops issued per launch
+    method_fl = ent * nrhs * 8                                                # the method's own flops (8 per CMAC)
     sync_peak = ((peaks.get("pipes") or {}).get(key) or 0.0) * 1e12   # mma.sync rate measured on this pool
     if dtype == "c64" and peaks.get("bf16_tflops"):
         pipe_peak = peaks["bf16_tflops"] * TF32_OVER_BF16 * 1e12
@@ -195,17 +224,41 @@ def dominant_roofline(dtype, name, rounds, mean, nrhs, cs, peaks):
     return {"bound": bound, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
             "frac": main["frac"], "traffic": traffic, "kernel": name, "launches_per_step": len(idx),
             "share_of_step": float(sum(mean[i] for i in idx) / mean.sum()), "peak_source": main["peak_source"],
-            "alg_bytes_per_launch": b, "pipe_flops_per_launch": fl,
+            "alg_bytes_per_launch": b, "pipe_flops_per_launch": fl, "pipe_cols_issued": cols,
+            "method_flops_per_launch": method_fl, "method_tflops": method_fl / t / 1e12,
             "other_bound": dict(other, bound="hbm" if bound == "tensor" else "tensor"),
             "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
                             "(profiles/traffic.json)"}
 
 
+def alg_entries(bf):
+    """Factor entries an apply must stream: all of U, R, W, Vt.  The centre B^{lc} is folded into
+    R^{lc} at create (R' = R B, the same shape as R), so its r x c entries per
+    centre block are never read by an apply and are not counted (config 5: 4.19 M entries,
+    1.9 % of the SURVEY 8(d) count, stated in config.b_folded_entries)."""
+    return bf.nnz() - int(bf.B.data.size)
+
+
 def alg_bytes(bf, nrhs, cs):
-    return (bf.nnz() + (bf.m + bf.n) * nrhs) * cs
+    return (alg_entries(bf) + (bf.m + bf.n) * nrhs) * cs
+
+
+def make_config(args, bf, cs, world):
+    """The config dict both arms print (same keys, same values)."""
+    return {"workload": workload(args), "op": args.op, "nrhs": args.nrhs, "n": bf.n, "L": bf.L,
+            "factor_entries": bf.nnz(), "alg_entries": alg_entries(bf), "b_folded_entries": int(bf.B.data.size),
+            "alg_bytes_per_step": alg_bytes(bf, args.nrhs, cs),
+            "l2": "inputs larger than L2 (factors %.2f GB >> 126 MB); no flush" % (bf.nnz() * cs / 1e9),
+            "parallelism": "single GPU" if world == 1 else
+            f"tree split over {world} GPUs (column subtrees -> "
+            + ("fused peer-memory exchange" if args.exchange == "p2p" else "NCCL all-to-all")
+            + " -> row subtrees)"}
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle as it stands, on the host cores.  Each step is one FULL
+    config-5 apply by the level-by-level oracle (oracle/stagewise.py; measured, nothing
+    extrapolated).  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -213,20 +266,21 @@ def run_reference(args):
     cs = 16 if args.dtype == "c128" else 8
     ab = alg_bytes(bf, args.nrhs, cs)
     times = []
-    sample = None
+    threads = None
     for i in range(args.warmup + args.steps):
-        full, spent, sample = oracle_sample(bf, X, nrows=(8, 64), centre=1 + (i % 8))
+        t, threads = method_sample(bf, X, args.op)
         if i >= args.warmup:
-            times.append(full)
+            times.append(t)
     t = float(np.median(times))
     val = ab / t / 1e9
-    cores = cpu_threads()
+    sample = (f"one full config-5 apply (nrhs {args.nrhs}, op {args.op}) per step by oracle/stagewise.py "
+              f"(level-by-level complex128 apply, {threads} threads); median of {args.steps} measured steps")
     line = {"metric": METRIC, "value": val, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": WORKLOAD, "op": args.op, "nrhs": args.nrhs},
-            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
-                             "sample": sample + " (each step one such sample; value from the median extrapolation)"},
+            "config": make_config(args, bf, cs, 1),
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cpu_threads(), "cpu_model": cpu_model(),
+                             "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -382,25 +436,25 @@ def main():
     elif not args.no_e2e and world > 1:
         e2e = h.time_e2e(X_loc_host=Xd.cpu(), op=args.op, steps=max(3, min(args.steps, 10)), alg_bytes=ab)
 
-    cpu = None
+    cpu = cpu_m = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         full, spent, sample = oracle_sample(bf, X)
-        cpu = {"value": ab / full / 1e9, "unit": "GB/s", "cores": cpu_threads(), "cpu_model": cpu_model(), "kind": "oracle",
-               "sample": sample}
+        cpu = {"value": ab / full / 1e9, "unit": "GB/s", "cores": cpu_threads(), "cpu_model": cpu_model(),
+               "kind": "oracle", "extrapolated": True,
+               "sample": "dense-definition oracle (oracle/dense.py, Eq. 3.1-3.2 per sampled row): " + sample}
+        tm, thr = method_sample(bf, X, args.op)
+        cpu_m = {"value": ab / tm / 1e9, "unit": "GB/s", "cores": thr, "cpu_model": cpu_model(), "kind": "method",
+                 "extrapolated": False, "ms_per_step": tm * 1e3,
+                 "sample": f"one full config-5 apply (nrhs {nrhs}, op {args.op}) by the level-by-level CPU apply "
+                           f"(oracle/stagewise.py, SURVEY C2 step 6), {thr} threads, measured"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-                "config": {"workload": WORKLOAD, "op": args.op, "nrhs": nrhs, "n": bf.n, "L": bf.L,
-                           "factor_entries": bf.nnz(), "alg_bytes_per_step": ab,
-                           "l2": "inputs larger than L2 (factors %.2f GB >> 126 MB); no flush" % (bf.nnz() * cs / 1e9),
-                           "parallelism": "single GPU" if world == 1 else
-                           f"tree split over {world} GPUs (column subtrees -> "
-                           + ("fused peer-memory exchange" if args.exchange == "p2p" else "NCCL all-to-all")
-                           + " -> row subtrees)"},
+                "config": make_config(args, bf, cs, world),
                 "rhs_cols_per_s": nrhs / (ms * 1e-3), "hbm_frac": value / peaks["hbm_gbs"],
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_method": cpu_m, "e2e": e2e,
                 "gpu_launches": launches * args.steps, "clocks": clk.summary(), "per_round": per_round,
                 "ms_per_step_evented": ms_evented}
         print(json.dumps(line), flush=True)

@@ -66,7 +66,7 @@ typedef enum { BF_OP_N = 0, BF_OP_T = 1, BF_OP_C = 2 } bf_op;
 
 typedef enum {
   BF_OK = 0,
-  BF_ERR_ARG = -1,    /* NULL / negative argument, aliasing X == Y, workspace too small   */
+  BF_ERR_ARG = -1,    /* NULL / negative argument, X and Y overlap, workspace too small   */
   BF_ERR_SHAPE = -2,  /* leaf offsets not monotone / not summing to m, n; L out of range  */
   BF_ERR_RANK = -3,   /* negative rank, or factor lengths inconsistent with the ranks     */
   BF_ERR_PERM = -4,   /* a permutation is not a bijection                                 */
@@ -124,7 +124,8 @@ int bf_destroy(bf_handle h);
 int bf_info(bf_handle h, bf_info_t* info);
 /* Bytes of device workspace one apply with `nrhs` columns needs (any op). */
 int bf_workspace_size(bf_handle h, int64_t nrhs, size_t* bytes);
-/* Y (m x nrhs) <- K X (X: n x nrhs). */
+/* Y (m x nrhs) <- K X (X: n x nrhs).  The byte ranges of X and Y (first to last element) must
+ * not overlap (BF_ERR_ARG); Y is overwritten (beta = 0). */
 int bf_apply(bf_handle h, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
              void* work, size_t work_bytes, bf_stream_t stream);
 /* Y (n x nrhs) <- K^H X (X: m x nrhs). */

@@ -220,16 +220,28 @@ def _check_rhs(X: torch.Tensor, rows: int, code: int, name: str):
 
 
 class Workspace:
-    """A cached device byte buffer, grown on demand (one per handle and stream)."""
+    """Cached device byte buffers, one per stream, grown on demand.
+
+    Applies on different streams that do not pass an explicit ``work=`` therefore never share a
+    slab buffer (the header allows concurrent applies only with distinct workspaces).  A buffer
+    that is replaced by a larger one is retired with ``record_stream`` on the stream that used
+    it, so the caching allocator cannot hand it out again before that stream's work on it ends.
+    """
 
     def __init__(self, device):
         self.device = device
-        self.buf = None
+        self.bufs = {}
 
-    def get(self, nbytes: int) -> torch.Tensor:
-        if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
-        return self.buf
+    def get(self, nbytes: int, stream=None) -> torch.Tensor:
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        key = st.cuda_stream
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                buf.record_stream(st)
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self.bufs[key] = buf
+        return buf
 
 
 class BFHandle:
@@ -281,7 +293,7 @@ class BFHandle:
         ldy = _check_rhs(out, rout, self.code, "Y")
         wb = self.workspace_size(nrhs)
         if work is None:
-            work = self.ws.get(wb)
+            work = self.ws.get(wb, stream)
         _check("bf_apply_op", lib().bf_apply_op(self.h, OPS[op], nrhs, C.c_void_p(X.data_ptr()), ldx,
                                                 C.c_void_p(out.data_ptr()), ldy,
                                                 C.c_void_p(work.data_ptr()), work.numel(),
@@ -301,7 +313,7 @@ class BFHandle:
             out = torch.empty((nrhs, rout), dtype=X.dtype, device=X.device)
         ldy = _check_rhs(out, rout, self.code, "Y")
         if work is None:
-            work = self.ws.get(self.workspace_size(nrhs))
+            work = self.ws.get(self.workspace_size(nrhs), stream)
         evs = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
         _check("bf_apply_op_events", lib().bf_apply_op_events(
             self.h, OPS[op], nrhs, C.c_void_p(X.data_ptr()), ldx, C.c_void_p(out.data_ptr()), ldy,
@@ -332,7 +344,7 @@ class BFHandle:
         s = C.c_size_t()
         _check("bf_workspace_size_host", lib().bf_workspace_size_host(self.h, OPS[op], nrhs, C.byref(s)))
         if work is None:
-            work = self.ws.get(s.value)
+            work = self.ws.get(s.value, stream)
         _check("bf_apply_host", lib().bf_apply_host(self.h, OPS[op], nrhs, C.c_void_p(Xh.data_ptr()),
                                                     max(rin, 1), C.c_void_p(out.data_ptr()), max(rout, 1),
                                                     C.c_void_p(work.data_ptr()), work.numel(),
@@ -442,7 +454,7 @@ class HODBFHandle:
             out = torch.empty((nrhs, self.n), dtype=X.dtype, device=X.device)
         ldy = _check_rhs(out, self.n, self.code, "Y")
         if work is None:
-            work = self.ws.get(self.workspace_size(nrhs))
+            work = self.ws.get(self.workspace_size(nrhs), stream)
         _check("hodbf_apply", lib().hodbf_apply(self.h, OPS[op], nrhs, C.c_void_p(X.data_ptr()), ldx,
                                                 C.c_void_p(out.data_ptr()), ldy,
                                                 C.c_void_p(work.data_ptr()), work.numel(),
@@ -463,7 +475,7 @@ class HODBFHandle:
             out = torch.empty((nrhs, self.n), dtype=X.dtype, device=X.device)
         ldy = _check_rhs(out, self.n, self.code, "Y")
         if work is None:
-            work = self.ws.get(self.workspace_size(nrhs))
+            work = self.ws.get(self.workspace_size(nrhs), stream)
         evs = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
         _check("hodbf_apply_events", lib().hodbf_apply_events(
             self.h, OPS[op], nrhs, C.c_void_p(X.data_ptr()), ldx, C.c_void_p(out.data_ptr()), ldy,
@@ -478,7 +490,7 @@ class HODBFHandle:
         s = C.c_size_t()
         _check("hodbf_workspace_size_host", lib().hodbf_workspace_size_host(self.h, nrhs, C.byref(s)))
         if work is None:
-            work = self.ws.get(s.value)
+            work = self.ws.get(s.value, stream)
         _check("hodbf_apply_host", lib().hodbf_apply_host(self.h, OPS[op], nrhs, C.c_void_p(Xh.data_ptr()),
                                                           max(self.n, 1), C.c_void_p(out.data_ptr()),
                                                           max(self.n, 1), C.c_void_p(work.data_ptr()),

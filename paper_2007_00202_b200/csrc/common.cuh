@@ -1,6 +1,7 @@
 // Shared definitions of libbfapply (host + device).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdlib>
 #include <stdint.h>
 
@@ -87,6 +88,42 @@ void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const vo
 void launch_extract_u_rows(int dtype, int64_t nE, const int64_t* imap, const int64_t* ocol, const void* pool,
                            const void* S, int64_t ldS, void* out, int64_t ldo, cudaStream_t st);
 void launch_extract_gather(int dtype, int64_t n, const int64_t* pairs, const void* pool, void* out, cudaStream_t st);
+
+// Per-device launch attributes.  A process may hold handles on several GPUs (a handle is bound to
+// the device it was created on and launches with that device current), so everything cached about
+// "the device" is cached per device id, lock-free and thread-safe.
+constexpr int BF_MAX_DEVICES = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+// streaming multiprocessors of the current device
+inline int device_sm_count() {
+  static std::atomic<int> cache[BF_MAX_DEVICES];
+  const int d = current_device();
+  if (d < 0 || d >= BF_MAX_DEVICES) throw Err{BF_ERR_DEVICE, "device id out of range"};
+  int v = cache[d].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    if (e != cudaSuccess || v <= 0) throw Err{BF_ERR_CUDA, std::string("SM count: ") + cudaGetErrorString(e)};
+    cache[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+// cudaFuncAttributeMaxDynamicSharedMemorySize of `kernel` on the current device, set once per
+// device and raised when a larger launch needs it; `state` is the caller's per-kernel static
+// (one slot per device: the largest size set so far).  Failures surface as BF_ERR_CUDA.
+inline void ensure_smem_attr(std::atomic<size_t> (&state)[BF_MAX_DEVICES], const void* kernel, size_t smem) {
+  const int d = current_device();
+  if (d < 0 || d >= BF_MAX_DEVICES) throw Err{BF_ERR_DEVICE, "device id out of range"};
+  if (state[d].load(std::memory_order_acquire) >= smem) return;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) throw Err{BF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)};
+  size_t cur = state[d].load(std::memory_order_relaxed);
+  while (cur < smem && !state[d].compare_exchange_weak(cur, smem, std::memory_order_release)) {
+  }
+}
 
 // Launch with programmatic stream serialization (PDL, see mma.cuh pdl_wait) unless env BF_NO_PDL
 // is set; the kernel must call pdl_wait() before touching stream-ordered memory.

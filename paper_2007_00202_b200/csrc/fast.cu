@@ -424,13 +424,10 @@ const char* fast_kernel_name(int dtype) { return dtype == BF_C128 ? "k_bf_pass<c
 
 template <class Pol, int D, int HV>
 static void launch_hv(const FastArgs& a, unsigned grid, cudaStream_t st) {
-  static bool attr = false;
+  static std::atomic<size_t> attr[BF_MAX_DEVICES];
   const size_t smem = PassCfg<Pol, D>::smem();
   static_assert(PassCfg<Pol, D>::smem() <= 227 * 1024, "pass kernel shared memory");
-  if (!attr) {
-    cudaFuncSetAttribute(k_bf_pass<Pol, D, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem_attr(attr, (const void*)k_bf_pass<Pol, D, HV>, smem);
   launch_pdl(k_bf_pass<Pol, D, HV>, grid, FAST_THREADS, smem, st, a);
 }
 
@@ -441,12 +438,7 @@ static void launch_one(const FastArgs& a, unsigned grid, cudaStream_t st) {
 }
 
 void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = device_sm_count();
   const int64_t items = a.p.nwin * ((a.nrhs + FAST_NB - 1) / FAST_NB);  // (window, rhs tile)
   const unsigned grid = (unsigned)(items < nsm ? items : nsm);
   const int d = a.p.d;

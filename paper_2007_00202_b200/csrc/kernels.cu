@@ -208,11 +208,8 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
 template <class Pol, bool M3>
 static void launch_tile_t(dim3 grid, const StageArgs& a, cudaStream_t st) {
   constexpr size_t smem = TileCfg<Pol>::NST * TileCfg<Pol>::STAGE * sizeof(typename Pol::E);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_stage_tile<Pol, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static std::atomic<size_t> attr[BF_MAX_DEVICES];
+  ensure_smem_attr(attr, (const void*)k_stage_tile<Pol, M3>, smem);
   launch_pdl(k_stage_tile<Pol, M3>, grid.x, grid.y, 256, smem, st, a);
 }
 template <class Pol>
@@ -254,12 +251,7 @@ __global__ void k_accumulate(int64_t rows, int64_t nrhs, const V* __restrict__ A
 
 void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,
                        cudaStream_t st) {
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = device_sm_count();
   const int64_t total = rows * nrhs;
   if (total == 0) return;
   const int64_t want = (total + 255) / 256;

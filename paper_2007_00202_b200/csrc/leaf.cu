@@ -198,12 +198,7 @@ constexpr size_t LEAF_SMEM = 227 * 1024;
 
 template <class Pol, int MODE>
 static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = device_sm_count();
   using E = typename Pol::E;
   const int nch = a.leaf / a.brows;
   const size_t a_chunk = (size_t)a.nsteps * FAST_FRAG / nch;
@@ -220,11 +215,8 @@ static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
   a.npairs = np;
   a.nst = np * dep;
   const size_t smem = (size_t)a.nst * stg + (size_t)a.nst * 8;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_leaf<Pol, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  static std::atomic<size_t> attr[BF_MAX_DEVICES];
+  ensure_smem_attr(attr, (const void*)k_leaf<Pol, MODE>, smem);
   const int64_t items = a.nleaf * ((a.nrhs + FAST_NB - 1) / FAST_NB);
   const unsigned grid = (unsigned)(items < nsm ? items : nsm);
   launch_pdl(k_leaf<Pol, MODE>, grid, LEAF_THREADS, smem, st, a);

@@ -1036,6 +1036,9 @@ struct bf_s {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
   int64_t hcalls = 0;
+  int h_last_op = -1;              // (op, nrhs, workspace) of the previous call: a change relocates
+  int64_t h_last_nrhs = -1;        // the buffer sets inside the workspace
+  const void* h_last_work = nullptr;
   std::vector<int64_t> h_rinv, h_cinv;  // bf_extract: user index -> tree position (filled on first use)
   XScratch xs;                          // bf_extract's device scratch
   ~bf_s() {
@@ -1165,13 +1168,18 @@ static Slabs touched_slabs(const Geom& G, const Touch& T, int64_t& cursor) {
 static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 static void validate_apply(int64_t nrhs, const void* X, int64_t ldx, int64_t rows_x, const void* Y,
-                           int64_t ldy, int64_t rows_y, size_t work_bytes, size_t need) {
+                           int64_t ldy, int64_t rows_y, size_t work_bytes, size_t need, size_t cs) {
   require(nrhs >= 0, BF_ERR_ARG, "nrhs < 0");
   if (nrhs == 0) return;
   require(X != nullptr && Y != nullptr, BF_ERR_ARG, "X or Y is NULL");
-  require(X != Y, BF_ERR_ARG, "X and Y must not alias");
   require(ldx >= std::max<int64_t>(rows_x, 1) && ldy >= std::max<int64_t>(rows_y, 1), BF_ERR_ARG,
           "leading dimension smaller than the number of rows");
+  // X and Y must not overlap: compare the byte extents [first element, last element] of the two
+  // column-major blocks (the apply reads X after it has started writing Y)
+  const uintptr_t x0 = reinterpret_cast<uintptr_t>(X), y0 = reinterpret_cast<uintptr_t>(Y);
+  const uintptr_t x1 = x0 + (uintptr_t)(((nrhs - 1) * ldx + std::max<int64_t>(rows_x, 1)) * (int64_t)cs);
+  const uintptr_t y1 = y0 + (uintptr_t)(((nrhs - 1) * ldy + std::max<int64_t>(rows_y, 1)) * (int64_t)cs);
+  require(x1 <= y0 || y1 <= x0, BF_ERR_ARG, "X and Y must not overlap");
   require(work_bytes >= need, BF_ERR_ARG, "workspace too small");
 }
 
@@ -1430,7 +1438,7 @@ int bf_apply_op_events(bf_handle h, int op, int64_t nrhs, const void* X, int64_t
     const int64_t rx = fwd ? h->G.n : h->G.m, ry = fwd ? h->G.m : h->G.n;
     size_t need = 0;
     bf_workspace_size(h, nrhs, &need);
-    validate_apply(nrhs, X, ldx, rx, Y, ldy, ry, work_bytes, need);
+    validate_apply(nrhs, X, ldx, rx, Y, ldy, ry, work_bytes, need, csize(h->dtype));
     if (nrhs == 0 || ry == 0) return BF_OK;
     require(need == 0 || work != nullptr, BF_ERR_ARG, "workspace is NULL");
     DeviceGuard dg(h->device);
@@ -1550,7 +1558,7 @@ int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx
     size_t need = 0, s = 0;
     bf_workspace_size_host(h, op, nrhs, &need);
     bf_workspace_size(h, nrhs, &s);
-    validate_apply(nrhs, Xh, ldx, rx, Yh, ldy, ry, work_bytes, need);
+    validate_apply(nrhs, Xh, ldx, rx, Yh, ldy, ry, work_bytes, need, csize(h->dtype));
     if (nrhs == 0) return BF_OK;
     DeviceGuard dg(h->device);
     std::lock_guard<std::mutex> lk(h->hmu);
@@ -1569,8 +1577,16 @@ int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx
     const int set = (int)(h->hcalls & 1);
     char* dX = static_cast<char*>(work) + s + set * (bx + by);
     char* dY = dX + bx;
-    // H2D into this set once the apply that last read it (call k - 2) is done
-    if (h->hcalls >= 2) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_cmp[set], 0));
+    // H2D into this set once call k - 2 is done with it: its apply read dX and its D2H read dY
+    // (ev_d2h follows ev_cmp).  The X / Y regions of a set move with (op, nrhs) -- the slab
+    // workspace grows with nrhs and rx / ry swap with op -- and with the workspace pointer, so
+    // after such a change this call's regions may overlap the other set's: wait for both.
+    const bool relayout = h->hcalls > 0 && (op != h->h_last_op || nrhs != h->h_last_nrhs || work != h->h_last_work);
+    if (h->hcalls >= 2) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_d2h[set], 0));
+    if (relayout) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_d2h[set ^ 1], 0));
+    h->h_last_op = op;
+    h->h_last_nrhs = nrhs;
+    h->h_last_work = work;
     if (ldx == rx) {
       BF_CK(cudaMemcpyAsync(dX, Xh, (size_t)rx * nrhs * cs, cudaMemcpyHostToDevice, h->s_h2d));
     } else {
@@ -1875,7 +1891,7 @@ int hodbf_apply_events(hodbf_handle h, int op, int64_t nrhs, const void* X, int6
     require(op == BF_OP_N || op == BF_OP_C || op == BF_OP_T, BF_ERR_ARG, "bad op");
     size_t need = 0;
     hodbf_workspace_size(h, nrhs, &need);
-    validate_apply(nrhs, X, ldx, h->n, Y, ldy, h->n, work_bytes, need);
+    validate_apply(nrhs, X, ldx, h->n, Y, ldy, h->n, work_bytes, need, csize(h->dtype));
     if (nrhs == 0 || h->n == 0) return BF_OK;
     require(nrhs <= (int64_t)65535 * 32, BF_ERR_ARG, "nrhs too large for one launch");
     DeviceGuard dg(h->device);
@@ -1914,7 +1930,7 @@ int hodbf_apply_host(hodbf_handle h, int op, int64_t nrhs, const void* Xh, int64
     size_t need = 0, s = 0;
     hodbf_workspace_size_host(h, nrhs, &need);
     hodbf_workspace_size(h, nrhs, &s);
-    validate_apply(nrhs, Xh, ldx, h->n, Yh, ldy, h->n, work_bytes, need);
+    validate_apply(nrhs, Xh, ldx, h->n, Yh, ldy, h->n, work_bytes, need, csize(h->dtype));
     if (nrhs == 0 || h->n == 0) return BF_OK;
     DeviceGuard dg(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -170,11 +170,14 @@ class DistBFHandle:
         ldy = _check_rhs(out, ro, self.code, "Y_loc")
         wb = self.layout(op, nrhs)[0]
         if work is None:
-            work = self.ws.get(wb)
+            work = self.ws.get(wb, stream)
         st = _stream_handle(stream)
         _check("bf_dist_apply_pre", lib().bf_dist_apply_pre(self.h, OPS[op], nrhs, C.c_void_p(Xloc.data_ptr()), ldx,
                                                              C.c_void_p(work.data_ptr()), work.numel(), st))
-        self.exchange(work, op, nrhs)
+        # NCCL orders the all-to-all against torch's current stream: make that the apply's stream,
+        # so the collective reads the send region after pre and post reads the recv region after it
+        with torch.cuda.stream(self._torch_stream(stream)):
+            self.exchange(work, op, nrhs)
         _check("bf_dist_apply_post", lib().bf_dist_apply_post(self.h, OPS[op], nrhs, C.c_void_p(out.data_ptr()), ldy,
                                                                C.c_void_p(work.data_ptr()), work.numel(), st))
         return out
@@ -192,11 +195,17 @@ class DistBFHandle:
         _check("bf_dist_apply_pre_p2p", _lib().bf_dist_apply_pre_p2p(
             self.h, OPS[op], nrhs, C.c_void_p(Xloc.data_ptr()), ldx, C.c_void_p(work.data_ptr()), work.numel(),
             p2p["peers"], st))
-        p2p["hdl"].barrier(channel=0)   # every sender's slabs have landed
+        ts = self._torch_stream(stream)
+        with torch.cuda.stream(ts):   # the symmetric-memory barriers are issued on the current stream
+            p2p["hdl"].barrier(channel=0)   # every sender's slabs have landed
         _check("bf_dist_apply_post", lib().bf_dist_apply_post(self.h, OPS[op], nrhs, C.c_void_p(out.data_ptr()), ldy,
                                                                C.c_void_p(work.data_ptr()), work.numel(), st))
-        p2p["hdl"].barrier(channel=0)   # every receiver has read them (the next pre may write)
+        with torch.cuda.stream(ts):
+            p2p["hdl"].barrier(channel=0)   # every receiver has read them (the next pre may write)
         return out
+
+    def _torch_stream(self, stream):
+        return stream if stream is not None else torch.cuda.current_stream(torch.device("cuda", self.device))
 
     def time_e2e(self, X_loc_host: torch.Tensor, op: str, steps: int, alg_bytes: int):
         """End-to-end timing through the public API: pinned host X_loc -> device, apply,

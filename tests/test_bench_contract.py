@@ -1,5 +1,6 @@
 """bench.py's JSON-line contract (task statement): the reference arm (the
-CPU oracle on a bounded sample of config 5) runs anywhere; the GPU arm is checked on a B200."""
+CPU oracle: full config-5 applies by the level-by-level CPU apply) runs anywhere; the GPU arm is
+checked on a B200."""
 import json
 import os
 import subprocess
@@ -32,17 +33,27 @@ def test_reference_arm_line():
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("cfg5")
+    assert set(d["config"]) == {"workload", "op", "nrhs", "n", "L", "factor_entries", "alg_entries",
+                                "b_folded_entries", "alg_bytes_per_step", "l2", "parallelism"}
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dtype", ["c128", "c64"])
-def test_gpu_arm_line(dtype):
-    d = run_bench("--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--dtype", dtype)
+@pytest.mark.parametrize("dtype,nrhs", [("c128", 32), ("c64", 32), ("c128", 1), ("c128", 8), ("c128", 16),
+                                        ("c64", 1), ("c64", 16)])
+def test_gpu_arm_line(dtype, nrhs):
+    """The GPU arm's line; the roofline fraction stays <= 1 at every nrhs (the pipe work is counted
+    with the column widths the kernels actually issue), and the config carries the same keys as
+    the reference arm's."""
+    d = run_bench("--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--dtype", dtype, "--nrhs", str(nrhs))
+    assert d["config"]["nrhs"] == nrhs and f"nrhs={nrhs}" in d["config"]["workload"]
+    assert set(d["config"]) == {"workload", "op", "nrhs", "n", "L", "factor_entries", "alg_entries",
+                                "b_folded_entries", "alg_bytes_per_step", "l2", "parallelism"}
     assert BASE_KEYS <= d.keys(), BASE_KEYS - d.keys()
     assert d["dtype"] == dtype and d["n_gpus"] == 1 and d["steps"] == 3
     assert d["value"] > 0 and abs(d["value"] - d["config"]["alg_bytes_per_step"] / (d["ms_per_step"] * 1e6)) < 1e-6 * d["value"]
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] <= 1.0 and r["peak"] > 0
+    assert 0 < r["other_bound"]["frac"] <= 1.0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     e = d["e2e"]
     assert e["unit"] == "GB/s" and 0 < e["value"] < d["value"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0

@@ -99,10 +99,10 @@ def test_dist_fast_emulated(P, L, dtype):
     bf = random_butterfly(L=L, leaf=16, r=16, seed=L + P, dtype=dtype)
     assert DistBFHandle(bf, 0, P, 0).slab_format() == 1
     K = oracle.bf_dense(bf)
-    for op, nr in (("N", 32), ("C", 45), ("T", 7)):
+    for op, nr in (("N", 32), ("C", 45), ("T", 7), ("N", 16), ("C", 12)):
         X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=P + nr, dtype=dtype)
         err = oracle.rel_err(emulate(bf, X, op, P), oracle.apply_op(K, X, op))
-        assert err <= TOL[dtype], (op, err)
+        assert err <= TOL[dtype], (op, nr, err)
 
 
 @pytest.mark.parametrize("op", ["N", "C"])

@@ -65,6 +65,28 @@ def test_fast_large_leaves_and_thin_blocks(L, leaf, nrhs, dtype):
 
 
 @pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("L,leaf,lc", [(3, 16, None), (4, 32, None), (6, 16, 1), (7, 16, None), (5, 64, 5),
+                                       (3, 256, None)])
+@pytest.mark.parametrize("nrhs", [9, 12, 16])
+def test_fast_half_tile_nrhs(L, leaf, lc, nrhs, dtype):
+    """9 <= nrhs <= 16 selects separate instantiations: the pass kernel with one working column
+    half (HV = 1: the second half's warps exit, release counts cover the first half only) and
+    the 16-column leaf kernels (PolC*<2>).  Every pass layout, permuted rows and columns, op
+    N / C / T."""
+    bf = random_butterfly(L=L, leaf=leaf, r=16, seed=L * 10 + leaf + nrhs, lc=lc, dtype=dtype)
+    rng = np.random.default_rng(L + nrhs)
+    bf.row_perm = rng.permutation(bf.m).astype(np.int64)
+    bf.col_perm = rng.permutation(bf.n).astype(np.int64)
+    h = pkg.BFHandle(bf)
+    assert h.rounds("N")[0]["name"].startswith("k_leaf"), "expected the fused path"
+    K = oracle.bf_dense(bf)
+    for op in "NCT":
+        X = random_rhs(bf.n if op == "N" else bf.m, nrhs, seed=L + nrhs, dtype=dtype)
+        err = oracle.rel_err(host(h.apply(dev(X), op)), oracle.apply_op(K, X, op))
+        assert err <= TOL[dtype], (op, nrhs, err)
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
 @pytest.mark.parametrize("L,nrhs,leaf", [(6, 1000, 16), (7, 700, 16), (5, 64 * 32 + 5, 16), (6, 1000, 64), (7, 640, 32)])
 def test_fast_many_items(L, nrhs, leaf, dtype):
     """More work items (windows x rhs tiles) than SMs: each persistent CTA loops over

@@ -195,30 +195,61 @@ def test_concurrent_streams():
         assert oracle.rel_err(host(Y), ref) <= 1e-12
 
 
-# ------------------------------------------------------------------ config 5 (full size, sampled)
-@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
-def test_cfg5_sampled(dtype):
+# ------------------------------------------------------------------ config 5 (full size)
+def _c2_sample(nb, leaf, size, seed):
+    """SURVEY C2 step 5's sample: every index of 8 seeded-random leaves plus 512 seeded-random
+    indices spread over the whole matrix (unique, sorted)."""
+    rng = np.random.default_rng(seed)
+    leaves = rng.choice(nb, 8, replace=False)
+    full = np.concatenate([np.arange(l * leaf, (l + 1) * leaf) for l in leaves])
+    return np.unique(np.concatenate([full, rng.choice(size, 512, replace=False)]))
+
+
+@pytest.fixture(scope="module", params=[np.complex128, np.complex64], ids=["c128", "c64"])
+def cfg5_run(request):
+    """Config 5 at its full size (n = 2^20, L = 14, r = 16, nrhs = 32), applied once per op on
+    the GPU in the launch configuration bench.py times."""
+    dtype = request.param
     bf, X = cfg5(dtype)
     h = pkg.BFHandle(bf)
-    Y = run(h, X, "N")
-    rng = np.random.default_rng(0)
-    # all rows of one centre node's two leaves plus scattered rows in the same centre node
-    w = bf.m >> bf.lc
-    tc = 37
-    rows = np.unique(np.concatenate([np.arange(tc * w, tc * w + 128),
-                                     rng.choice(np.arange(tc * w, (tc + 1) * w), 64, replace=False)]))
-    ref = oracle.bf_rows_apply(bf, rows, X)
-    assert oracle.rel_err(Y[rows], ref) <= TOL[dtype]
     Z = random_rhs(bf.m, 32, seed=12, dtype=dtype)
-    Ya = run(h, Z, "C")
-    wc = bf.n >> (bf.L - bf.lc)
-    cols = np.arange(5 * wc, 5 * wc + 96)
+    out = {"bf": bf, "X": X, "Z": Z, "dtype": dtype, "Y": run(h, X, "N"), "Ya": run(h, Z, "C"),
+           "Yt": run(h, Z, "T")}
+    del h
+    torch.cuda.empty_cache()
+    return out
+
+
+def test_cfg5_sampled(cfg5_run):
+    """C2 step 5: rows of 8 random leaves + 512 random rows across all centre nodes against the
+    sampled-row oracle (Eq. 3.1-3.2 evaluated per row); the same for columns of the adjoint."""
+    bf, X, Z, dtype = cfg5_run["bf"], cfg5_run["X"], cfg5_run["Z"], cfg5_run["dtype"]
+    nb = 1 << bf.L
+    rows = _c2_sample(nb, bf.m // nb, bf.m, seed=0)
+    w = bf.m >> bf.lc
+    assert len(np.unique(rows // w)) >= 100          # spread over (almost) every centre node
+    ref = oracle.bf_rows_apply(bf, rows, X)
+    assert oracle.rel_err(cfg5_run["Y"][rows], ref) <= TOL[dtype]
+    cols = _c2_sample(nb, bf.n // nb, bf.n, seed=1)
     refc = oracle.bf_cols_apply_adj(bf, cols, Z)
-    assert oracle.rel_err(Ya[cols], refc) <= TOL[dtype]
+    assert oracle.rel_err(cfg5_run["Ya"][cols], refc) <= TOL[dtype]
     # dot-product identity over the full vectors (P5)
+    Y, Ya = cfg5_run["Y"], cfg5_run["Ya"]
     lhs = np.vdot(Z.astype(np.complex128), Y.astype(np.complex128))
     rhs = np.vdot(Ya.astype(np.complex128), X.astype(np.complex128))
     assert abs(lhs - rhs) <= TOL[dtype] * np.linalg.norm(Z) * np.linalg.norm(Y)
+
+
+def test_cfg5_full_vector(cfg5_run):
+    """C2 step 6: the whole m x nrhs output of ops N, C and T at config 5 against the
+    independent CPU level-by-level apply (oracle/stagewise.py, complex128 on the same -- for c64
+    the c64-rounded -- factors and inputs)."""
+    from oracle.stagewise import bf_apply_stagewise
+    bf, X, Z, dtype = cfg5_run["bf"], cfg5_run["X"], cfg5_run["Z"], cfg5_run["dtype"]
+    for key, op, V in (("Y", "N", X), ("Ya", "C", Z), ("Yt", "T", Z)):
+        ref = bf_apply_stagewise(bf, V, op)
+        err = oracle.rel_err(cfg5_run[key], ref)
+        assert err <= TOL[dtype], (op, err)
 
 
 # ------------------------------------------------------------------ config 2 (kernel butterfly)
@@ -271,6 +302,10 @@ def test_cfg4():
     lhs = np.vdot(Z, Y[:, :8])
     rhs = np.vdot(Ya, X[:, :8])
     assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(Z) * np.linalg.norm(Y[:, :8])
+    # full vectors (all 51200 x 512 outputs, and the adjoint) against the level-by-level CPU apply
+    from oracle.stagewise import hodbf_apply_stagewise
+    assert oracle.rel_err(Y, hodbf_apply_stagewise(H, X, "N")) <= 1e-12
+    assert oracle.rel_err(Ya, hodbf_apply_stagewise(H, Z, "C")) <= 1e-12
 
 
 @pytest.mark.parametrize("fast", [True, False])
@@ -310,3 +345,74 @@ def test_cuda_graph_replay(kind):
     Yd = h.apply(X2, "N")
     torch.cuda.synchronize()
     assert torch.equal(Yg, Yd)
+
+
+@pytest.mark.parametrize("fast", [True, False])
+def test_host_apply_relayout(fast):
+    """bf_apply_host with nrhs and op changing between back-to-back calls on a non-square
+    butterfly: the buffer sets inside the workspace move with (op, nrhs), so a call must not
+    overwrite a region an earlier call is still copying back (every result is checked after one
+    synchronise)."""
+    if fast:
+        bf = random_butterfly(L=6, leaf=32, r=16, seed=14)
+        bf.row_perm = np.random.default_rng(1).permutation(bf.m)
+    else:
+        rng = np.random.default_rng(6)
+        bf = random_ranks_butterfly(5, rng.integers(1, 30, 32), rng.integers(1, 12, 32), seed=6, rmin=1, rmax=8)
+    assert fast or bf.m != bf.n
+    h = pkg.BFHandle(bf)
+    K = oracle.bf_dense(bf)
+    plan = [("N", 64), ("N", 32), ("C", 32), ("N", 7), ("C", 64), ("T", 33), ("N", 64), ("C", 5)]
+    work = torch.empty(max(h.workspace_size_host(nr, op) for op, nr in plan), dtype=torch.uint8, device="cuda")
+    Xs, Ys = [], []
+    for i, (op, nr) in enumerate(plan):
+        X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=60 + i)
+        rows_out = bf.m if op == "N" else bf.n
+        Xh = torch.from_numpy(np.ascontiguousarray(X.T)).pin_memory()
+        Yh = torch.full((nr, rows_out), 3.0, dtype=torch.complex128).pin_memory()
+        h.apply_host(Xh, op, out=Yh, work=work)
+        Xs.append((X, op))
+        Ys.append(Yh)
+    torch.cuda.synchronize()
+    for (X, op), Yh in zip(Xs, Ys):
+        assert oracle.rel_err(Yh.numpy().T, oracle.apply_op(K, X, op)) <= 1e-12, op
+
+
+def test_streams_default_workspaces():
+    """Concurrent applies on two streams without explicit workspaces: the binding keeps one
+    cached workspace per stream, so they never share slab buffers."""
+    bf = random_butterfly(L=7, leaf=32, r=16, seed=5)
+    h = pkg.BFHandle(bf)
+    X = random_rhs(bf.n, 48, seed=1)
+    ref = oracle.bf_apply(bf, X)
+    Xd = dev(X)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(6):
+        with torch.cuda.stream(s1):
+            outs.append(h.apply(Xd, stream=s1))
+        with torch.cuda.stream(s2):
+            outs.append(h.apply(Xd, stream=s2))
+    torch.cuda.synchronize()
+    assert len(h.ws.bufs) >= 2
+    for Y in outs:
+        assert oracle.rel_err(host(Y), ref) <= 1e-12
+
+
+def test_overlapping_x_y_rejected():
+    """X and Y that overlap without being the same pointer (a shifted view of one buffer) are
+    rejected with BF_ERR_ARG before anything launches."""
+    bf, X = cfg1()
+    h = pkg.BFHandle(bf)
+    buf = torch.zeros((17, bf.n), dtype=torch.complex128, device="cuda")
+    buf[:16] = dev(X)
+    with pytest.raises(pkg.BFError) as e:
+        h.apply(buf[:16], out=buf[1:17])
+    assert e.value.code == -1
+    # disjoint halves of one buffer are fine
+    big = torch.zeros((32, bf.n), dtype=torch.complex128, device="cuda")
+    big[:16] = dev(X)
+    h.apply(big[:16], out=big[16:])
+    torch.cuda.synchronize()
+    assert oracle.rel_err(host(big[16:]), oracle.bf_apply(bf, X)) <= 1e-12

@@ -1,12 +1,29 @@
 """Summarise an ncu report: key throughput metrics, stall reasons, top SASS stall sites."""
-import csv, subprocess, sys, collections
+import csv, re, subprocess, sys, collections
 
 def raw(rep):
+    """(header, rows) of the raw page; section prefixes ("SM_C.TriageCompute.") are stripped so
+    every metric is found by its plain name."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    return rows[0], rows[2:]
+    hdr = []
+    for h in rows[0]:
+        m = re.search(r"([a-z][a-z0-9]*__\S*)$", h)
+        hdr.append(m.group(1) if m and m.group(1) not in hdr else h)
+    return hdr, rows[2:]
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        # tensor pipe (sm_100 names): DMMA = mma.sync f64 (complex128), HMMA = mma.sync tf32 (complex64),
+        # tc = tcgen05 (UTC*MMA)
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__cycles_elapsed.avg.per_second",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__pipe_tensor_subpipe_dmma_cycles_active.avg", "sm__cycles_active.avg",
         "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
