@@ -266,6 +266,96 @@ int hodbf_apply_events(hodbf_handle h, int op, int64_t nrhs, const void* X, int6
                        void* const* events, int32_t nevents);
 
 /* ---- misc ---------------------------------------------------------------------------- */
+/* Copy a single-GPU handle's factors back to HOST arrays in the bf_desc layout (levels and blocks in
+ * canonical order, column-major blocks).  lens[5] receives the element counts of U, R, B, W, Vt;
+ * rank_row ((L-lc+1) 2^L) and rank_col ((lc+1) 2^L) the ranks; any pointer may be NULL.  The
+ * trees (leaf offsets, perms) are the ones the handle was created with.  Synchronous. */
+int bf_export(bf_handle h, int64_t* lens, int32_t* rank_row, int32_t* rank_col, void* U, void* R, void* B,
+              void* W, void* Vt);
+
+/* ---- randomized matrix-free construction (BF_random_matvec) ------------------------------
+ * PAPER.md Sec. 3.3: a butterfly built from multi-RHS products with an operator A that
+ * is available only as a matvec; O(sqrt(n)) sketch columns of an O(n log n) matvec.  Its consumer
+ * is the Schur-complement construction of Alg. 5 and the HOD-BF inversion of Alg. 4
+ * (P:576-612).  The trees (leaf offsets and perms) of the result are the caller's; ranks come from
+ * interpolative decompositions of Gaussian sketches, truncated at relative tolerance
+ * eps, capped at rank_max (the sketch width is rank_max + oversample per block).  The algorithm
+ * (level-by-level peeling) runs on the device: sketch generation, the
+ * gathers, a batched column-pivoted QR per block and the centre least-squares solves are library
+ * kernels; only the small per-block results (ranks, pivots, interpolation matrices) pass through
+ * the host to be packed into the result's descriptor, which is then bf_create'd on `device`.
+ *
+ * The operator is a callback: fn(ctx, op, nrhs, X, ldx, Y, ldy, stream) must write
+ * Y = A X (op BF_OP_N: X n x nrhs, Y m x nrhs) or Y = A^H X (op BF_OP_C: X m x nrhs, Y n x nrhs),
+ * column-major DEVICE blocks in user order, ordered on `stream`, and return BF_OK.  bf_operator_apply
+ * below is such a callback for sums of products of library handles.  Synchronous: the call
+ * returns with the result built (it synchronises `stream`).  Errors: BF_ERR_ARG (bad descriptor,
+ * callback failure), BF_ERR_SHAPE / BF_ERR_PERM (trees), BF_ERR_CUDA, BF_ERR_OOM. */
+typedef int (*bf_matvec_fn)(void* ctx, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                            bf_stream_t stream);
+typedef struct {
+  int32_t dtype;                 /* bf_dtype of the result and of the sketches                   */
+  int32_t L, lc;                 /* levels and centre level of the result (lc < 0: floor(L/2))   */
+  int32_t rank_max;              /* rank cap per block                                           */
+  int64_t m, n;                  /* A is m x n                                                   */
+  const int64_t* row_leaf_ptr;   /* 2^L + 1 offsets of T_O leaves (tree order)                   */
+  const int64_t* col_leaf_ptr;   /* 2^L + 1 offsets of T_S leaves                                */
+  const int64_t* row_perm;       /* tree position -> user row; NULL = identity                  */
+  const int64_t* col_perm;       /* tree position -> user column; NULL = identity               */
+  double eps;                    /* relative ID truncation |R_jj| <= eps |R_11|                  */
+  int32_t oversample;            /* extra sketch columns per block (>= 0; 8-16 typical)          */
+  int32_t reserved;
+  uint64_t seed;                 /* counter-based Gaussian sketches: same seed, same result      */
+  size_t chunk_bytes;            /* device budget of one sketch block + its product (0: 1 GiB)   */
+} bf_rmv_desc;
+typedef struct {
+  int64_t matvec_cols_n;         /* columns applied through A (op N)                             */
+  int64_t matvec_cols_c;         /* columns applied through A^H (op C)                           */
+  int32_t max_rank;              /* largest block rank of the result                             */
+  int32_t saturated;             /* blocks whose rank reached rank_max (sketch possibly too thin) */
+  double t_matvec_ms;            /* device time inside the callback (CUDA events)                */
+  double t_total_ms;             /* wall time of the whole construction                          */
+} bf_rmv_stats;
+int bf_random_matvec(const bf_rmv_desc* desc, bf_matvec_fn fn, void* ctx, int device, bf_stream_t stream,
+                     bf_handle* out, bf_rmv_stats* stats);
+
+/* The batched interpolative decomposition bf_random_matvec runs, exposed for reuse and testing:
+ * nmat complex matrices, matrix i k x pcnt[i] column-major (ld k), packed back to back in the
+ * DEVICE buffer M.  Each is factored in place by Householder QR with column pivoting (largest
+ * remaining column norm, ties to the lowest index), stopped at rank r where |R_rr| <= eps |R_00|
+ * or r = rmax.  Outputs (DEVICE): rank[i]; perm[sum_{j<i} pcnt[j] ..]
+ * the column order (the first r are the skeleton columns); and, in rows 0..r-1 of the columns
+ * r..pcnt[i]-1 of matrix i, T = R11^{-1} R12, so M(:, perm[r + j]) ~= sum_q M(:, perm[q]) T(q, j).
+ * Synchronous. */
+int bf_batched_id(int dtype, int64_t nmat, int32_t k, const int64_t* pcnt, void* M, double eps, int32_t rmax,
+                  int32_t* rank, int32_t* perm, bf_stream_t stream);
+
+/* Composite operators: A = sum_s alpha_s P_s, each product P_s = fac[nfac-1] ... fac[0] (fac[0]
+ * applied first) mapping X rows [col_off, col_off + fac[0].cols) to Y rows [row_off, row_off +
+ * fac[nfac-1].rows) of the m x n operator (block placement).  A factor is a butterfly or HOD-BF
+ * handle with op BF_OP_N or BF_OP_C, or the identity; rows x cols is its shape as it appears.
+ * bf_operator_apply(ctx = const bf_operator*) has the bf_matvec_fn signature: Y = A X (op N) or
+ * A^H X (op C) on device blocks; it allocates its temporaries and synchronises `stream`. */
+typedef enum { BF_FACTOR_BF = 0, BF_FACTOR_HODBF = 1, BF_FACTOR_IDENTITY = 2 } bf_factor_kind;
+typedef struct {
+  int32_t kind, op;
+  void* handle;                  /* bf_handle / hodbf_handle; NULL for the identity              */
+  int64_t rows, cols;
+} bf_factor;
+typedef struct {
+  double alpha_re, alpha_im;
+  int32_t nfac, reserved;
+  const bf_factor* fac;
+  int64_t row_off, col_off;
+} bf_product;
+typedef struct {
+  int32_t dtype, nprod;
+  int64_t m, n;
+  const bf_product* prod;
+} bf_operator;
+int bf_operator_apply(void* op, int opn, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                      bf_stream_t stream);
+
 const char* bf_status_string(int status);
 const char* bf_last_error(void);
 /* Library version and the compile target, e.g. "bfapply 0.1 sm_100a". */

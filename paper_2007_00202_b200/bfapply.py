@@ -259,6 +259,18 @@ class BFHandle:
         _check("bf_info", lib().bf_info(h, C.byref(inf)))
         self.info = {f: getattr(inf, f) for f, _ in bf_info_t._fields_}
 
+    @classmethod
+    def from_raw(cls, h, device: int, code: int, m: int, n: int) -> "BFHandle":
+        """Wrap a handle the library created (e.g. bf_random_matvec's result)."""
+        self = cls.__new__(cls)
+        self.h, self.device, self.code = h, device, code
+        self.m, self.n = m, n
+        self.ws = Workspace(torch.device("cuda", device))
+        inf = bf_info_t()
+        _check("bf_info", lib().bf_info(h, C.byref(inf)))
+        self.info = {f: getattr(inf, f) for f, _ in bf_info_t._fields_}
+        return self
+
     def close(self):
         if getattr(self, "h", None):
             lib().bf_destroy(self.h)

@@ -249,6 +249,36 @@ __global__ void k_accumulate(int64_t rows, int64_t nrhs, const V* __restrict__ A
   }
 }
 
+// Y += alpha A (bf_operator_apply's accumulation of one product into the sum)
+template <typename V>
+__global__ void k_axpy(int64_t rows, int64_t nrhs, double are, double aim, const V* __restrict__ A, int64_t lda,
+                       V* __restrict__ Y, int64_t ldy) {
+  const int64_t total = rows * nrhs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / rows, r = i - c * rows;
+    const V a = A[r + c * lda];
+    V y = Y[r + c * ldy];
+    y.x += (are * a.x - aim * a.y);
+    y.y += (are * a.y + aim * a.x);
+    Y[r + c * ldy] = y;
+  }
+}
+
+void launch_axpy(int dtype, int64_t rows, int64_t nrhs, double are, double aim, const void* A, int64_t lda, void* Y,
+                 int64_t ldy, cudaStream_t st) {
+  const int64_t total = rows * nrhs;
+  if (total == 0) return;
+  const int nsm = device_sm_count();
+  const int64_t want = (total + 255) / 256;
+  const unsigned grid = (unsigned)(want < 8LL * nsm ? want : 8LL * nsm);
+  if (dtype == BF_C128)
+    k_axpy<double2><<<grid, 256, 0, st>>>(rows, nrhs, are, aim, static_cast<const double2*>(A), lda,
+                                          static_cast<double2*>(Y), ldy);
+  else
+    k_axpy<float2><<<grid, 256, 0, st>>>(rows, nrhs, are, aim, static_cast<const float2*>(A), lda,
+                                         static_cast<float2*>(Y), ldy);
+}
+
 void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,
                        cudaStream_t st) {
   const int nsm = device_sm_count();

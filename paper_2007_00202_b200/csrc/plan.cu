@@ -1319,6 +1319,35 @@ int bf_info(bf_handle h, bf_info_t* info) {
   return BF_OK;
 }
 
+// Copy a (single-GPU) handle's factors back to host arrays in the bf_desc layout: the five
+// packed arrays and the two rank arrays.  lens (5 entries) receives the element counts of U, R,
+// B, W, Vt; any output pointer may be NULL (then only lens / ranks are filled).  Used to hand a
+// butterfly built on the device (bf_random_matvec) to host tooling and to the CPU oracle.
+int bf_export(bf_handle h, int64_t* lens, int32_t* rank_row, int32_t* rank_col, void* U, void* R, void* B, void* W,
+              void* Vt) {
+  if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
+  try {
+    require(!h->dist, BF_ERR_ARG, "bf_export: distributed handles hold a rank-local part only");
+    const Geom& G = h->G;
+    const int64_t L5[5] = {G.len_U, G.len_R, G.len_B, G.len_W, G.len_Vt};
+    if (lens)
+      for (int q = 0; q < 5; ++q) lens[q] = L5[q];
+    if (rank_row) std::copy(G.rr.begin(), G.rr.end(), rank_row);
+    if (rank_col) std::copy(G.rc.begin(), G.rc.end(), rank_col);
+    DeviceGuard dg(h->device);
+    const size_t cs = csize(h->dtype);
+    void* dst[5] = {U, R, B, W, Vt};
+    int64_t off = 0;
+    for (int q = 0; q < 5; ++q) {
+      if (dst[q] && L5[q]) BF_CK(cudaMemcpy(dst[q], static_cast<char*>(h->pool) + off * cs, L5[q] * cs, cudaMemcpyDeviceToHost));
+      off += L5[q];
+    }
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
 // fast-path workspace: two slab buffers (every slab of a level, [tile][half][slab][16 x 16]) and,
 // on a split handle, the send and recv regions of the centre exchange (2^L / P slabs each)
 static size_t fast_buf_bytes(bf_handle h, int64_t nrhs) {
@@ -2655,3 +2684,5 @@ int bf_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t 
 }
 
 }  // extern "C"
+
+#include "rmatvec_host.inc"

@@ -1,0 +1,376 @@
+// Device kernels of the randomized matrix-free butterfly construction (bf_random_matvec,
+// SURVEY 8(f) NEXT-2; Sec. 3.3, "BF_random_matvec": a butterfly built from
+// O(n^{1/2}) multi-RHS applies of an O(n log n) matvec; Alg. 5 line S_construction).
+// The host driver is rmatvec_host.inc (level-by-level peeling).
+//
+//   k_sketch_fill   Gaussian sketch blocks with a per-row group support (counter-based RNG:
+//                   every entry is a pure function of (seed, level, row, column), so chunking
+//                   and launch order never change the sketch)
+//   k_gather_t      the sketch rows of each block's candidate skeletons, transposed into one
+//                   packed k x p matrix per block (conjugated for the column side)
+//   k_batched_id    interpolative decomposition of every packed matrix: Householder QR with
+//                   column pivoting, truncated at |R_jj| < eps |R_11| ("U = P[I;
+//                   (R11^-1 R12)^T]"), T = R11^-1 R12 written over R12; one CTA per matrix
+//   k_batched_lsq   the centre blocks: B = Y Z^+ (least squares through a Householder QR of Z^H)
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace bfa {
+
+// ---- complex helpers on double2 / float2 -------------------------------------------------
+template <typename V> struct Real;
+template <> struct Real<double2> { using T = double; };
+template <> struct Real<float2> { using T = float; };
+
+template <typename V> __device__ __forceinline__ V cmk(typename Real<V>::T x, typename Real<V>::T y) {
+  V v;
+  v.x = x;
+  v.y = y;
+  return v;
+}
+template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return cmk<V>(a.x + b.x, a.y + b.y); }
+template <typename V> __device__ __forceinline__ V csub(V a, V b) { return cmk<V>(a.x - b.x, a.y - b.y); }
+template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
+  return cmk<V>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// conj(a) * b
+template <typename V> __device__ __forceinline__ V cmulc(V a, V b) {
+  return cmk<V>(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+template <typename V> __device__ __forceinline__ V cconj(V a) { return cmk<V>(a.x, -a.y); }
+template <typename V> __device__ __forceinline__ typename Real<V>::T cabs2(V a) { return a.x * a.x + a.y * a.y; }
+template <typename V> __device__ __forceinline__ V cdiv(V a, V b) {
+  const typename Real<V>::T d = cabs2(b);
+  return cmk<V>((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+template <typename V> __device__ __forceinline__ V cscale(V a, typename Real<V>::T s) { return cmk<V>(a.x * s, a.y * s); }
+
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- counter-based Gaussian --------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+// one standard complex Gaussian (re, im each N(0, 1)) for the counter (seed, level, row, col)
+__device__ __forceinline__ void gauss2(uint64_t seed, int level, int64_t row, int64_t col, double& re, double& im) {
+  const uint64_t h0 = splitmix64(seed ^ ((uint64_t)level << 58) ^ splitmix64((uint64_t)row * 0x100000001B3ull + (uint64_t)col));
+  const uint64_t h1 = splitmix64(h0);
+  const double u1 = ((h0 >> 11) + 1) * (1.0 / 9007199254740992.0);  // (0, 1]
+  const double u2 = (h1 >> 11) * (1.0 / 9007199254740992.0);        // [0, 1)
+  const double rad = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  re = rad * c;
+  im = rad * s;
+}
+
+// Om[u + c ld] for user rows u < rows, columns c < ncols.  group[u] is the tree node (at the
+// sketch's level) that row u belongs to.  overlay = 0: column c belongs to group g0 + c / k and is
+// nonzero only on that group's rows; overlay = 1: column c of every row u is column
+// group[u] * k + c of the full (block-diagonal) sketch -- the groups' disjoint supports folded
+// into k columns.
+template <typename V>
+__global__ void k_sketch_fill(V* __restrict__ Om, int64_t ld, int64_t rows, int64_t ncols, const int64_t* __restrict__ group,
+                              int64_t g0, int k, uint64_t seed, int level, int overlay) {
+  const int64_t total = rows * ncols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / rows, u = e - c * rows;
+    const int64_t g = group[u];
+    int64_t gc;
+    bool on;
+    if (overlay) {
+      on = g >= 0;
+      gc = g * k + c;
+    } else {
+      on = g == g0 + c / k;
+      gc = g0 * k + c;
+    }
+    double re = 0.0, im = 0.0;
+    if (on) gauss2(seed, level, u, gc, re, im);
+    Om[u + c * ld] = cmk<V>((typename Real<V>::T)re, (typename Real<V>::T)im);
+  }
+}
+
+// Packed matrix i (k rows x p_i columns, column-major, ld k) at out + out_off[i]:
+//   out[a + b k] = f(Y[rows[moff[i] + b] + (mcol[i] + a) ldy]),  f = conj if cj else identity.
+// One CTA per matrix.
+template <typename V>
+__global__ void k_gather_t(V* __restrict__ out, const V* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ rows,
+                           const int64_t* __restrict__ moff, const int64_t* __restrict__ mcol,
+                           const int64_t* __restrict__ out_off, int k, int cj) {
+  const int64_t i = blockIdx.x;
+  const int64_t r0 = moff[i], p = moff[i + 1] - r0, c0 = mcol[i];
+  V* o = out + out_off[i];
+  for (int64_t e = threadIdx.x; e < p * k; e += blockDim.x) {
+    const int64_t b = e / k, a = e - b * k;
+    V v = Y[rows[r0 + b] + (c0 + a) * ldy];
+    if (cj) v.y = -v.y;
+    o[a + b * k] = v;
+  }
+}
+
+// ---- Householder QR (with optional column pivoting) of one k x p matrix in global memory --
+// Reflector for column j: H = I - v v^H * (2 / v^H v), v = x - beta e_0, beta = -e^{i arg x_0} ||x||,
+// so that H x = beta e_0.  With pivot != 0 the column of largest remaining norm is moved to
+// position j first (ties: the lowest index) and the factorisation stops at rank r when
+// |R_rr| <= eps |R_00| (relative truncation) or at rmax.  Columns [ncols_fac, p)
+// are only updated (right-hand sides of a least-squares solve).  Returns the rank (number of
+// reflectors applied) in *rank_out; perm (p entries) gets the column order.
+constexpr int QR_THREADS = 256;
+constexpr int QR_WARPS = QR_THREADS / 32;
+constexpr int QR_MAXK = 1024;  // rows of a packed matrix (sketch width) held in shared memory
+
+template <typename V>
+__device__ int householder_qr(V* A, int k, int p, int ncols_fac, int pivot, double eps, int rmax, int* perm,
+                              typename Real<V>::T* cn, V* v) {
+  using T = typename Real<V>::T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ T s_vv, s_r00;
+  __shared__ int s_piv, s_stop;
+  for (int c = threadIdx.x; c < p; c += blockDim.x) perm[c] = c;
+  const int jmax = min(min(k, ncols_fac), rmax);
+  int j = 0;
+  for (; j < jmax; ++j) {
+    // pivot: remaining column norms over rows j..k-1 (recomputed: robust, same order of work)
+    if (pivot) {
+      for (int c = j + warp; c < ncols_fac; c += QR_WARPS) {
+        T s = 0;
+        for (int r = j + lane; r < k; r += 32) s += cabs2(A[r + (int64_t)c * k]);
+        s = warp_sum(s);
+        if (lane == 0) cn[c] = s;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        T best = -1;
+        int bi = ncols_fac;
+        for (int c = j + lane; c < ncols_fac; c += 32)
+          if (cn[c] > best) {  // strict: the lowest index wins ties within a lane
+            best = cn[c];
+            bi = c;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const T ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          s_piv = bi;
+          const T nrm = sqrt(max(best, (T)0));
+          if (j == 0) s_r00 = nrm;
+          s_stop = !(nrm > 0) || (j > 0 && nrm <= (T)eps * s_r00);
+        }
+      }
+      __syncthreads();
+      if (s_stop) break;
+      const int pv = s_piv;
+      if (pv != j) {
+        for (int r = threadIdx.x; r < k; r += blockDim.x) {
+          const V t = A[r + (int64_t)j * k];
+          A[r + (int64_t)j * k] = A[r + (int64_t)pv * k];
+          A[r + (int64_t)pv * k] = t;
+        }
+        if (threadIdx.x == 0) {
+          const int t = perm[j];
+          perm[j] = perm[pv];
+          perm[pv] = t;
+        }
+      }
+      __syncthreads();
+    }
+    // reflector of column j, rows j..k-1
+    if (warp == 0) {
+      T s = 0;
+      for (int r = j + lane; r < k; r += 32) {
+        const V x = A[r + (int64_t)j * k];
+        v[r] = x;
+        s += cabs2(x);
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        const V x0 = v[j];
+        const T nx = sqrt(s), a0 = sqrt(cabs2(x0));
+        // beta = -e^{i arg x0} ||x||
+        const V ph = a0 > 0 ? cmk<V>(x0.x / a0, x0.y / a0) : cmk<V>(1, 0);
+        const V beta = cmk<V>(-ph.x * nx, -ph.y * nx);
+        v[j] = csub(x0, beta);
+        s_vv = s - cabs2(x0) + cabs2(v[j]);
+        A[j + (int64_t)j * k] = beta;
+      }
+    }
+    __syncthreads();
+    const T vv = s_vv;
+    // apply H to the trailing columns (and the right-hand-side columns)
+    for (int c = j + 1 + warp; c < p; c += QR_WARPS) {
+      V* col = A + (int64_t)c * k;
+      V d = cmk<V>(0, 0);
+      for (int r = j + lane; r < k; r += 32) d = cadd(d, cmulc(v[r], col[r]));
+      d.x = warp_sum(d.x);
+      d.y = warp_sum(d.y);
+      if (vv > 0) {
+        const V f = cscale(d, (T)2 / vv);
+        for (int r = j + lane; r < k; r += 32) col[r] = csub(col[r], cmul(v[r], f));
+      }
+    }
+    for (int r = j + 1 + threadIdx.x; r < k; r += blockDim.x) A[r + (int64_t)j * k] = cmk<V>(0, 0);
+    __syncthreads();
+  }
+  return j;
+}
+
+// Interpolative decomposition of every packed matrix (k x p_i, ld k) in place.  On return:
+//   rank[i] = r; perm[poff[i] + 0..p_i) = column order (the first r are the skeleton columns);
+//   rows 0..r-1 of columns r..p_i-1 hold T = R11^{-1} R12, so that
+//   M(:, perm[r + j]) ~= sum_q M(:, perm[q]) T(q, j)   (the column ID of P:285-288).
+template <typename V>
+__global__ void __launch_bounds__(QR_THREADS) k_batched_id(V* __restrict__ M, const int64_t* __restrict__ moff,
+                                                             const int64_t* __restrict__ pcnt, int k, double eps,
+                                                             int rmax, int32_t* __restrict__ rank,
+                                                             int32_t* __restrict__ perm, const int64_t* __restrict__ poff) {
+  using T = typename Real<V>::T;
+  extern __shared__ __align__(16) unsigned char sm[];
+  V* v = reinterpret_cast<V*>(sm);                       // k
+  T* cn = reinterpret_cast<T*>(sm + sizeof(V) * k);      // p
+  const int64_t i = blockIdx.x;
+  const int p = (int)pcnt[i];
+  V* A = M + moff[i];
+  int* pm = perm + poff[i];
+  const int r = householder_qr<V>(A, k, p, p, 1, eps, rmax, pm, cn, v);
+  __syncthreads();
+  // T = R11^{-1} R12 by back substitution, one column of R12 per thread
+  for (int c = r + threadIdx.x; c < p; c += blockDim.x) {
+    V* col = A + (int64_t)c * k;
+    for (int q = r - 1; q >= 0; --q) {
+      V s = col[q];
+      for (int w = q + 1; w < r; ++w) s = csub(s, cmul(A[q + (int64_t)w * k], col[w]));
+      const V d = A[q + (int64_t)q * k];
+      col[q] = cabs2(d) > 0 ? cdiv(s, d) : cmk<V>(0, 0);
+    }
+  }
+  if (threadIdx.x == 0) rank[i] = r;
+}
+
+// Centre blocks (least squares B Z = Y, Z: c x k full row rank, Y: r x k):
+//   work (k x (c + r), ld k) = [Z^H | Y^H]; Householder QR of the first c columns applied to all;
+//   B^H = R^{-1} (Q^H Y^H)[0..c);  B (r x c, column-major) written to out + boff[i].
+// Z rows come from the slab space (row zrow[i] + q, k contiguous columns: Z(q, a) = S[(zrow + q) k + a]),
+// Y rows from the sketch (user row yrows[yoff[i] + q], columns ycol[i] + a).
+template <typename V>
+__global__ void __launch_bounds__(QR_THREADS) k_batched_lsq(V* __restrict__ work, const int64_t* __restrict__ woff,
+                                                              const V* __restrict__ S, const int64_t* __restrict__ zrow,
+                                                              const int32_t* __restrict__ cdim, const V* __restrict__ Ysk,
+                                                              int64_t ldy, const int64_t* __restrict__ yrows,
+                                                              const int64_t* __restrict__ yoff, const int64_t* __restrict__ ycol,
+                                                              int k, V* __restrict__ out, const int64_t* __restrict__ boff) {
+  using T = typename Real<V>::T;
+  extern __shared__ __align__(16) unsigned char sm[];
+  V* v = reinterpret_cast<V*>(sm);
+  T* cn = reinterpret_cast<T*>(sm + sizeof(V) * k);
+  int* pm = reinterpret_cast<int*>(sm + sizeof(V) * k + sizeof(T) * k);
+  const int64_t i = blockIdx.x;
+  const int c = cdim[i];
+  const int r = (int)(yoff[i + 1] - yoff[i]);
+  if (r == 0) return;  // B is r x c: nothing to write
+  if (c == 0) return;
+  V* A = work + woff[i];
+  for (int64_t e = threadIdx.x; e < (int64_t)k * (c + r); e += blockDim.x) {
+    const int col = (int)(e / k), a = (int)(e - (int64_t)col * k);
+    V x;
+    if (col < c)
+      x = cconj(S[(zrow[i] + col) * (int64_t)k + a]);
+    else
+      x = cconj(Ysk[yrows[yoff[i] + (col - c)] + (ycol[i] + a) * ldy]);
+    A[a + (int64_t)col * k] = x;
+  }
+  __syncthreads();
+  householder_qr<V>(A, k, c + r, c, 0, 0.0, c, pm, cn, v);
+  __syncthreads();
+  // back substitution: B^H(:, q) = R^{-1} (Q^H Y^H)(0..c, q), one right-hand side per thread
+  for (int q = threadIdx.x; q < r; q += blockDim.x) {
+    V* col = A + (int64_t)(c + q) * k;
+    for (int a = c - 1; a >= 0; --a) {
+      V s = col[a];
+      for (int w = a + 1; w < c; ++w) s = csub(s, cmul(A[a + (int64_t)w * k], col[w]));
+      const V d = A[a + (int64_t)a * k];
+      col[a] = cabs2(d) > 0 ? cdiv(s, d) : cmk<V>(0, 0);
+    }
+    // B(q, a) = conj(B^H(a, q))
+    for (int a = 0; a < c; ++a) out[boff[i] + q + (int64_t)a * r] = cconj(col[a]);
+  }
+}
+
+// ---- launchers ----------------------------------------------------------------------------
+void launch_sketch_fill(int dtype, void* Om, int64_t ld, int64_t rows, int64_t ncols, const int64_t* group, int64_t g0,
+                        int k, uint64_t seed, int level, int overlay, cudaStream_t st) {
+  const int64_t total = rows * ncols;
+  if (total == 0) return;
+  const int nsm = device_sm_count();
+  const int64_t want = (total + 255) / 256;
+  const unsigned grid = (unsigned)(want < 16LL * nsm ? want : 16LL * nsm);
+  if (dtype == BF_C128)
+    k_sketch_fill<double2><<<grid, 256, 0, st>>>(static_cast<double2*>(Om), ld, rows, ncols, group, g0, k, seed, level, overlay);
+  else
+    k_sketch_fill<float2><<<grid, 256, 0, st>>>(static_cast<float2*>(Om), ld, rows, ncols, group, g0, k, seed, level, overlay);
+}
+
+void launch_gather_t(int dtype, int64_t nmat, void* out, const void* Y, int64_t ldy, const int64_t* rows, const int64_t* moff,
+                     const int64_t* mcol, const int64_t* out_off, int k, int cj, cudaStream_t st) {
+  if (nmat == 0) return;
+  if (dtype == BF_C128)
+    k_gather_t<double2><<<(unsigned)nmat, 256, 0, st>>>(static_cast<double2*>(out), static_cast<const double2*>(Y), ldy,
+                                                         rows, moff, mcol, out_off, k, cj);
+  else
+    k_gather_t<float2><<<(unsigned)nmat, 256, 0, st>>>(static_cast<float2*>(out), static_cast<const float2*>(Y), ldy,
+                                                        rows, moff, mcol, out_off, k, cj);
+}
+
+void launch_batched_id(int dtype, int64_t nmat, void* M, const int64_t* moff, const int64_t* pcnt, int k, int pmax,
+                       double eps, int rmax, int32_t* rank, int32_t* perm, const int64_t* poff, cudaStream_t st) {
+  if (nmat == 0) return;
+  if (k > QR_MAXK) throw Err{BF_ERR_ARG, "sketch width above the batched ID's limit (1024)"};
+  const size_t cs = dtype == BF_C128 ? 16 : 8;
+  const size_t smem = cs * k + (cs / 2) * (size_t)(pmax > 0 ? pmax : 1);
+  static std::atomic<size_t> a128[BF_MAX_DEVICES], a64[BF_MAX_DEVICES];
+  if (dtype == BF_C128) {
+    ensure_smem_attr(a128, (const void*)k_batched_id<double2>, smem);
+    k_batched_id<double2><<<(unsigned)nmat, QR_THREADS, smem, st>>>(static_cast<double2*>(M), moff, pcnt, k, eps, rmax,
+                                                                    rank, perm, poff);
+  } else {
+    ensure_smem_attr(a64, (const void*)k_batched_id<float2>, smem);
+    k_batched_id<float2><<<(unsigned)nmat, QR_THREADS, smem, st>>>(static_cast<float2*>(M), moff, pcnt, k, eps, rmax,
+                                                                   rank, perm, poff);
+  }
+}
+
+void launch_batched_lsq(int dtype, int64_t nmat, void* work, const int64_t* woff, const void* S, const int64_t* zrow,
+                        const int32_t* cdim, const void* Ysk, int64_t ldy, const int64_t* yrows, const int64_t* yoff,
+                        const int64_t* ycol, int k, int maxcr, void* out, const int64_t* boff, cudaStream_t st) {
+  if (nmat == 0) return;
+  const size_t cs = dtype == BF_C128 ? 16 : 8;
+  const size_t smem = cs * k + (cs / 2) * (size_t)k + sizeof(int) * (size_t)(maxcr > 0 ? maxcr : 1);
+  static std::atomic<size_t> a128[BF_MAX_DEVICES], a64[BF_MAX_DEVICES];
+  if (dtype == BF_C128) {
+    ensure_smem_attr(a128, (const void*)k_batched_lsq<double2>, smem);
+    k_batched_lsq<double2><<<(unsigned)nmat, QR_THREADS, smem, st>>>(
+        static_cast<double2*>(work), woff, static_cast<const double2*>(S), zrow, cdim, static_cast<const double2*>(Ysk), ldy,
+        yrows, yoff, ycol, k, static_cast<double2*>(out), boff);
+  } else {
+    ensure_smem_attr(a64, (const void*)k_batched_lsq<float2>, smem);
+    k_batched_lsq<float2><<<(unsigned)nmat, QR_THREADS, smem, st>>>(
+        static_cast<float2*>(work), woff, static_cast<const float2*>(S), zrow, cdim, static_cast<const float2*>(Ysk), ldy,
+        yrows, yoff, ycol, k, static_cast<float2*>(out), boff);
+  }
+}
+
+}  // namespace bfa
