@@ -336,11 +336,21 @@ int bf_batched_id(int dtype, int64_t nmat, int32_t k, const int64_t* pcnt, void*
  * handle with op BF_OP_N or BF_OP_C, or the identity; rows x cols is its shape as it appears.
  * bf_operator_apply(ctx = const bf_operator*) has the bf_matvec_fn signature: Y = A X (op N) or
  * A^H X (op C) on device blocks; it allocates its temporaries and synchronises `stream`. */
-typedef enum { BF_FACTOR_BF = 0, BF_FACTOR_HODBF = 1, BF_FACTOR_IDENTITY = 2 } bf_factor_kind;
+typedef enum {
+  BF_FACTOR_BF = 0,              /* a butterfly handle, op N or C                                 */
+  BF_FACTOR_HODBF = 1,           /* an HOD-BF handle                                              */
+  BF_FACTOR_IDENTITY = 2,        /* I (rows == cols)                                              */
+  BF_FACTOR_BF_PLUS_I = 3,       /* I + K for a square butterfly handle K                         */
+  BF_FACTOR_SELECT = 4,          /* rows < cols: rows [aux0, aux0 + rows) of X; rows > cols: X     *
+                                  * embedded at rows [aux0, aux0 + cols) of a zero block          */
+  BF_FACTOR_HODBF_INV = 5,       /* A^{-1} of an HOD-BF inverse handle (user order)               */
+  BF_FACTOR_HODBF_INV_NODE = 6   /* D_tau^{-1} of node (l = aux0, tau = aux1), tree order          */
+} bf_factor_kind;
 typedef struct {
   int32_t kind, op;
-  void* handle;                  /* bf_handle / hodbf_handle; NULL for the identity              */
+  void* handle;                  /* bf_handle / hodbf_handle / hodbf_inv_handle; NULL otherwise   */
   int64_t rows, cols;
+  int64_t aux0, aux1;
 } bf_factor;
 typedef struct {
   double alpha_re, alpha_im;
@@ -355,6 +365,32 @@ typedef struct {
 } bf_operator;
 int bf_operator_apply(void* op, int opn, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
                       bf_stream_t stream);
+
+/* ---- HOD-BF inversion (Alg. 4 HODBF_invert with BF_SMW) -------------------------
+ * Builds A^{-1} of an HOD-BF matrix in the multiplicative form of Alg. 4 line 9: dense leaf inverses
+ * (line 3) and, for every internal node tau of T_H, a butterfly K_tau over T_tau x T_tau with
+ * (I + K_tau) = BF_SMW([I, B'_tau1; B'_tau2, I]) where B'_tau_i = BF_random_matvec(D_tau_i^{-1} B_tau_i)
+ * (lines 7-8).  BF_SMW follows Alg. 4 on the node's child split (readings in DESIGN.md section 3);
+ * nodes of at most dense_max rows are inverted densely (the low-rank / dense SMW base case).
+ * Every compression is bf_random_matvec with (eps, rank_max, oversample).  The descriptor is the
+ * hodbf_create one (host arrays, caller-owned).  Synchronous.  stats accumulates the constructions'
+ * sketch columns and ranks.  Errors: as bf_random_matvec; BF_ERR_ARG for a singular leaf. */
+typedef struct hodbf_inv_s* hodbf_inv_handle;
+typedef struct {
+  double eps;                    /* relative ID tolerance of every compression                     */
+  int32_t rank_max, oversample;
+  uint64_t seed;
+  int64_t dense_max;             /* nodes with at most this many rows: dense inverse (0: leaves only) */
+} bf_inv_opts;
+int hodbf_invert(const hodbf_desc* desc, const bf_inv_opts* opts, int device, bf_stream_t stream,
+                 hodbf_inv_handle* out, bf_rmv_stats* stats);
+int hodbf_inv_destroy(hodbf_inv_handle h);
+/* Y = A^{-1} X (op N) or A^{-H} X (op C); X, Y n x nrhs column-major DEVICE blocks in user order,
+ * non-overlapping.  Allocates its temporaries and synchronises `stream`. */
+int hodbf_inv_apply(hodbf_inv_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                    bf_stream_t stream);
+/* stored entries (dense leaf inverses + every K_tau's factors) and number of K_tau butterflies */
+int hodbf_inv_info(hodbf_inv_handle h, int64_t* factor_entries, int32_t* nbutterflies);
 
 const char* bf_status_string(int status);
 const char* bf_last_error(void);

@@ -16,7 +16,8 @@ import torch
 from .bfapply import (BF_C128, BF_C64, OPS, BFHandle, HODBFHandle, _check, _i64p, _np_dtype_code, _ptr,
                       _torch_dtype, lib)
 
-BF_FACTOR_BF, BF_FACTOR_HODBF, BF_FACTOR_IDENTITY = 0, 1, 2
+(BF_FACTOR_BF, BF_FACTOR_HODBF, BF_FACTOR_IDENTITY, BF_FACTOR_BF_PLUS_I, BF_FACTOR_SELECT, BF_FACTOR_HODBF_INV,
+ BF_FACTOR_HODBF_INV_NODE) = range(7)
 
 MATVEC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                         C.c_void_p)
@@ -37,7 +38,12 @@ class bf_rmv_stats(C.Structure):
 
 class bf_factor(C.Structure):
     _fields_ = [("kind", C.c_int32), ("op", C.c_int32), ("handle", C.c_void_p), ("rows", C.c_int64),
-                ("cols", C.c_int64)]
+                ("cols", C.c_int64), ("aux0", C.c_int64), ("aux1", C.c_int64)]
+
+
+class bf_inv_opts(C.Structure):
+    _fields_ = [("eps", C.c_double), ("rank_max", C.c_int32), ("oversample", C.c_int32), ("seed", C.c_uint64),
+                ("dense_max", C.c_int64)]
 
 
 class bf_product(C.Structure):
@@ -66,6 +72,16 @@ def _lib():
         L.bf_batched_id.restype = C.c_int
         L.bf_batched_id.argtypes = [C.c_int, C.c_int64, C.c_int32, C.POINTER(C.c_int64), C.c_void_p, C.c_double,
                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.hodbf_invert.restype = C.c_int
+        L.hodbf_invert.argtypes = [C.c_void_p, C.POINTER(bf_inv_opts), C.c_int, C.c_void_p, C.POINTER(C.c_void_p),
+                                   C.POINTER(bf_rmv_stats)]
+        L.hodbf_inv_destroy.restype = C.c_int
+        L.hodbf_inv_destroy.argtypes = [C.c_void_p]
+        L.hodbf_inv_apply.restype = C.c_int
+        L.hodbf_inv_apply.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                      C.c_void_p]
+        L.hodbf_inv_info.restype = C.c_int
+        L.hodbf_inv_info.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         L.bf_export.restype = C.c_int
         L.bf_export.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -79,7 +95,8 @@ Factor = Union[Tuple[object, str], Tuple[str, int]]
 class Operator:
     """A = sum_s alpha_s P_s with P_s = f_{q-1} ... f_0 (f_0 applied first), each placed at
     (row_off, col_off) inside the m x n operator.  A factor is (handle, "N" | "C") for a
-    BFHandle / HODBFHandle, or ("I", size).  Applied by the library (bf_operator_apply)."""
+    BFHandle / HODBFHandle / HODBFInverse, ("I", size) or ("I+", K) for I + K.  Applied by the
+    library (bf_operator_apply)."""
 
     def __init__(self, m: int, n: int, dtype, products: Sequence[Tuple[complex, Sequence[Factor], int, int]]):
         self.m, self.n = m, n
@@ -93,10 +110,16 @@ class Operator:
                 if f[0] == "I":
                     a.kind, a.op, a.handle, a.rows, a.cols = BF_FACTOR_IDENTITY, OPS["N"], None, f[1], f[1]
                     continue
+                if f[0] == "I+":  # ("I+", K): I + K for a square butterfly handle
+                    a.kind, a.op, a.handle, a.rows, a.cols = BF_FACTOR_BF_PLUS_I, OPS["N"], f[1].h, f[1].m, f[1].m
+                    self._keep.append(f[1])
+                    continue
                 h, op = f
                 self._keep.append(h)
                 if isinstance(h, HODBFHandle):
                     a.kind, rows, cols = BF_FACTOR_HODBF, h.n, h.n
+                elif isinstance(h, HODBFInverse):
+                    a.kind, rows, cols = BF_FACTOR_HODBF_INV, h.n, h.n
                 else:
                     a.kind, rows, cols = BF_FACTOR_BF, h.m, h.n
                 a.op, a.handle = OPS[op], h.h
@@ -278,3 +301,45 @@ def batched_id(mats: Sequence[torch.Tensor], eps: float, rmax: int):
         o += p * k
         po += p
     return out
+
+
+class HODBFInverse:
+    """A^{-1} of an HOD-BF matrix built by hodbf_invert (Alg. 4 HODBF_invert with BF_SMW,
+    P:569-615): dense leaf inverses and one butterfly per internal node, applied as their
+    product (include/bfapply.h)."""
+
+    def __init__(self, H, eps: float = 1e-10, rank_max: int = 64, oversample: int = 10, seed: int = 1,
+                 dense_max: int = 0, device: int = 0):
+        from .bfapply import _Keep, make_hodbf_desc
+        keep = _Keep()
+        d = make_hodbf_desc(H, keep)
+        code = d.dtype
+        o = bf_inv_opts(eps, rank_max, oversample, seed, dense_max)
+        h = C.c_void_p()
+        st = bf_rmv_stats()
+        cs = torch.cuda.current_stream(device)
+        _check("hodbf_invert", _lib().hodbf_invert(C.byref(d), C.byref(o), device, C.c_void_p(cs.cuda_stream),
+                                                     C.byref(h), C.byref(st)))
+        self.h, self.n, self.code, self.device = h, H.n, code, device
+        self.stats = {f: getattr(st, f) for f, _ in bf_rmv_stats._fields_}
+        fe, nb = C.c_int64(), C.c_int32()
+        _check("hodbf_inv_info", _lib().hodbf_inv_info(h, C.byref(fe), C.byref(nb)))
+        self.factor_entries, self.nbutterflies = fe.value, nb.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().hodbf_inv_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def apply(self, X: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Y = A^{-1} X (op N) or A^{-H} X (op C); X (nrhs, n) on the device."""
+        assert X.is_cuda and X.dim() == 2 and X.shape[1] == self.n and X.stride(1) == 1
+        if out is None:
+            out = torch.empty((X.shape[0], self.n), dtype=X.dtype, device=X.device)
+        st = torch.cuda.current_stream()
+        _check("hodbf_inv_apply", _lib().hodbf_inv_apply(self.h, OPS[op], X.shape[0], C.c_void_p(X.data_ptr()),
+                                                          max(X.stride(0), self.n, 1), C.c_void_p(out.data_ptr()),
+                                                          max(out.stride(0), self.n, 1), C.c_void_p(st.cuda_stream)))
+        return out

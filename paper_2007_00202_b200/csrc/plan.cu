@@ -2686,3 +2686,4 @@ int bf_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t 
 }  // extern "C"
 
 #include "rmatvec_host.inc"
+#include "hinv_host.inc"

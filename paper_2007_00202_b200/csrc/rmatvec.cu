@@ -374,3 +374,185 @@ void launch_batched_lsq(int dtype, int64_t nmat, void* work, const int64_t* woff
 }
 
 }  // namespace bfa
+
+namespace bfa {
+
+// In-place inverse of every square matrix (n_i x n_i, column-major, ld n_i) packed in M
+// (Gauss-Jordan elimination with partial pivoting, one CTA per matrix): the dense leaf inverses
+// of Alg. 4 line 3 ("Directly compute D_tau^{-1}") and the L = 0 base case of BF_SMW.
+// info[i] = 0, or j + 1 when pivot column j was exactly singular.
+template <typename V>
+__global__ void __launch_bounds__(QR_THREADS) k_batched_inv(V* __restrict__ M, const int64_t* __restrict__ moff,
+                                                              const int64_t* __restrict__ dim, int32_t* __restrict__ info) {
+  using T = typename Real<V>::T;
+  extern __shared__ __align__(16) unsigned char sm[];
+  int* piv = reinterpret_cast<int*>(sm);  // n: row order
+  __shared__ int s_p, s_bad;
+  const int64_t i = blockIdx.x;
+  const int n = (int)dim[i];
+  V* A = M + moff[i];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_bad = 0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) piv[r] = r;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (warp == 0) {  // partial pivot: largest |A(r, j)|, r >= j (lowest index on ties)
+      T best = -1;
+      int bi = j;
+      for (int r = j + lane; r < n; r += 32) {
+        const T a = cabs2(A[r + (int64_t)j * n]);
+        if (a > best) {
+          best = a;
+          bi = r;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const T ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        if (!(best > 0) && s_bad == 0) s_bad = j + 1;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != j) {  // swap rows j and p (all columns)
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        const V t = A[j + (int64_t)c * n];
+        A[j + (int64_t)c * n] = A[p + (int64_t)c * n];
+        A[p + (int64_t)c * n] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = piv[j];
+        piv[j] = piv[p];
+        piv[p] = t;
+      }
+    }
+    __syncthreads();
+    const V d = A[j + (int64_t)j * n];
+    const V dinv = cabs2(d) > 0 ? cdiv(cmk<V>(1, 0), d) : cmk<V>(0, 0);
+    __syncthreads();
+    // scale row j: A(j, c) *= 1/d for c != j; A(j, j) = 1/d
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      if (c == j)
+        A[j + (int64_t)c * n] = dinv;
+      else
+        A[j + (int64_t)c * n] = cmul(A[j + (int64_t)c * n], dinv);
+    }
+    __syncthreads();
+    // eliminate column j from every other row: A(r, c) -= A(r, j) A(j, c); A(r, j) = -A(r, j) / d
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int c = e / n, r = e - c * n;
+      if (r == j || c == j) continue;
+      A[r + (int64_t)c * n] = csub(A[r + (int64_t)c * n], cmul(A[r + (int64_t)j * n], A[j + (int64_t)c * n]));
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < n; r += blockDim.x)
+      if (r != j) A[r + (int64_t)j * n] = cmul(cmk<V>(-A[r + (int64_t)j * n].x, -A[r + (int64_t)j * n].y), dinv);
+    __syncthreads();
+  }
+  // A now holds inv(P A_orig) = inv(A_orig) P^T, P the accumulated row interchanges (row j of P A
+  // is row piv[j] of A): permute the columns back, inv(A_orig)(:, piv[c]) = A(:, c)
+  V* tmp = reinterpret_cast<V*>(sm + ((sizeof(int) * (size_t)n + 15) & ~size_t(15)));
+  for (int r = 0; r < n; ++r) {
+    for (int c = threadIdx.x; c < n; c += blockDim.x) tmp[piv[c]] = A[r + (int64_t)c * n];
+    __syncthreads();
+    for (int c = threadIdx.x; c < n; c += blockDim.x) A[r + (int64_t)c * n] = tmp[c];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) info[i] = s_bad;
+}
+
+void launch_batched_inv(int dtype, int64_t nmat, void* M, const int64_t* moff, const int64_t* dim, int nmax,
+                        int32_t* info, cudaStream_t st) {
+  if (nmat == 0) return;
+  const size_t cs = dtype == BF_C128 ? 16 : 8;
+  const size_t smem = ((sizeof(int) * (size_t)nmax + 15) & ~size_t(15)) + cs * (size_t)nmax;
+  static std::atomic<size_t> a128[BF_MAX_DEVICES], a64[BF_MAX_DEVICES];
+  if (dtype == BF_C128) {
+    ensure_smem_attr(a128, (const void*)k_batched_inv<double2>, smem);
+    k_batched_inv<double2><<<(unsigned)nmat, QR_THREADS, smem, st>>>(static_cast<double2*>(M), moff, dim, info);
+  } else {
+    ensure_smem_attr(a64, (const void*)k_batched_inv<float2>, smem);
+    k_batched_inv<float2><<<(unsigned)nmat, QR_THREADS, smem, st>>>(static_cast<float2*>(M), moff, dim, info);
+  }
+}
+
+}  // namespace bfa
+
+namespace bfa {
+
+// Y(leaf rows) = D_t X(leaf rows) (op N) or D_t^H X (op C) for the leaves t of one node: the dense
+// leaf-inverse factor of the HOD-BF inverse.  lp points at the node's first leaf offset (absolute
+// tree positions; r0 = the node's first row), D_t column-major at D + doff[t].  Grid: (leaf,
+// 8-column group).
+template <typename V>
+__global__ void k_blockdiag(const int64_t* __restrict__ lp, int64_t r0, const V* __restrict__ D,
+                            const int64_t* __restrict__ doff, int op, int64_t nrhs, const V* __restrict__ X, int64_t ldx,
+                            V* __restrict__ Y, int64_t ldy) {
+  const int64_t t = blockIdx.x, j0 = (int64_t)blockIdx.y * 8;
+  const int64_t a = lp[t] - r0, s = lp[t + 1] - lp[t];
+  const V* Dt = D + doff[t];
+  const int nj = (int)min((int64_t)8, nrhs - j0);
+  for (int64_t e = threadIdx.x; e < s * nj; e += blockDim.x) {
+    const int64_t jj = e / s, r = e - jj * s, j = j0 + jj;
+    V acc = cmk<V>(0, 0);
+    if (op == BF_OP_N) {
+      for (int64_t k = 0; k < s; ++k) acc = cadd(acc, cmul(Dt[r + k * s], X[a + k + j * ldx]));
+    } else {
+      for (int64_t k = 0; k < s; ++k) acc = cadd(acc, cmulc(Dt[k + r * s], X[a + k + j * ldx]));
+    }
+    Y[a + r + j * ldy] = acc;
+  }
+}
+
+void launch_blockdiag(int dtype, int64_t nleaf, const int64_t* lp, int64_t r0, const void* D, const int64_t* doff, int op,
+                      int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy, int lmax, cudaStream_t st) {
+  if (nleaf == 0 || nrhs == 0) return;
+  (void)lmax;
+  dim3 grid((unsigned)nleaf, (unsigned)((nrhs + 7) / 8));
+  if (dtype == BF_C128)
+    k_blockdiag<double2><<<grid, 256, 0, st>>>(lp, r0, static_cast<const double2*>(D), doff, op, nrhs,
+                                               static_cast<const double2*>(X), ldx, static_cast<double2*>(Y), ldy);
+  else
+    k_blockdiag<float2><<<grid, 256, 0, st>>>(lp, r0, static_cast<const float2*>(D), doff, op, nrhs,
+                                              static_cast<const float2*>(X), ldx, static_cast<float2*>(Y), ldy);
+}
+
+// gather (scatter = 0): Y[i] = X[perm[i]]; scatter (1): Y[perm[i]] = X[i]; perm NULL = identity
+template <typename V>
+__global__ void k_permute_rows(int64_t rows, int64_t nrhs, const int64_t* __restrict__ perm, int scatter,
+                               const V* __restrict__ X, int64_t ldx, V* __restrict__ Y, int64_t ldy) {
+  const int64_t total = rows * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    const int64_t p = perm ? perm[i] : i;
+    if (scatter)
+      Y[p + j * ldy] = X[i + j * ldx];
+    else
+      Y[i + j * ldy] = X[p + j * ldx];
+  }
+}
+
+void launch_permute_rows(int dtype, int64_t rows, int64_t nrhs, const int64_t* perm, int scatter, const void* X,
+                         int64_t ldx, void* Y, int64_t ldy, cudaStream_t st) {
+  const int64_t total = rows * nrhs;
+  if (total == 0) return;
+  const int nsm = device_sm_count();
+  const int64_t want = (total + 255) / 256;
+  const unsigned grid = (unsigned)(want < 8LL * nsm ? want : 8LL * nsm);
+  if (dtype == BF_C128)
+    k_permute_rows<double2><<<grid, 256, 0, st>>>(rows, nrhs, perm, scatter, static_cast<const double2*>(X), ldx,
+                                                  static_cast<double2*>(Y), ldy);
+  else
+    k_permute_rows<float2><<<grid, 256, 0, st>>>(rows, nrhs, perm, scatter, static_cast<const float2*>(X), ldx,
+                                                 static_cast<float2*>(Y), ldy);
+}
+
+}  // namespace bfa
