@@ -386,11 +386,39 @@ int hodbf_invert(const hodbf_desc* desc, const bf_inv_opts* opts, int device, bf
                  hodbf_inv_handle* out, bf_rmv_stats* stats);
 int hodbf_inv_destroy(hodbf_inv_handle h);
 /* Y = A^{-1} X (op N) or A^{-H} X (op C); X, Y n x nrhs column-major DEVICE blocks in user order,
- * non-overlapping.  Allocates its temporaries and synchronises `stream`. */
+ * non-overlapping; work: hodbf_inv_workspace_size bytes of device memory.  Asynchronous on
+ * `stream` (the product of the inverse's factors: one blocked dense-leaf launch and the node
+ * butterflies' applies, level by level). */
+int hodbf_inv_workspace_size(hodbf_inv_handle h, int64_t nrhs, size_t* bytes);
 int hodbf_inv_apply(hodbf_inv_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                    bf_stream_t stream);
+                    void* work, size_t work_bytes, bf_stream_t stream);
 /* stored entries (dense leaf inverses + every K_tau's factors) and number of K_tau butterflies */
 int hodbf_inv_info(hodbf_inv_handle h, int64_t* factor_entries, int32_t* nbutterflies);
+
+/* ---- multifrontal solve-phase sweep (Alg. 1 line precGMRES) ---------------------------
+ * An assembly tree of compressed fronts: front i has separator unknowns [s_off, s_off + s_len) of
+ * the global N-vector (disjoint ranges), update unknowns u_idx (u_len distinct global indices held
+ * by its ancestors), F11^{-1} as an HOD-BF inverse (s x s, its own user order = the separator's local
+ * order), and F12 (s x u) / F21 (u x s) as butterflies.  Fronts are listed in topological order:
+ * every front before its parent.  The handles are BORROWED: they must outlive the bf_mf handle.
+ *   forward (children first): z_s = F11^{-1} y_s; y_u -= F21 z_s   (y starts as B)
+ *   backward (root first):    x_s = z_s - F11^{-1} F12 x_u
+ * bf_mf_solve writes X = M^{-1} B (N x nrhs, column-major DEVICE blocks, non-overlapping) with a
+ * workspace of bf_mf_workspace_size bytes; asynchronous on `stream`, no allocation. */
+typedef struct bf_mf_s* bf_mf_handle;
+typedef struct {
+  int32_t parent, reserved;      /* parent front (-1: a root)                                      */
+  int64_t s_off, s_len;
+  int64_t u_len;
+  const int64_t* u_idx;          /* host array, copied at create                                   */
+  hodbf_inv_handle F11inv;
+  bf_handle F12, F21;
+} bf_front;
+int bf_mf_create(int dtype, int64_t N, int32_t nfront, const bf_front* fronts, int device, bf_mf_handle* out);
+int bf_mf_destroy(bf_mf_handle h);
+int bf_mf_workspace_size(bf_mf_handle h, int64_t nrhs, size_t* bytes);
+int bf_mf_solve(bf_mf_handle h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx, void* work,
+                size_t work_bytes, bf_stream_t stream);
 
 const char* bf_status_string(int status);
 const char* bf_last_error(void);

@@ -79,7 +79,9 @@ def _lib():
         L.hodbf_inv_destroy.argtypes = [C.c_void_p]
         L.hodbf_inv_apply.restype = C.c_int
         L.hodbf_inv_apply.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
-                                      C.c_void_p]
+                                      C.c_void_p, C.c_size_t, C.c_void_p]
+        L.hodbf_inv_workspace_size.restype = C.c_int
+        L.hodbf_inv_workspace_size.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_size_t)]
         L.hodbf_inv_info.restype = C.c_int
         L.hodbf_inv_info.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         L.bf_export.restype = C.c_int
@@ -339,7 +341,81 @@ class HODBFInverse:
         if out is None:
             out = torch.empty((X.shape[0], self.n), dtype=X.dtype, device=X.device)
         st = torch.cuda.current_stream()
+        ws = C.c_size_t()
+        _check("hodbf_inv_workspace_size", _lib().hodbf_inv_workspace_size(self.h, X.shape[0], C.byref(ws)))
+        work = torch.empty(max(ws.value, 1), dtype=torch.uint8, device=X.device)
         _check("hodbf_inv_apply", _lib().hodbf_inv_apply(self.h, OPS[op], X.shape[0], C.c_void_p(X.data_ptr()),
                                                           max(X.stride(0), self.n, 1), C.c_void_p(out.data_ptr()),
-                                                          max(out.stride(0), self.n, 1), C.c_void_p(st.cuda_stream)))
+                                                          max(out.stride(0), self.n, 1), C.c_void_p(work.data_ptr()),
+                                                          work.numel(), C.c_void_p(st.cuda_stream)))
+        return out
+
+
+class bf_front(C.Structure):
+    _fields_ = [("parent", C.c_int32), ("reserved", C.c_int32), ("s_off", C.c_int64), ("s_len", C.c_int64),
+                ("u_len", C.c_int64), ("u_idx", C.POINTER(C.c_int64)), ("F11inv", C.c_void_p), ("F12", C.c_void_p),
+                ("F21", C.c_void_p)]
+
+
+class MFSolver:
+    """The multifrontal solve-phase sweep (bf_mf_solve) over an assembly tree of fronts
+    (bfinputs.fronts.Front: F11 HOD-BF, F12 / F21 butterflies, separator range, update indices).
+    Builds every F11^{-1} with hodbf_invert (Alg. 4) and uploads F12 / F21."""
+
+    def __init__(self, fronts, N: int, eps: float = 1e-10, rank_max: int = 64, dense_max: int = 0, device: int = 0):
+        L = _lib()
+        for name, args in (("bf_mf_create", [C.c_int, C.c_int64, C.c_int32, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+                           ("bf_mf_destroy", [C.c_void_p]),
+                           ("bf_mf_workspace_size", [C.c_void_p, C.c_int64, C.POINTER(C.c_size_t)]),
+                           ("bf_mf_solve", [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                            C.c_void_p, C.c_size_t, C.c_void_p])):
+            getattr(L, name).restype = C.c_int
+            getattr(L, name).argtypes = args
+        self.N, self.device = N, device
+        self.inv, self.bfs, keep = [], [], []
+        arr = (bf_front * len(fronts))()
+        code = _np_dtype_code(fronts[0].F11.dtype)
+        for k, f in enumerate(fronts):
+            inv = HODBFInverse(f.F11, eps=eps, rank_max=rank_max, dense_max=dense_max, device=device)
+            self.inv.append(inv)
+            a = arr[k]
+            a.parent, a.s_off, a.s_len = f.parent, f.s_off, f.s_len
+            u = np.ascontiguousarray(f.u_idx, dtype=np.int64)
+            keep.append(u)
+            a.u_len = len(u)
+            a.u_idx = u.ctypes.data_as(C.POINTER(C.c_int64)) if len(u) else None
+            a.F11inv = inv.h
+            if len(u):
+                h12, h21 = BFHandle(f.F12, device), BFHandle(f.F21, device)
+                self.bfs += [h12, h21]
+                a.F12, a.F21 = h12.h, h21.h
+        h = C.c_void_p()
+        _check("bf_mf_create", L.bf_mf_create(code, N, len(fronts), C.cast(arr, C.c_void_p), device, C.byref(h)))
+        self.h, self.code = h, code
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().bf_mf_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def workspace_size(self, nrhs: int) -> int:
+        s = C.c_size_t()
+        _check("bf_mf_workspace_size", _lib().bf_mf_workspace_size(self.h, nrhs, C.byref(s)))
+        return s.value
+
+    def solve(self, B: torch.Tensor, out: Optional[torch.Tensor] = None, work: Optional[torch.Tensor] = None):
+        """X = M^{-1} B; B (nrhs, N) on the device."""
+        assert B.is_cuda and B.dim() == 2 and B.shape[1] == self.N and B.stride(1) == 1
+        nrhs = B.shape[0]
+        if out is None:
+            out = torch.empty_like(B)
+        if work is None:
+            work = torch.empty(max(self.workspace_size(nrhs), 1), dtype=torch.uint8, device=B.device)
+        st = torch.cuda.current_stream()
+        _check("bf_mf_solve", _lib().bf_mf_solve(self.h, nrhs, C.c_void_p(B.data_ptr()), max(B.stride(0), self.N, 1),
+                                                 C.c_void_p(out.data_ptr()), max(out.stride(0), self.N, 1),
+                                                 C.c_void_p(work.data_ptr()), work.numel(),
+                                                 C.c_void_p(st.cuda_stream)))
         return out

@@ -2687,3 +2687,4 @@ int bf_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t 
 
 #include "rmatvec_host.inc"
 #include "hinv_host.inc"
+#include "mf_host.inc"

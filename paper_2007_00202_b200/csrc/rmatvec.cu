@@ -556,3 +556,43 @@ void launch_permute_rows(int dtype, int64_t rows, int64_t nrhs, const int64_t* p
 }
 
 }  // namespace bfa
+
+namespace bfa {
+
+// rows[i] of an index list: gather Y[i] = X[idx[i]] (add = 0) or scatter-add Y[idx[i]] += alpha X[i]
+// (add = 1; the indices of one call are distinct, so no two threads update the same row): the
+// extend-add moves of the multifrontal solve sweep
+template <typename V>
+__global__ void k_index_rows(int64_t rows, int64_t nrhs, const int64_t* __restrict__ idx, int add, double are,
+                             double aim, const V* __restrict__ X, int64_t ldx, V* __restrict__ Y, int64_t ldy) {
+  const int64_t total = rows * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    if (add) {
+      const V a = X[i + j * ldx];
+      V y = Y[idx[i] + j * ldy];
+      y.x += (are * a.x - aim * a.y);
+      y.y += (are * a.y + aim * a.x);
+      Y[idx[i] + j * ldy] = y;
+    } else {
+      Y[i + j * ldy] = X[idx[i] + j * ldx];
+    }
+  }
+}
+
+void launch_index_rows(int dtype, int64_t rows, int64_t nrhs, const int64_t* idx, int add, double are, double aim,
+                       const void* X, int64_t ldx, void* Y, int64_t ldy, cudaStream_t st) {
+  const int64_t total = rows * nrhs;
+  if (total == 0) return;
+  const int nsm = device_sm_count();
+  const int64_t want = (total + 255) / 256;
+  const unsigned grid = (unsigned)(want < 8LL * nsm ? want : 8LL * nsm);
+  if (dtype == BF_C128)
+    k_index_rows<double2><<<grid, 256, 0, st>>>(rows, nrhs, idx, add, are, aim, static_cast<const double2*>(X), ldx,
+                                                static_cast<double2*>(Y), ldy);
+  else
+    k_index_rows<float2><<<grid, 256, 0, st>>>(rows, nrhs, idx, add, are, aim, static_cast<const float2*>(X), ldx,
+                                               static_cast<float2*>(Y), ldy);
+}
+
+}  // namespace bfa
