@@ -205,6 +205,276 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Persistent, transposed-orientation gather-sum (complex128; SURVEY 7.3 hard part 2, VERDICT r1
+// item 3):   out^T (nrhs x m) = sum_t In_t^T (nrhs x k) A_t^T (k x m)
+// * M of the MMA is the right-hand sides (a multiple of 8) and N the task's output rows, padded
+//   only to 8 (runtime n-tile count) instead of to the 32-row tile: the ragged small ranks of the
+//   kernel-compressed butterflies and HOD-BF (configs 2-4, ranks ~6-70) waste far fewer DMMAs.
+// * Persistent: a grid of 2 CTAs per SM walks the round's items (unit = (task, 32-row block)) x
+//   64-column tile) with a cp.async ring of NST K-chunks whose loader runs NST - 1 chunks ahead
+//   ACROSS item boundaries, so the first loads of the next item overlap the current item's MMAs
+//   and epilogue (the one-item-per-CTA version paid a full load latency per item: each item is
+//   only ~2-5 chunks of 16).
+// Warp w owns the 8 columns 8w.. of the item's tile and every 8-row n-tile holding task rows:
+//   A frag (8 x 4, [nrhs][k]) of lane (g, t) = In(k0 + t, 8w + g)
+//   B frag (4 x 8, [k][row])  of lane (g, t) = A(8 nt + g, k0 + t)
+//   C (8 x 8)  c[g][2t + e]   = out(row 8 nt + 2t + e, column 8w + g)
+// ------------------------------------------------------------------------------------
+template <bool M3, int NST>
+__global__ void __launch_bounds__(256, 2) k_stage_tileT(StageArgs a) {
+  using E = double2;
+  using C = TileCfg<PolC128<2>>;
+  constexpr int TR = C::TR, TC = C::TC, KC = C::KC, SA = C::SA, SB = C::SB, STAGE = C::STAGE;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  E* sm = reinterpret_cast<E*>(sm_raw);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ctiles = (a.nrhs + TC - 1) / TC;
+  const int64_t nitems = (int64_t)a.nunits * ctiles;
+  const E* __restrict__ pool = static_cast<const E*>(a.pool);
+  const E* __restrict__ S = static_cast<const E*>(a.S);
+  const E* __restrict__ X = static_cast<const E*>(a.X);
+  pdl_wait();  // slabs / X / Y of the previous rounds
+  // ---- loader: its own walk over (item, term, K chunk), NST - 1 chunks ahead of the consumer
+  int64_t l_item = blockIdx.x;
+  int l_q = 0, l_kc = 0;
+  Task l_tk{};
+  int l_r0 = 0, l_j0 = 0;
+  auto l_fetch = [&]() {  // task of l_item; skips items without terms (they consume no chunk)
+    for (; l_item < nitems; l_item += gridDim.x) {
+      const int2 un = a.units[l_item / ctiles];
+      l_tk = a.tasks[un.x];
+      l_r0 = un.y * TR;
+      l_j0 = (int)(l_item % ctiles) * TC;
+      bool skip = l_tk.nterm == 0;
+      if (!skip && a.cols) {
+        const int2 cr = a.cols[un.x];
+        skip = l_j0 >= cr.y || l_j0 + TC <= cr.x;
+      }
+      if (!skip) return;
+    }
+  };
+  l_fetch();
+  auto load = [&](int stg) {
+    if (l_item >= nitems) return;
+    const Term tm = a.terms[l_tk.term0 + l_q];
+    E* sA = sm + stg * STAGE;
+    E* sB = sA + KC * SA;
+#pragma unroll
+    for (int e = 0; e < TR * KC / 256; ++e) {
+      const int x = tid + 256 * e;
+      int i, k;
+      if (tm.a_rs == 1) {
+        i = x % TR;
+        k = x / TR;
+      } else {
+        k = x % KC;
+        i = x / KC;
+      }
+      const bool ok = l_r0 + i < l_tk.m && l_kc + k < tm.k;
+      const E* src = pool + (ok ? tm.a_off + (int64_t)(l_r0 + i) * tm.a_rs + (int64_t)(l_kc + k) * tm.a_cs : 0);
+      cp_async_el(sA + k * SA + i, src, ok, 16);
+    }
+#pragma unroll
+    for (int e = 0; e < KC * TC / 256; ++e) {
+      const int x = tid + 256 * e;
+      int k, j;
+      if (tm.in_kind == 0) {
+        j = x % TC;
+        k = x / TC;
+      } else {
+        k = x % KC;
+        j = x / KC;
+      }
+      const bool ok = l_kc + k < tm.k && l_j0 + j < a.nrhs;
+      const E* src = S;
+      if (ok) {
+        const int64_t p = tm.in_row + l_kc + k;
+        src = tm.in_kind == 0 ? S + p * a.ldS + l_j0 + j : X + (a.xperm ? a.xperm[p] : p) + (int64_t)(l_j0 + j) * a.ldx;
+      }
+      cp_async_el(sB + k * SB + j, src, ok, 16);
+    }
+    l_kc += KC;
+    if (l_kc >= tm.k) {
+      l_kc = 0;
+      if (++l_q >= l_tk.nterm) {
+        l_q = 0;
+        l_item += gridDim.x;
+        l_fetch();
+      }
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < NST - 1; ++st) {
+    load(st);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  const int cw = 8 * w;
+  int c = 0;  // consumed chunks
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int2 un = a.units[item / ctiles];
+    const Task tk = a.tasks[un.x];
+    const int r0 = un.y * TR, j0 = (int)(item % ctiles) * TC;
+    if (a.cols) {
+      const int2 cr = a.cols[un.x];
+      if (j0 >= cr.y || j0 + TC <= cr.x) continue;  // bf_extract: column tile outside the task's range
+    }
+    const int ntiles = min(4, (tk.m - r0 + 7) >> 3);  // 8-row n-tiles holding task rows
+    double acc[3][4][2];
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) acc[q][nt][0] = acc[q][nt][1] = 0.0;
+    for (int q = 0; q < tk.nterm; ++q) {
+      const Term tm = a.terms[tk.term0 + q];
+      const bool cj = (tm.conj != 0) != (a.conj_flip != 0);
+      for (int kc = 0; kc < tm.k; kc += KC, ++c) {
+        load((c + NST - 1) % NST);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(NST - 1) : "memory");
+        __syncthreads();
+        const E* sA = sm + (c % NST) * STAGE;
+        const E* sB = sA + KC * SA;
+#pragma unroll
+        for (int k0 = 0; k0 < KC; k0 += 4) {
+          const E x = sB[(k0 + t) * SB + cw + g];  // In^T fragment
+          const double xs = x.x + x.y;
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (nt < ntiles) {
+              E f = sA[(k0 + t) * SA + 8 * nt + g];  // A^T fragment
+              f.y = conj_im(f.y, cj);
+              if (M3) {
+                PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], x.x, f.x);
+                PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.y, f.y);
+                PolC128<1>::mma(acc[2][nt][0], acc[2][nt][1], xs, f.x + f.y);
+              } else {  // 4M: re += xr fr - xi fi, im += xr fi + xi fr (exact on selection factors)
+                PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], x.x, f.x);
+                PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], -x.y, f.y);
+                PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.x, f.y);
+                PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.y, f.x);
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const int col = j0 + cw + g;
+    if (col < a.nrhs) {
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        if (nt >= ntiles) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = r0 + 8 * nt + 2 * t + e;
+          if (r >= tk.m) continue;
+          E v;
+          if (M3) {
+            const double p1 = acc[0][nt][e], p2 = acc[1][nt][e], p3 = acc[2][nt][e];
+            v = make_double2(p1 - p2, p3 - p1 - p2);
+          } else {
+            v = make_double2(acc[0][nt][e], acc[1][nt][e]);
+          }
+          if (a.out_kind == 0) {
+            static_cast<E*>(a.S)[(tk.out_row + r) * a.ldS + col] = v;
+          } else {
+            const int64_t p = tk.out_row + r;
+            static_cast<E*>(a.Y)[(a.yperm ? a.yperm[p] : p) + (int64_t)col * a.ldy] = v;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  pdl_trigger();
+}
+
+template <bool M3, int NST>
+static void launch_tileT_t(const StageArgs& a, cudaStream_t st) {
+  using C = TileCfg<PolC128<2>>;
+  constexpr size_t smem = NST * C::STAGE * sizeof(double2);
+  static std::atomic<size_t> attr[BF_MAX_DEVICES];
+  ensure_smem_attr(attr, (const void*)k_stage_tileT<M3, NST>, smem);
+  // one item per CTA: measured faster than a persistent grid of 2 CTAs per SM walking the items
+  // with the loader running ahead across them (config 3: 1.48 vs 1.67 ms) -- the hardware
+  // scheduler balances the uneven items (ragged ranks and K) better than a static stride
+  const int64_t items = (int64_t)a.nunits * ((a.nrhs + C::TC - 1) / C::TC);
+  launch_pdl(k_stage_tileT<M3, NST>, (unsigned)items, 1u, 256, smem, st, a);
+}
+
+// ------------------------------------------------------------------------------------
+// Narrow right-hand-side blocks (nrhs <= 4, the solve regime of P:697): the round's products
+// are matrix-vector products, bound by reading the factor entries once.  CUDA-core FMAs, one
+// warp per unit (task, 32-row block), lane = output row, persistent grid-stride over units;
+// per k the lanes read one factor column (coalesced for op N, a_rs = 1) and broadcast-read the
+// k-th input row.
+// ------------------------------------------------------------------------------------
+template <typename V, int NR>
+__global__ void __launch_bounds__(256) k_stage_gemv(StageArgs a) {
+  using T = decltype(V{}.x);
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const V* __restrict__ pool = static_cast<const V*>(a.pool);
+  const V* __restrict__ S = static_cast<const V*>(a.S);
+  const V* __restrict__ X = static_cast<const V*>(a.X);
+  pdl_wait();
+  for (int64_t u = wid; u < a.nunits; u += nw) {
+    const int2 un = a.units[u];
+    const Task tk = a.tasks[un.x];
+    const int r = un.y * 32 + lane;
+    const bool act = r < tk.m;
+    T re[NR], im[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) re[j] = im[j] = 0;
+    for (int q = 0; q < tk.nterm; ++q) {
+      const Term tm = a.terms[tk.term0 + q];
+      const bool cj = (tm.conj != 0) != (a.conj_flip != 0);
+      const V* Ar = pool + tm.a_off + (int64_t)(act ? r : 0) * tm.a_rs;
+#pragma unroll 4
+      for (int k = 0; k < tm.k; ++k) {
+        V f = act ? __ldg(Ar + (int64_t)k * tm.a_cs) : V{};
+        f.y = conj_im(f.y, cj);
+        const int64_t p = tm.in_row + k;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          V x = V{};
+          if (j < a.nrhs) x = tm.in_kind == 0 ? S[p * a.ldS + j] : X[(a.xperm ? a.xperm[p] : p) + (int64_t)j * a.ldx];
+          re[j] = fma(f.x, x.x, re[j]);
+          re[j] = fma(-f.y, x.y, re[j]);
+          im[j] = fma(f.x, x.y, im[j]);
+          im[j] = fma(f.y, x.x, im[j]);
+        }
+      }
+    }
+    if (!act) continue;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      if (j >= a.nrhs) break;
+      V v;
+      v.x = re[j];
+      v.y = im[j];
+      if (a.out_kind == 0) {
+        static_cast<V*>(a.S)[(tk.out_row + r) * a.ldS + j] = v;
+      } else {
+        const int64_t p = tk.out_row + r;
+        static_cast<V*>(a.Y)[(a.yperm ? a.yperm[p] : p) + (int64_t)j * a.ldy] = v;
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+template <typename V, int NR>
+static void launch_gemv_t(const StageArgs& a, cudaStream_t st) {
+  const int64_t warps = a.nunits;
+  const int64_t cap = 16LL * device_sm_count() * 8;  // 16 CTAs of 8 warps per SM
+  const int64_t w = warps < cap ? warps : cap;
+  launch_pdl(k_stage_gemv<V, NR>, (unsigned)((w + 7) / 8), 1u, 256, 0, st, a);
+}
+
 template <class Pol, bool M3>
 static void launch_tile_t(dim3 grid, const StageArgs& a, cudaStream_t st) {
   constexpr size_t smem = TileCfg<Pol>::NST * TileCfg<Pol>::STAGE * sizeof(typename Pol::E);
@@ -227,6 +497,28 @@ static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
   a.out_kind = r.out_kind;
   a.cols = r.cols;
   dim3 grid(r.nunits, (a.nrhs + 63) / 64);  // CTA tile: 32 rows x 64 columns
+  // kernel choice: nrhs <= 4 -> matrix-vector kernel; complex128 with nrhs > 8 -> the persistent
+  // transposed-orientation kernel; otherwise the row-tile kernel.  (env BF_TILE = 0 forces the
+  // row-tile kernel everywhere, for A/B measurements)
+  // (the matrix-vector kernel k_stage_gemv measured 3.3x slower than the tile kernels on the
+  // nrhs = 1 solve sweep -- one warp per small task leaves most lanes idle -- and is only
+  // selected by BF_TILE = 2, for measurements)
+  static const int mode = getenv("BF_TILE") ? atoi(getenv("BF_TILE")) : 1;
+  if (mode == 2 && a.nrhs <= 4 && !a.cols) {
+    if (a.nrhs == 1) launch_gemv_t<V, 1>(a, st);
+    else if (a.nrhs == 2) launch_gemv_t<V, 2>(a, st);
+    else launch_gemv_t<V, 4>(a, st);
+    return;
+  }
+  // rounds into the slab space (leaf V, W, centre and R stages: ranks as output rows) run
+  // transposed; the rounds that write user rows (leaf U blocks, HOD-BF diagonal blocks: leaf-size
+  // outputs) keep the row tiles (config 3: 1.48 ms all-transposed, 1.58 row tiles; the last round
+  // 0.279 vs 0.259 ms)
+  if (mode && sizeof(V) == 16 && a.nrhs > 8 && r.out_kind == 0) {
+    if (a.m3) launch_tileT_t<true, 2>(a, st);
+    else launch_tileT_t<false, 2>(a, st);
+    return;
+  }
   if (sizeof(V) == 16)
     launch_tile<PolC128<2>>(grid, a, st);
   else
