@@ -20,7 +20,8 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbfapply.so")
+# BF_LIB: an alternative build of the same library (A/B measurements of compile-time variants)
+LIB_PATH = os.environ.get("BF_LIB") or os.path.join(_PKG, "libbfapply.so")
 
 BF_C64, BF_C128 = 1, 2
 OPS = {"N": 0, "T": 1, "C": 2}

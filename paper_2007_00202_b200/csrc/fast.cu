@@ -23,15 +23,21 @@
 
 namespace bfa {
 
-template <class Pol, int D>
+template <class Pol, int D, int HV = 2>
 struct PassCfg {
   using E = typename Pol::E;
   static constexpr int WINH = (1 << (D > 3 ? D : 3)) * FAST_HSLAB;  // half window (elements)
-  static constexpr int WIN = 2 * WINH;                        // window buffer: [half][slot][16 x 16]
+  // window buffer: [half][slot][16 x 16]; with nrhs <= 16 (HV <= 1) the second column half is
+  // padding and is neither loaded nor stored, so a buffer holds one half
+  static constexpr int HALVES = HV == 2 ? 2 : 1;
+  static constexpr int WIN = HALVES * WINH;
   static constexpr int PG = 32768;                            // ring page (bytes)
   // ring pages: complex128 3 (2 x 64 KB windows), complex64 4 (3-level windows) or 3 (4-level).
   // (Measured on complex64: a 5th page or a third window buffer, which lets the next window load
-  // a whole item ahead, made the 3-level pass slower: 0.1156 / 0.1168 vs 0.1136 ms.)
+  // a whole item ahead, made the 3-level pass slower: 0.1156 / 0.1168 vs 0.1136 ms.)  With one
+  // window half (nrhs <= 16) the freed shared memory could deepen the ring to 5-6 pages: measured
+  // neutral at nrhs 1 / 8 / 16 for both dtypes (0.639 vs 0.636 ms c128 at nrhs 1,
+  // tools/gpurun_scripts/r2_g9.sh), so the ring keeps its depth.
   static constexpr int NP = sizeof(E) == 16 ? 3 : D > 3 ? 3 : 4;
   __host__ __device__ static constexpr size_t bars_off() { return 2 * WIN * sizeof(E) + (size_t)NP * PG; }
   __host__ __device__ static constexpr size_t smem() { return bars_off() + (1 + NP) * 8 + (1 + NP) * 4; }
@@ -39,10 +45,10 @@ struct PassCfg {
 
 // The operand stream of one CTA: page j (0, 1, 2, ...) is k-steps [s0, s0 + nst) of op q of the
 // CTA's item j / PPI.
-template <class Pol, int D>
+template <class Pol, int D, int HV = 2>
 struct Stream {
   using E = typename Pol::E;
-  using Cfg = PassCfg<Pol, D>;
+  using Cfg = PassCfg<Pol, D, HV>;
   static constexpr int S = 1 << D;
   static constexpr int SPP = Cfg::PG / (S * FAST_FRAG);  // k-steps per page
   static constexpr int SPL = fast_spl((int)sizeof(E), S); // k-steps per page of the column-leaf op
@@ -102,9 +108,9 @@ struct Stream {
     const int64_t w = item & (P.nwin - 1), jt = item >> (P.a_log + P.b_log);
     const int64_t a = P.a_lo + (w >> P.b_log), b = P.b_lo + (w & ((int64_t(1) << P.b_log) - 1));
     const uint32_t bytes = (uint32_t)(S * FAST_HSLAB * sizeof(E));
-    mbar_expect_tx(winF, 2 * bytes);
+    mbar_expect_tx(winF, Cfg::HALVES * bytes);
     const E* Sin = static_cast<const E*>(A.Sin);
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < Cfg::HALVES; ++h) {
       E* dst = winbuf + wb * Cfg::WIN + h * Cfg::WINH;
       if (!P.xin) {  // the window's input slabs are contiguous in the slab buffer
         bulk_g2s(dst, Sin + pass_slab_off(P, 0, jt, h, A.nlev, A.ntiles, a, b, P.in_s, 0), bytes, winF);
@@ -132,8 +138,8 @@ struct Stream {
 template <class Pol, int D, int HV = 2>
 __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_constant__ FastArgs A) {
   using E = typename Pol::E;
-  using Cfg = PassCfg<Pol, D>;
-  using St = Stream<Pol, D>;
+  using Cfg = PassCfg<Pol, D, HV>;
+  using St = Stream<Pol, D, HV>;
   constexpr int NT = Pol::NT;
   constexpr int S = 1 << D;                          // slots of the window
   constexpr int CT = HV == 0 ? 1 : 2 / NT;           // column tiles per slot (in a half)
@@ -425,8 +431,8 @@ const char* fast_kernel_name(int dtype) { return dtype == BF_C128 ? "k_bf_pass<c
 template <class Pol, int D, int HV>
 static void launch_hv(const FastArgs& a, unsigned grid, cudaStream_t st) {
   static std::atomic<size_t> attr[BF_MAX_DEVICES];
-  const size_t smem = PassCfg<Pol, D>::smem();
-  static_assert(PassCfg<Pol, D>::smem() <= 227 * 1024, "pass kernel shared memory");
+  const size_t smem = PassCfg<Pol, D, HV>::smem();
+  static_assert(PassCfg<Pol, D, HV>::smem() <= 227 * 1024, "pass kernel shared memory");
   ensure_smem_attr(attr, (const void*)k_bf_pass<Pol, D, HV>, smem);
   launch_pdl(k_bf_pass<Pol, D, HV>, grid, FAST_THREADS, smem, st, a);
 }
