@@ -232,17 +232,23 @@ __global__ void __launch_bounds__(256, 2) k_stage_tileT(StageArgs a) {
   const int g = lane >> 2, t = lane & 3;
   const int ctiles = (a.nrhs + TC - 1) / TC;
   const int64_t nitems = (int64_t)a.nunits * ctiles;
+  // the CTA's items: one unit with all its column tiles (grid = units; the loader runs ahead across
+  // the column tiles), or a persistent stride over every item (grid < units x tiles)
+  const bool per_unit = gridDim.x == (unsigned)a.nunits;
+  const int64_t i0 = per_unit ? (int64_t)blockIdx.x * ctiles : blockIdx.x;
+  const int64_t i1 = per_unit ? i0 + ctiles : nitems;
+  const int64_t istep = per_unit ? 1 : gridDim.x;
   const E* __restrict__ pool = static_cast<const E*>(a.pool);
   const E* __restrict__ S = static_cast<const E*>(a.S);
   const E* __restrict__ X = static_cast<const E*>(a.X);
   pdl_wait();  // slabs / X / Y of the previous rounds
   // ---- loader: its own walk over (item, term, K chunk), NST - 1 chunks ahead of the consumer
-  int64_t l_item = blockIdx.x;
+  int64_t l_item = i0;
   int l_q = 0, l_kc = 0;
   Task l_tk{};
   int l_r0 = 0, l_j0 = 0;
   auto l_fetch = [&]() {  // task of l_item; skips items without terms (they consume no chunk)
-    for (; l_item < nitems; l_item += gridDim.x) {
+    for (; l_item < i1; l_item += istep) {
       const int2 un = a.units[l_item / ctiles];
       l_tk = a.tasks[un.x];
       l_r0 = un.y * TR;
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tileT(StageArgs a) {
   };
   l_fetch();
   auto load = [&](int stg) {
-    if (l_item >= nitems) return;
+    if (l_item >= i1) return;
     const Term tm = a.terms[l_tk.term0 + l_q];
     E* sA = sm + stg * STAGE;
     E* sB = sA + KC * SA;
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tileT(StageArgs a) {
       l_kc = 0;
       if (++l_q >= l_tk.nterm) {
         l_q = 0;
-        l_item += gridDim.x;
+        l_item += istep;
         l_fetch();
       }
     }
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(256, 2) k_stage_tileT(StageArgs a) {
   }
   const int cw = 8 * w;
   int c = 0;  // consumed chunks
-  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+  for (int64_t item = i0; item < i1; item += istep) {
     const int2 un = a.units[item / ctiles];
     const Task tk = a.tasks[un.x];
     const int r0 = un.y * TR, j0 = (int)(item % ctiles) * TC;
@@ -397,11 +403,19 @@ static void launch_tileT_t(const StageArgs& a, cudaStream_t st) {
   constexpr size_t smem = NST * C::STAGE * sizeof(double2);
   static std::atomic<size_t> attr[BF_MAX_DEVICES];
   ensure_smem_attr(attr, (const void*)k_stage_tileT<M3, NST>, smem);
-  // one item per CTA: measured faster than a persistent grid of 2 CTAs per SM walking the items
-  // with the loader running ahead across them (config 3: 1.48 vs 1.67 ms) -- the hardware
-  // scheduler balances the uneven items (ragged ranks and K) better than a static stride
-  const int64_t items = (int64_t)a.nunits * ((a.nrhs + C::TC - 1) / C::TC);
-  launch_pdl(k_stage_tileT<M3, NST>, (unsigned)items, 1u, 256, smem, st, a);
+  // grid: one CTA per unit walking all its column tiles (the loader runs ahead across them) when
+  // the round has enough units to fill the SMs (>= 4 per SM), else one CTA per (unit, column tile)
+  // -- config 4: 18.7 vs 19.6 ms, config 3's small late rounds: per-item is faster.  BF_TILE_GRID
+  // = 0 / 1 forces either, 2 = a persistent stride (2 CTAs per SM; config 3 1.67 vs 1.48 ms: a static
+  // stride balances the uneven items worse than the hardware scheduler).
+  static const int gm = getenv("BF_TILE_GRID") ? atoi(getenv("BF_TILE_GRID")) : -1;
+  const int64_t ct = (a.nrhs + C::TC - 1) / C::TC;
+  const int64_t items = (int64_t)a.nunits * ct;
+  const int nsm = device_sm_count();
+  const int mode = gm >= 0 ? gm : (a.nunits >= 4LL * nsm ? 1 : 0);
+  int64_t grid = mode == 1 ? a.nunits : mode == 0 ? items : std::min<int64_t>(items, 2LL * nsm);
+  if (mode != 1 && ct > 1 && grid == a.nunits) grid = std::max<int64_t>(1, grid - 1);  // stride mode, not per-unit
+  launch_pdl(k_stage_tileT<M3, NST>, (unsigned)grid, 1u, 256, smem, st, a);
 }
 
 // ------------------------------------------------------------------------------------
