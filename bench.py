@@ -412,6 +412,16 @@ def main():
         roofline = dominant_roofline(args.dtype, name, rounds, mean, nrhs, cs, peaks)
         roofline["kernels"] = {k: {"ms_per_step": v[0], "launches_per_step": v[2], "alg_bytes_per_step": v[1]}
                                for k, v in by_kernel.items()}
+    elif world > 1:
+        # N > 1: per rank, the whole split apply (its leaf / pass launches and the exchange) against
+        # the HBM roofline of one GPU -- each rank streams 1/N of the factors and its subtrees' rows
+        # (per-launch events are not exposed by the split's pre / post calls, so this is step-level)
+        per_rank = ab / world
+        ach = per_rank / (ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / peaks["hbm_gbs"], "traffic": None, "kernel": "split apply per rank (step-level)",
+                    "alg_bytes_per_rank": per_rank, "peak_source": peaks.get("source"),
+                    "note": "max over ranks of the step time; algorithmic bytes / N per rank"}
 
     e2e = None
     if not args.no_e2e and world == 1:

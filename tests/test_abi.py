@@ -107,3 +107,51 @@ def test_no_device_fails_loudly():
     assert _create(bf) == -8
     with pytest.raises(B.BFError):
         pkg.BFHandle(bf, 0)
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of the C-ABI structs have the header's sizes and field offsets (a
+    mismatch would corrupt every call silently): compile a probe against include/bfapply.h."""
+    import subprocess
+    from paper_2007_00202_b200 import construct as cx
+    structs = {"bf_desc": B.bf_desc, "hodbf_desc": B.hodbf_desc, "bf_info_t": B.bf_info_t,
+               "bf_round_info_t": B.bf_round_info_t, "bf_rmv_desc": cx.bf_rmv_desc, "bf_rmv_stats": cx.bf_rmv_stats,
+               "bf_factor": cx.bf_factor, "bf_product": cx.bf_product, "bf_operator": cx.bf_operator,
+               "bf_inv_opts": cx.bf_inv_opts, "bf_front": cx.bf_front}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "bfapply.h"', 'int main(void) {']
+    for name, st in structs.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in st._fields_:
+            lines.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines.append('  return 0; }')
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-std=c99", "-I", inc, str(src), "-o", str(exe)], check=True)
+    out = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines())
+    for name, st in structs.items():
+        assert int(out[name]) == C.sizeof(st), name
+        for f, _ in st._fields_:
+            assert int(out[f"{name}.{f}"]) == getattr(st, f).offset, (name, f)
+
+
+def test_construction_calls_need_a_device():
+    """bf_random_matvec / hodbf_invert / bf_mf_create have no CPU path: without a CUDA device they
+    return BF_ERR_DEVICE (or BF_ERR_ARG for an obviously bad argument) instead of computing."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    from paper_2007_00202_b200 import construct as cx
+    L = cx._lib()
+    d = cx.bf_rmv_desc()
+    lp = np.array([0, 4, 8], dtype=np.int64)
+    d.dtype, d.L, d.lc, d.rank_max, d.m, d.n = 2, 1, -1, 4, 8, 8
+    d.row_leaf_ptr = lp.ctypes.data_as(C.POINTER(C.c_int64))
+    d.col_leaf_ptr = lp.ctypes.data_as(C.POINTER(C.c_int64))
+    d.eps, d.oversample = 1e-10, 4
+    h = C.c_void_p()
+    st = cx.bf_rmv_stats()
+    rc = L.bf_random_matvec(C.byref(d), C.cast(L.bf_operator_apply, C.c_void_p), None, 0, None, C.byref(h),
+                            C.byref(st))
+    assert rc == -8 and not h.value
