@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
 //   B frag (4 x 8, [k][row])  of lane (g, t) = A(8 nt + g, k0 + t)
 //   C (8 x 8)  c[g][2t + e]   = out(row 8 nt + 2t + e, column 8w + g)
 // ------------------------------------------------------------------------------------
-template <bool M3, int NST>
-__global__ void __launch_bounds__(256, 2) k_stage_tileT(StageArgs a) {
+template <bool M3, int NST, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_stage_tileT(StageArgs a) {
   using E = double2;
   using C = TileCfg<PolC128<2>>;
   constexpr int TR = C::TR, TC = C::TC, KC = C::KC, SA = C::SA, SB = C::SB, STAGE = C::STAGE;
@@ -397,12 +397,12 @@ __global__ void __launch_bounds__(256, 2) k_stage_tileT(StageArgs a) {
   pdl_trigger();
 }
 
-template <bool M3, int NST>
+template <bool M3, int NST, int MINB = 2>
 static void launch_tileT_t(const StageArgs& a, cudaStream_t st) {
   using C = TileCfg<PolC128<2>>;
   constexpr size_t smem = NST * C::STAGE * sizeof(double2);
   static std::atomic<size_t> attr[BF_MAX_DEVICES];
-  ensure_smem_attr(attr, (const void*)k_stage_tileT<M3, NST>, smem);
+  ensure_smem_attr(attr, (const void*)k_stage_tileT<M3, NST, MINB>, smem);
   // grid: one CTA per unit walking all its column tiles (the loader runs ahead across them) when
   // the round has enough units to fill the SMs (>= 4 per SM), else one CTA per (unit, column tile)
   // -- config 4: 18.7 vs 19.6 ms, config 3's small late rounds: per-item is faster.  BF_TILE_GRID
@@ -415,7 +415,7 @@ static void launch_tileT_t(const StageArgs& a, cudaStream_t st) {
   const int mode = gm >= 0 ? gm : (a.nunits >= 4LL * nsm ? 1 : 0);
   int64_t grid = mode == 1 ? a.nunits : mode == 0 ? items : std::min<int64_t>(items, 2LL * nsm);
   if (mode != 1 && ct > 1 && grid == a.nunits) grid = std::max<int64_t>(1, grid - 1);  // stride mode, not per-unit
-  launch_pdl(k_stage_tileT<M3, NST>, (unsigned)grid, 1u, 256, smem, st, a);
+  launch_pdl(k_stage_tileT<M3, NST, MINB>, (unsigned)grid, 1u, 256, smem, st, a);
 }
 
 // ------------------------------------------------------------------------------------
@@ -529,8 +529,14 @@ static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
   // outputs) keep the row tiles (config 3: 1.48 ms all-transposed, 1.58 row tiles; the last round
   // 0.279 vs 0.259 ms)
   if (mode && sizeof(V) == 16 && a.nrhs > 8 && r.out_kind == 0) {
-    if (a.m3) launch_tileT_t<true, 2>(a, st);
-    else launch_tileT_t<false, 2>(a, st);
+    static const int minb = getenv("BF_TILE_MINB") ? atoi(getenv("BF_TILE_MINB")) : 2;
+    if (minb >= 3) {
+      if (a.m3) launch_tileT_t<true, 2, 3>(a, st);
+      else launch_tileT_t<false, 2, 3>(a, st);
+    } else {
+      if (a.m3) launch_tileT_t<true, 2>(a, st);
+      else launch_tileT_t<false, 2>(a, st);
+    }
     return;
   }
   if (sizeof(V) == 16)
