@@ -86,8 +86,8 @@ __device__ __forceinline__ void tile_frags(PolC64<NT>, typename PolC64<NT>::Frag
   }
 }
 
-template <class Pol, bool M3>
-__global__ void __launch_bounds__(256, 2) k_stage_tile(StageArgs a) {
+template <class Pol, bool M3, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_stage_tile(StageArgs a) {
   using E = typename Pol::E;
   using C = TileCfg<Pol>;
   constexpr int KS = Pol::KS, TR = C::TR, TC = C::TC, KC = C::KC, SA = C::SA, SB = C::SB;
@@ -489,17 +489,28 @@ static void launch_gemv_t(const StageArgs& a, cudaStream_t st) {
   launch_pdl(k_stage_gemv<V, NR>, (unsigned)((w + 7) / 8), 1u, 256, 0, st, a);
 }
 
-template <class Pol, bool M3>
+template <class Pol, bool M3, int MINB>
 static void launch_tile_t(dim3 grid, const StageArgs& a, cudaStream_t st) {
   constexpr size_t smem = TileCfg<Pol>::NST * TileCfg<Pol>::STAGE * sizeof(typename Pol::E);
   static std::atomic<size_t> attr[BF_MAX_DEVICES];
-  ensure_smem_attr(attr, (const void*)k_stage_tile<Pol, M3>, smem);
-  launch_pdl(k_stage_tile<Pol, M3>, grid.x, grid.y, 256, smem, st, a);
+  ensure_smem_attr(attr, (const void*)k_stage_tile<Pol, M3, MINB>, smem);
+  launch_pdl(k_stage_tile<Pol, M3, MINB>, grid.x, grid.y, 256, smem, st, a);
+}
+// BF_TILE_MINB: CTAs per SM the tile kernels are compiled for (register cap): 3 (72-80 registers,
+// no spills; 3 x 51 KB of shared memory), measured on configs 2-4 against 2
+static int tile_minb() {
+  static const int v = getenv("BF_TILE_MINB") ? atoi(getenv("BF_TILE_MINB")) : 3;
+  return v;
 }
 template <class Pol>
 static void launch_tile(dim3 grid, const StageArgs& a, cudaStream_t st) {
-  if (a.m3) launch_tile_t<Pol, true>(grid, a, st);
-  else launch_tile_t<Pol, false>(grid, a, st);
+  if (tile_minb() >= 3) {
+    if (a.m3) launch_tile_t<Pol, true, 3>(grid, a, st);
+    else launch_tile_t<Pol, false, 3>(grid, a, st);
+    return;
+  }
+  if (a.m3) launch_tile_t<Pol, true, 2>(grid, a, st);
+  else launch_tile_t<Pol, false, 2>(grid, a, st);
 }
 
 template <typename V>
@@ -529,8 +540,8 @@ static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
   // outputs) keep the row tiles (config 3: 1.48 ms all-transposed, 1.58 row tiles; the last round
   // 0.279 vs 0.259 ms)
   if (mode && sizeof(V) == 16 && a.nrhs > 8 && r.out_kind == 0) {
-    static const int minb = getenv("BF_TILE_MINB") ? atoi(getenv("BF_TILE_MINB")) : 2;
-    if (minb >= 3) {
+    if (tile_minb() >= 3) {  // 78 registers, 3 CTAs / SM: config 3 1.47 vs 1.56 ms, config 4 17.2 vs 18.7
+                              // (config 2 0.247 vs 0.237)
       if (a.m3) launch_tileT_t<true, 2, 3>(a, st);
       else launch_tileT_t<false, 2, 3>(a, st);
     } else {
