@@ -81,6 +81,18 @@ struct StageArgs {
 };
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);
+// One product of the compact extraction (bf_extract, Alg. 3): out[out_off + i out_ld + j] (+ if acc)=
+// sum_k pool[a_off + i a_rs + k a_cs] in[in_off + k in_ld + j], i < m, j < w, k < kk (row-major
+// compact slabs, rmatvec.cu k_xprod)
+struct XProd {
+  int64_t a_off, in_off, out_off;
+  int32_t a_rs, a_cs, m, kk, w, in_ld, out_ld, acc;
+};
+void launch_xprod(int dtype, int64_t np, const void* P, const void* pool, const void* S, void* O, cudaStream_t st);
+void launch_xgather_vt(int dtype, int64_t n, const int64_t* e, const void* pool, void* S, cudaStream_t st);
+void launch_xscatter(int dtype, int64_t nI, int64_t nJ, const int64_t* orow, const int64_t* ocol, const void* T, void* out,
+                     int64_t ldo, cudaStream_t st);
+
 void launch_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t lda, void* Y, int64_t ldy,
                        cudaStream_t st);
 void launch_extract_vt_cols(int dtype, int64_t nJ, const int64_t* jmap, const void* pool, void* S, int64_t ldS,

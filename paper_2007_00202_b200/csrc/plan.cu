@@ -25,6 +25,7 @@
 #include <string>
 #include <type_traits>
 #include <vector>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "fast.cuh"
@@ -2383,6 +2384,301 @@ struct XPart {
   XQuery q;
 };
 
+// Compact extraction (Alg. 3 extract_BF: "each block is multiplied only once",
+// P:524-526): every touched block (l, tau, nu) holds a slab of rank x w_nu, w_nu = the number of
+// requested columns under nu (T_S level L - l; the columns are put in tree order, so they form one
+// contiguous range per node).  A W / R stage block then splits into one product per touched child
+// (each child's columns are a sub-range of the parent's), so no block is ever multiplied at a
+// column it does not need and no slab space is zero-filled.  One launch of k_xprod per stage for
+// all parts (the parts never interact), the level-0 Vt columns gathered, the U rows times y^L
+// into a compact nI x nJ block per part, scattered to `out`.  Synchronous on `st`.
+static void extract_compact(int dtype, const void* pool, std::vector<XPart>& parts, void* out, int64_t ldo,
+                            cudaStream_t st, XScratch& xs) {
+  const size_t cs = csize(dtype);
+  static const bool timing = getenv("BF_EXTRACT_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  int Lmax = 0;
+  for (XPart& pt : parts) Lmax = std::max(Lmax, pt.G->L);
+  // stages: 0 = level-0 gather (separate), 1..: products by level of the recursion
+  std::vector<std::vector<XProd>> stage((size_t)2 * Lmax + 4);
+  std::vector<int64_t> vtg;                       // k_xgather_vt entries
+  std::vector<int64_t> sc_orow, sc_ocol;          // per part: result scatter maps
+  struct PartOut { int64_t toff, nI, nJ, orow0, ocol0; };
+  std::vector<PartOut> pouts;
+  int64_t slab = 0;  // compact slab elements (all parts)
+  for (XPart& pt : parts) {
+    const Geom& G = *pt.G;
+    const int L = G.L, lc = G.lc;
+    XQuery& q = pt.q;
+    const int64_t nI = (int64_t)q.pr.size(), nJ = (int64_t)q.pc.size();
+    if (nI == 0 || nJ == 0) continue;
+    {  // the part's columns in tree order
+      std::vector<int64_t> ord(nJ);
+      for (int64_t j = 0; j < nJ; ++j) ord[j] = j;
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return q.pc[x] < q.pc[y]; });
+      XQuery s2 = q;
+      for (int64_t j = 0; j < nJ; ++j) {
+        q.pc[j] = s2.pc[ord[j]];
+        q.vtoff[j] = s2.vtoff[ord[j]];
+        q.ocol[j] = s2.ocol[ord[j]];
+      }
+    }
+    std::vector<int64_t> tj(nJ), ti(nI);
+    for (int64_t j = 0; j < nJ; ++j) tj[j] = leaf_of(G.clp, q.pc[j]);
+    for (int64_t i = 0; i < nI; ++i) ti[i] = leaf_of(G.rlp, q.pr[i]);
+    // column ranges: lo[l][nu], w[l][nu] for nu at T_S level L - l (node of leaf t: t >> l)
+    std::vector<std::vector<int32_t>> lo(L + 1), wd(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      lo[l].assign((size_t)1 << (L - l), 0);
+      wd[l].assign((size_t)1 << (L - l), 0);
+      for (int64_t j = 0; j < nJ; ++j) {
+        const int64_t nu = tj[j] >> l;
+        if (wd[l][nu] == 0) lo[l][nu] = (int32_t)j;
+        wd[l][nu]++;
+      }
+    }
+    // touched tau per T_O level l (ascending lists)
+    std::vector<std::vector<int64_t>> taus(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      std::vector<char> f((size_t)1 << l, 0);
+      for (int64_t i = 0; i < nI; ++i) f[ti[i] >> (L - l)] = 1;
+      for (size_t t = 0; t < f.size(); ++t)
+        if (f[t]) taus[l].push_back((int64_t)t);
+    }
+    // touched nu per level (ascending)
+    std::vector<std::vector<int64_t>> nus(L + 1);
+    for (int l = 0; l <= L; ++l)
+      for (size_t v = 0; v < wd[l].size(); ++v)
+        if (wd[l][v]) nus[l].push_back((int64_t)v);
+    // slab offsets: column side z (l = 0..lc), row side y (l = lc..L), flat over the touched
+    // (tau, nu) pairs of a level: slot = pos(tau) * |nus[l]| + pos(nu)
+    std::vector<std::vector<int32_t>> tpos(L + 1), npos(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      tpos[l].assign((size_t)1 << l, -1);
+      npos[l].assign((size_t)1 << (L - l), -1);
+      for (size_t k = 0; k < taus[l].size(); ++k) tpos[l][taus[l][k]] = (int32_t)k;
+      for (size_t k = 0; k < nus[l].size(); ++k) npos[l][nus[l][k]] = (int32_t)k;
+    }
+    std::vector<std::vector<int64_t>> zo(lc + 1), yo(L - lc + 1);
+    for (int l = 0; l <= lc; ++l) {
+      const int64_t nt = l == 0 ? 1 : (int64_t)taus[l].size(), nn = (int64_t)nus[l].size();
+      zo[l].assign((size_t)(nt * nn), -1);
+      for (int64_t pt2 = 0; pt2 < nt; ++pt2) {
+        const int64_t tau = l == 0 ? 0 : taus[l][pt2];
+        for (int64_t pn = 0; pn < nn; ++pn) {
+          const int64_t nu = nus[l][pn];
+          zo[l][pt2 * nn + pn] = slab;
+          slab += (int64_t)G.c(l, G.idx(l, tau, nu)) * wd[l][nu];
+        }
+      }
+    }
+    for (int l = lc; l <= L; ++l) {
+      const int64_t nt = (int64_t)taus[l].size(), nn = (int64_t)nus[l].size();
+      yo[l - lc].assign((size_t)(nt * nn), -1);
+      for (int64_t pt2 = 0; pt2 < nt; ++pt2)
+        for (int64_t pn = 0; pn < nn; ++pn) {
+          const int64_t tau = taus[l][pt2], nu = nus[l][pn];
+          yo[l - lc][pt2 * nn + pn] = slab;
+          slab += (int64_t)G.r(l, G.idx(l, tau, nu)) * wd[l][nu];
+        }
+    }
+    auto ZO = [&](int l, int64_t tau, int64_t nu) {
+      return zo[l][(int64_t)(l == 0 ? 0 : tpos[l][tau]) * (int64_t)nus[l].size() + npos[l][nu]];
+    };
+    auto YO = [&](int l, int64_t tau, int64_t nu) {
+      return yo[l - lc][(int64_t)tpos[l][tau] * (int64_t)nus[l].size() + npos[l][nu]];
+    };
+    // level 0: z^0_nu = Vt_nu(:, requested columns)
+    for (int64_t j = 0; j < nJ; ++j) {
+      const int64_t nu = tj[j];
+      vtg.push_back(ZO(0, 0, nu) + (j - lo[0][nu]));
+      vtg.push_back(wd[0][nu]);
+      vtg.push_back(G.c(0, nu));
+      vtg.push_back(q.vtoff[j]);
+    }
+    // W stages l = 1..lc: z^l_{tau,nu}(:, child s's columns) = W_{tau,nu}(:, child s block) z^{l-1}_{tau>>1, 2nu+s}
+    for (int l = 1; l <= lc; ++l)
+      for (int64_t tau : taus[l])
+        for (int64_t nu : nus[l]) {
+          const int64_t i = G.idx(l, tau, nu);
+          const int c = G.c(l, i);
+          if (c == 0) continue;
+          const int64_t ip = (l - 1 == 0) ? 0 : (tau >> 1);
+          int32_t coff = 0;
+          int cprev = 0;
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int64_t ch = 2 * nu + s2;
+            const int64_t ic = G.idx(l - 1, ip, ch);
+            const int cc = G.c(l - 1, ic);
+            const int32_t w = wd[l - 1][ch];
+            if (w > 0) {
+              XProd x{};
+              x.a_off = pt.F.w + G.w_off[l][i] + (int64_t)cprev * c;
+              x.a_rs = 1;
+              x.a_cs = c;
+              x.m = c;
+              x.kk = cc;
+              x.w = w;
+              x.in_off = ZO(l - 1, ip, ch);
+              x.in_ld = w;
+              x.out_off = ZO(l, tau, nu) + coff;
+              x.out_ld = wd[l][nu];
+              stage[l].push_back(x);
+            }
+            coff += w;
+            cprev += cc;
+          }
+        }
+    // centre: y^lc = B z^lc
+    for (int64_t tau : taus[lc])
+      for (int64_t nu : nus[lc]) {
+        const int64_t i = G.idx(lc, tau, nu);
+        const int r = G.r(lc, i), c = G.c(lc, i);
+        if (r == 0) continue;
+        XProd x{};
+        x.a_off = pt.F.b + G.b_off[i];
+        x.a_rs = 1;
+        x.a_cs = r;
+        x.m = r;
+        x.kk = c;
+        x.w = wd[lc][nu];
+        x.in_off = ZO(lc, lc == 0 ? 0 : tau, nu);
+        x.in_ld = wd[lc][nu];
+        x.out_off = YO(lc, tau, nu);
+        x.out_ld = wd[lc][nu];
+        stage[lc + 1].push_back(x);
+      }
+    // R stages l -> l+1 (gather form): y^{l+1}_{tp,np}(:, child s's columns) =
+    //   R_{tp>>1, 2np+s}(rows of child tp & 1) y^l_{tp>>1, 2np+s}
+    for (int l = lc; l < L; ++l)
+      for (int64_t tp : taus[l + 1])
+        for (int64_t np : nus[l + 1]) {
+          const int64_t io = G.idx(l + 1, tp, np);
+          const int ro = G.r(l + 1, io);
+          if (ro == 0) continue;
+          const int64_t a = tp >> 1;
+          const int part = (int)(tp & 1);
+          const int rt = G.r(l + 1, G.idx(l + 1, 2 * a, np)), rb = G.r(l + 1, G.idx(l + 1, 2 * a + 1, np));
+          int32_t coff = 0;
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int64_t ch = 2 * np + s2;
+            const int32_t w = wd[l][ch];
+            if (w > 0) {
+              const int64_t i = G.idx(l, a, ch);
+              XProd x{};
+              x.a_off = pt.F.r + G.r_off[l][i] + (part ? rt : 0);
+              x.a_rs = 1;
+              x.a_cs = rt + rb;
+              x.m = ro;
+              x.kk = G.r(l, i);
+              x.w = w;
+              x.in_off = YO(l, a, ch);
+              x.in_ld = w;
+              x.out_off = YO(l + 1, tp, np) + coff;
+              x.out_ld = wd[l + 1][np];
+              stage[l + 2].push_back(x);
+            }
+            coff += w;
+          }
+        }
+    // U rows: T(i, :) = U_tau(row, :) y^L_tau, into the part's compact nI x nJ block
+    PartOut po{0, nI, nJ, (int64_t)sc_orow.size(), (int64_t)sc_ocol.size()};
+    po.toff = slab;
+    slab += nI * nJ;
+    for (int64_t i = 0; i < nI; ++i) {
+      const int64_t tau = ti[i];
+      XProd x{};
+      x.a_off = q.uoff[i];
+      x.a_rs = 1;
+      x.a_cs = (int32_t)q.ustr[i];
+      x.m = 1;
+      x.kk = G.r(L, tau);
+      x.w = (int32_t)nJ;
+      x.in_off = YO(L, tau, 0);
+      x.in_ld = (int32_t)nJ;
+      x.out_off = po.toff + i * nJ;
+      x.out_ld = (int32_t)nJ;
+      stage[L + 2].push_back(x);
+    }
+    for (int64_t i = 0; i < nI; ++i) sc_orow.push_back(q.orow[i]);
+    for (int64_t j = 0; j < nJ; ++j) sc_ocol.push_back(q.ocol[j]);
+    pouts.push_back(po);
+  }
+  if (pouts.empty()) return;
+  // upload: [slab | products | vt gather | scatter maps]
+  // products of more than 128 outputs are cut into pieces of at most 128 (one warp each, <= 4
+  // outputs per lane): 32-column chunks of max(1, 128 / w) rows -- the lanes of a wide chunk share
+  // the factor row and read consecutive input columns; big blocks (wide queries, HOD-BF top
+  // levels) spread over many warps while the many small scattered-query products stay whole
+  constexpr int64_t XP_MAX = 128;
+  for (auto& sv : stage) {
+    bool big = false;
+    for (const XProd& x : sv) big |= (int64_t)x.m * x.w > XP_MAX;
+    if (!big) continue;
+    std::vector<XProd> nv;
+    nv.reserve(sv.size() + sv.size() / 2);
+    for (const XProd& x : sv) {
+      if ((int64_t)x.m * x.w <= XP_MAX) {
+        nv.push_back(x);
+        continue;
+      }
+      for (int32_t j0 = 0; j0 < x.w; j0 += 32) {
+        const int32_t w = std::min<int32_t>(32, x.w - j0);
+        const int32_t rp = std::max<int32_t>(1, (int32_t)(XP_MAX / w));
+        for (int32_t i0 = 0; i0 < x.m; i0 += rp) {
+          XProd y = x;
+          y.w = w;
+          y.m = std::min<int32_t>(rp, x.m - i0);
+          y.a_off += (int64_t)i0 * x.a_rs;
+          y.in_off += j0;
+          y.out_off += j0 + (int64_t)i0 * x.out_ld;
+          nv.push_back(y);
+        }
+      }
+    }
+    sv.swap(nv);
+  }
+  std::vector<int64_t> soff(stage.size() + 1, 0);
+  for (size_t k = 0; k < stage.size(); ++k) soff[k + 1] = soff[k] + (int64_t)stage[k].size();
+  std::vector<XProd> allp((size_t)soff.back());
+  for (size_t k = 0; k < stage.size(); ++k)
+    if (!stage[k].empty()) std::copy(stage[k].begin(), stage[k].end(), allp.begin() + soff[k]);
+  const size_t bS = align256((size_t)slab * cs), bP = align256(allp.size() * sizeof(XProd)),
+               bV = align256(vtg.size() * 8), bR = align256(sc_orow.size() * 8), bC = align256(sc_ocol.size() * 8);
+  std::lock_guard<std::mutex> lk(xs.mu);
+  char* base = static_cast<char*>(xs.get(bS + bP + bV + bR + bC));
+  void* dS = base;
+  XProd* dP = reinterpret_cast<XProd*>(base + bS);
+  int64_t* dV = reinterpret_cast<int64_t*>(base + bS + bP);
+  int64_t* dR = reinterpret_cast<int64_t*>(base + bS + bP + bV);
+  int64_t* dC = reinterpret_cast<int64_t*>(base + bS + bP + bV + bR);
+  if (!allp.empty()) BF_CK(cudaMemcpyAsync(dP, allp.data(), allp.size() * sizeof(XProd), cudaMemcpyHostToDevice, st));
+  BF_CK(cudaMemcpyAsync(dV, vtg.data(), vtg.size() * 8, cudaMemcpyHostToDevice, st));
+  BF_CK(cudaMemcpyAsync(dR, sc_orow.data(), sc_orow.size() * 8, cudaMemcpyHostToDevice, st));
+  BF_CK(cudaMemcpyAsync(dC, sc_ocol.data(), sc_ocol.size() * 8, cudaMemcpyHostToDevice, st));
+  const auto t1 = std::chrono::steady_clock::now();
+  launch_xgather_vt(dtype, (int64_t)vtg.size() / 4, dV, pool, dS, st);
+  for (size_t k = 0; k < stage.size(); ++k)
+    launch_xprod(dtype, soff[k + 1] - soff[k], dP + soff[k], pool, dS, dS, st);
+  for (const PartOut& po : pouts)
+    launch_xscatter(dtype, po.nI, po.nJ, dR + po.orow0, dC + po.ocol0, static_cast<char*>(dS) + (size_t)po.toff * cs,
+                    out, ldo, st);
+  BF_CK(cudaGetLastError());
+  BF_CK(cudaStreamSynchronize(st));
+  if (timing) {
+    const auto t2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "bf_extract (compact): plan %.3f ms, upload + device %.3f ms, %zu products, %lld slab entries\n",
+            std::chrono::duration<double, std::milli>(t1 - t0).count(),
+            std::chrono::duration<double, std::milli>(t2 - t1).count(), allp.size(), (long long)slab);
+  }
+}
+
+// BF_EXTRACT_LEGACY selects the round-1 plan (per-query generic rounds over full-width slabs)
+static bool extract_legacy() {
+  static const bool v = getenv("BF_EXTRACT_LEGACY") != nullptr;
+  return v;
+}
+
 // Sub-matrices of one or more butterflies stored in `pool`, as partial matvecs (Alg. 3
 // extract_BF), in ONE plan: every part's K E_J evaluated only on the blocks
 // (l, tau, nu) with tau an ancestor of a requested row's leaf and nu an ancestor of a requested
@@ -2573,7 +2869,10 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
     parts[0].G = &G;
     parts[0].F = F;
     parts[0].q = std::move(q);
-    extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
+    if (extract_legacy())
+      extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
+    else
+      extract_compact(h->dtype, h->pool, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
@@ -2660,7 +2959,10 @@ int hodbf_extract(hodbf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, c
         parts.push_back(XPart{&G, h->F[k], std::move(q)});
       }
     }
-    extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, st, h->xs);
+    if (extract_legacy())
+      extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, st, h->xs);
+    else
+      extract_compact(h->dtype, h->pool, parts, out, ldo, st, h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);

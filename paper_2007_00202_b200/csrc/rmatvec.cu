@@ -596,3 +596,90 @@ void launch_index_rows(int dtype, int64_t rows, int64_t nrhs, const int64_t* idx
 }
 
 }  // namespace bfa
+
+namespace bfa {
+
+// ---- compact sub-matrix extraction (Alg. 3 extract_BF: every touched block is
+// multiplied once, at the width of the requested columns under its column node) -------------
+// One product: out[out_off + i * out_ld + j] (+)= sum_k A(i, k) in[in_off + k * in_ld + j],
+// A(i, k) = pool[a_off + i * a_rs + k * a_cs]; i < m, j < w, k < kk.  Row-major compact slabs.
+
+// one warp per product; lanes over the m x w outputs
+template <typename V>
+__global__ void k_xprod(int64_t np, const XProd* __restrict__ P, const V* __restrict__ pool, const V* __restrict__ S,
+                        V* __restrict__ O) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = wid; p < np; p += nw) {
+    const XProd q = P[p];
+    const int tot = q.m * q.w;
+    for (int e = lane; e < tot; e += 32) {
+      const int i = e / q.w, j = e - i * q.w;
+      const V* a = pool + q.a_off + (int64_t)i * q.a_rs;
+      const V* x = S + q.in_off + j;
+      V s = cmk<V>(0, 0);
+      for (int k = 0; k < q.kk; ++k) s = cadd(s, cmul(a[(int64_t)k * q.a_cs], x[(int64_t)k * q.in_ld]));
+      V* o = O + q.out_off + (int64_t)i * q.out_ld + j;
+      if (q.acc) s = cadd(s, *o);
+      *o = s;
+    }
+  }
+}
+
+// the level-0 slabs: S[dst + r * w + jj] = pool[src + r] for r < c (the requested Vt columns;
+// entry e = {dst slab offset + column, w, rank c, pool offset of the Vt column})
+template <typename V>
+__global__ void k_xgather_vt(int64_t n, const int64_t* __restrict__ e, const V* __restrict__ pool, V* __restrict__ S) {
+  for (int64_t q = blockIdx.x; q < n; q += gridDim.x) {
+    const int64_t dst = e[4 * q], w = e[4 * q + 1], c = e[4 * q + 2], src = e[4 * q + 3];
+    for (int64_t r = threadIdx.x; r < c; r += blockDim.x) S[dst + r * w] = pool[src + r];
+  }
+}
+
+// scatter the compact result rows (tree-sorted columns) to the caller's matrix:
+// out[orow[i] + ocol[j] * ldo] = T[i * nJ + j]
+template <typename V>
+__global__ void k_xscatter(int64_t nI, int64_t nJ, const int64_t* __restrict__ orow, const int64_t* __restrict__ ocol,
+                           const V* __restrict__ T, V* __restrict__ out, int64_t ldo) {
+  const int64_t tot = nI * nJ;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / nJ, j = e - i * nJ;
+    out[orow[i] + ocol[j] * ldo] = T[e];
+  }
+}
+
+void launch_xprod(int dtype, int64_t np, const void* P, const void* pool, const void* S, void* O, cudaStream_t st) {
+  if (np == 0) return;
+  const int64_t blocks = std::min<int64_t>((np + 7) / 8, 65535 * 4);
+  if (dtype == BF_C128)
+    k_xprod<double2><<<(unsigned)blocks, 256, 0, st>>>(np, static_cast<const XProd*>(P), static_cast<const double2*>(pool),
+                                                        static_cast<const double2*>(S), static_cast<double2*>(O));
+  else
+    k_xprod<float2><<<(unsigned)blocks, 256, 0, st>>>(np, static_cast<const XProd*>(P), static_cast<const float2*>(pool),
+                                                       static_cast<const float2*>(S), static_cast<float2*>(O));
+}
+
+void launch_xgather_vt(int dtype, int64_t n, const int64_t* e, const void* pool, void* S, cudaStream_t st) {
+  if (n == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(n, 65535);
+  if (dtype == BF_C128)
+    k_xgather_vt<double2><<<grid, 64, 0, st>>>(n, e, static_cast<const double2*>(pool), static_cast<double2*>(S));
+  else
+    k_xgather_vt<float2><<<grid, 64, 0, st>>>(n, e, static_cast<const float2*>(pool), static_cast<float2*>(S));
+}
+
+void launch_xscatter(int dtype, int64_t nI, int64_t nJ, const int64_t* orow, const int64_t* ocol, const void* T, void* out,
+                     int64_t ldo, cudaStream_t st) {
+  const int64_t tot = nI * nJ;
+  if (tot == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, 8192);
+  if (dtype == BF_C128)
+    k_xscatter<double2><<<grid, 256, 0, st>>>(nI, nJ, orow, ocol, static_cast<const double2*>(T),
+                                              static_cast<double2*>(out), ldo);
+  else
+    k_xscatter<float2><<<grid, 256, 0, st>>>(nI, nJ, orow, ocol, static_cast<const float2*>(T),
+                                             static_cast<float2*>(out), ldo);
+}
+
+}  // namespace bfa
