@@ -214,11 +214,22 @@ int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t l
  * repeats allowed), out a DEVICE column-major nI x nJ block with ldo >= nI.  Computed as a
  * partial matvec: K E_J on the blocks (l, tau, nu) whose tau is an ancestor of a requested
  * row's leaf and whose nu is an ancestor of a requested column's leaf, then the requested rows.
- * Single-device handles only (BF_ERR_ARG for a bf_dist handle).  Synchronous: allocates and frees
- * its temporaries (slab space of nJ columns, the plan of the touched blocks) and returns after
- * the work on `stream` completed.  BF_ERR_ARG on out-of-range indices or NULL arguments. */
+ * Each touched block's slab holds only the requested columns under its column node (the columns
+ * in tree order form one range per node), so a W / R block is one product per touched child at
+ * that child's width: every block multiplied once.  Single-device handles only
+ * (BF_ERR_ARG for a bf_dist handle).  Synchronous: uses a grow-only scratch of the handle and
+ * returns after the work on `stream` completed.  BF_ERR_ARG on out-of-range indices or NULL
+ * arguments. */
 int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
                int64_t ldo, bf_stream_t stream);
+
+/* Alg. 3's list form: K(I_k, J_k) for every request k of a list, evaluated together
+ * (one launch per stage for all requests; each request's touched blocks multiplied once, at the
+ * width of its columns under the block's column node).  Request k: nI[k] rows rows[k][...] and
+ * nJ[k] columns cols[k][...] (HOST user indices), result into the DEVICE block out[k] (column-major,
+ * leading dimension ldo[k] >= nI[k]).  Synchronous on `stream`.  Errors as bf_extract. */
+int bf_extract_list(bf_handle h, int64_t npairs, const int64_t* nI, const int64_t* const* rows, const int64_t* nJ,
+                    const int64_t* const* cols, void* const* out, const int64_t* ldo, bf_stream_t stream);
 
 /* HOD-BF sub-matrix extraction (extract_HODBF): out(i, j) =
  * A(rows[i], cols[j]) for user indices, as bf_extract: the entries inside one leaf from D_t,

@@ -295,6 +295,31 @@ class BFHandle:
                                               max(len(r), 1), _stream_handle(stream)))
         return out.T
 
+    def extract_list(self, pairs, stream=None):
+        """[K(rows_k, cols_k) for (rows_k, cols_k) in pairs] (bf_extract_list: Alg. 3's list form,
+        one batched evaluation; synchronous).  Each result an (len(rows_k), len(cols_k)) tensor."""
+        L = lib()
+        if not getattr(L, "_xl_sig", False):
+            L.bf_extract_list.restype = C.c_int
+            L.bf_extract_list.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_void_p),
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                          C.POINTER(C.c_int64), C.c_void_p]
+            L._xl_sig = True
+        keep, outs = [], []
+        n = len(pairs)
+        nI, nJ, ldo = (C.c_int64 * max(n, 1))(), (C.c_int64 * max(n, 1))(), (C.c_int64 * max(n, 1))()
+        rp, cp, op = (C.c_void_p * max(n, 1))(), (C.c_void_p * max(n, 1))(), (C.c_void_p * max(n, 1))()
+        for k, (r, c) in enumerate(pairs):
+            r = np.ascontiguousarray(np.asarray(r, dtype=np.int64))
+            c = np.ascontiguousarray(np.asarray(c, dtype=np.int64))
+            keep += [r, c]
+            o = torch.zeros((len(c), len(r)), dtype=_torch_dtype(self.code), device=torch.device("cuda", self.device))
+            outs.append(o)
+            nI[k], nJ[k], ldo[k] = len(r), len(c), max(len(r), 1)
+            rp[k], cp[k], op[k] = r.ctypes.data, c.ctypes.data, o.data_ptr()
+        _check("bf_extract_list", L.bf_extract_list(self.h, n, nI, rp, nJ, cp, op, ldo, _stream_handle(stream)))
+        return [o.T for o in outs]
+
     def apply(self, X: torch.Tensor, op: str = "N", out: Optional[torch.Tensor] = None,
               work: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """Y = K X (op N), K^H X (op C) or K^T X (op T); X, Y shaped (nrhs, rows)."""

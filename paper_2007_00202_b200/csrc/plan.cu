@@ -2382,6 +2382,8 @@ struct XPart {
   const Geom* G;
   FBase F;
   XQuery q;
+  void* out = nullptr;  // bf_extract_list: this part's own output block (nullptr: the call's)
+  int64_t ldo = 0;
 };
 
 // Compact extraction (Alg. 3 extract_BF: "each block is multiplied only once",
@@ -2403,7 +2405,7 @@ static void extract_compact(int dtype, const void* pool, std::vector<XPart>& par
   std::vector<std::vector<XProd>> stage((size_t)2 * Lmax + 4);
   std::vector<int64_t> vtg;                       // k_xgather_vt entries
   std::vector<int64_t> sc_orow, sc_ocol;          // per part: result scatter maps
-  struct PartOut { int64_t toff, nI, nJ, orow0, ocol0; };
+  struct PartOut { int64_t toff, nI, nJ, orow0, ocol0; void* out; int64_t ldo; };
   std::vector<PartOut> pouts;
   int64_t slab = 0;  // compact slab elements (all parts)
   for (XPart& pt : parts) {
@@ -2582,7 +2584,8 @@ static void extract_compact(int dtype, const void* pool, std::vector<XPart>& par
           }
         }
     // U rows: T(i, :) = U_tau(row, :) y^L_tau, into the part's compact nI x nJ block
-    PartOut po{0, nI, nJ, (int64_t)sc_orow.size(), (int64_t)sc_ocol.size()};
+    PartOut po{0, nI, nJ, (int64_t)sc_orow.size(), (int64_t)sc_ocol.size(), pt.out ? pt.out : out,
+               pt.out ? pt.ldo : ldo};
     po.toff = slab;
     slab += nI * nJ;
     for (int64_t i = 0; i < nI; ++i) {
@@ -2662,7 +2665,7 @@ static void extract_compact(int dtype, const void* pool, std::vector<XPart>& par
     launch_xprod(dtype, soff[k + 1] - soff[k], dP + soff[k], pool, dS, dS, st);
   for (const PartOut& po : pouts)
     launch_xscatter(dtype, po.nI, po.nJ, dR + po.orow0, dC + po.ocol0, static_cast<char*>(dS) + (size_t)po.toff * cs,
-                    out, ldo, st);
+                    po.out, po.ldo, st);
   BF_CK(cudaGetLastError());
   BF_CK(cudaStreamSynchronize(st));
   if (timing) {
@@ -2810,6 +2813,70 @@ extern "C" {
 
 // K(I, J) (bf_extract): the user indices to tree positions, the standalone pool's U / Vt
 // locations, then extract_core.
+}  // extern "C"
+
+namespace bfa {
+// One (I, J) request of a butterfly handle as an extraction part (user indices -> tree positions,
+// the pool locations of the requested U rows / Vt columns).  Validates the indices.
+static XPart bf_extract_part(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols) {
+  const Geom& G = h->G;
+  require(nI >= 0 && nJ >= 0, BF_ERR_ARG, "negative size");
+  require((nI == 0 || rows != nullptr) && (nJ == 0 || cols != nullptr), BF_ERR_ARG, "NULL index list");
+  require(nJ <= (int64_t)65535 * 32, BF_ERR_ARG, "too many columns for one launch");
+  for (int64_t i = 0; i < nI; ++i) require(rows[i] >= 0 && rows[i] < G.m, BF_ERR_ARG, "row index out of range");
+  for (int64_t j = 0; j < nJ; ++j) require(cols[j] >= 0 && cols[j] < G.n, BF_ERR_ARG, "column index out of range");
+  {  // user index -> tree position, cached on the host on first use
+    std::lock_guard<std::mutex> lk(h->hmu);
+    if (h->h_rinv.empty()) {
+      std::vector<int64_t> rp(G.m), cp(G.n);
+      if (h->d_rperm) BF_CK(cudaMemcpy(rp.data(), h->d_rperm, G.m * 8, cudaMemcpyDeviceToHost));
+      else for (int64_t i = 0; i < G.m; ++i) rp[i] = i;
+      if (h->d_cperm) BF_CK(cudaMemcpy(cp.data(), h->d_cperm, G.n * 8, cudaMemcpyDeviceToHost));
+      else for (int64_t i = 0; i < G.n; ++i) cp[i] = i;
+      h->h_rinv.assign(G.m, 0);
+      h->h_cinv.assign(G.n, 0);
+      for (int64_t p = 0; p < G.m; ++p) h->h_rinv[rp[p]] = p;
+      for (int64_t p = 0; p < G.n; ++p) h->h_cinv[cp[p]] = p;
+    }
+  }
+  FBase F;
+  F.u = 0;
+  F.r = G.len_U;
+  F.b = F.r + G.len_R;
+  F.w = F.b + G.len_B;
+  F.vt = F.w + G.len_W;
+  XQuery q;
+  q.pr.resize(nI);
+  q.uoff.resize(nI);
+  q.ustr.resize(nI);
+  q.orow.resize(nI);
+  q.pc.resize(nJ);
+  q.vtoff.resize(nJ);
+  q.ocol.resize(nJ);
+  for (int64_t i = 0; i < nI; ++i) {
+    q.pr[i] = h->h_rinv[rows[i]];
+    const int64_t tau = leaf_of(G.rlp, q.pr[i]);
+    q.uoff[i] = F.u + G.u_off[tau] + (q.pr[i] - G.rlp[tau]);
+    q.ustr[i] = G.mt(tau);
+    q.orow[i] = i;
+  }
+  for (int64_t j = 0; j < nJ; ++j) {
+    q.pc[j] = h->h_cinv[cols[j]];
+    const int64_t nu = leaf_of(G.clp, q.pc[j]);
+    q.vtoff[j] = F.vt + G.vt_off[nu] + (q.pc[j] - G.clp[nu]) * G.c(0, nu);
+    q.ocol[j] = j;
+  }
+  XPart pt;
+  pt.G = &G;
+  pt.F = F;
+  pt.q = std::move(q);
+  return pt;
+}
+}  // namespace bfa
+
+extern "C" {
+
+// K(I, J) (bf_extract): one part, Alg. 3's compact evaluation (extract_compact)
 int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols, void* out,
                int64_t ldo, bf_stream_t stream) {
   try {
@@ -2819,60 +2886,40 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
     if (nI == 0 || nJ == 0) return BF_OK;
     require(rows != nullptr && cols != nullptr && out != nullptr, BF_ERR_ARG, "NULL argument");
     require(ldo >= nI, BF_ERR_ARG, "ldo < number of rows");
-    require(nJ <= (int64_t)65535 * 32, BF_ERR_ARG, "too many columns for one launch");
-    const Geom& G = h->G;
-    for (int64_t i = 0; i < nI; ++i) require(rows[i] >= 0 && rows[i] < G.m, BF_ERR_ARG, "row index out of range");
-    for (int64_t j = 0; j < nJ; ++j) require(cols[j] >= 0 && cols[j] < G.n, BF_ERR_ARG, "column index out of range");
     DeviceGuard dg(h->device);
-    {  // user index -> tree position, cached on the host on first use
-      std::lock_guard<std::mutex> lk(h->hmu);
-      if (h->h_rinv.empty()) {
-        std::vector<int64_t> rp(G.m), cp(G.n);
-        if (h->d_rperm) BF_CK(cudaMemcpy(rp.data(), h->d_rperm, G.m * 8, cudaMemcpyDeviceToHost));
-        else for (int64_t i = 0; i < G.m; ++i) rp[i] = i;
-        if (h->d_cperm) BF_CK(cudaMemcpy(cp.data(), h->d_cperm, G.n * 8, cudaMemcpyDeviceToHost));
-        else for (int64_t i = 0; i < G.n; ++i) cp[i] = i;
-        h->h_rinv.assign(G.m, 0);
-        h->h_cinv.assign(G.n, 0);
-        for (int64_t p = 0; p < G.m; ++p) h->h_rinv[rp[p]] = p;
-        for (int64_t p = 0; p < G.n; ++p) h->h_cinv[cp[p]] = p;
-      }
-    }
-    FBase F;
-    F.u = 0;
-    F.r = G.len_U;
-    F.b = F.r + G.len_R;
-    F.w = F.b + G.len_B;
-    F.vt = F.w + G.len_W;
-    XQuery q;
-    q.pr.resize(nI);
-    q.uoff.resize(nI);
-    q.ustr.resize(nI);
-    q.orow.resize(nI);
-    q.pc.resize(nJ);
-    q.vtoff.resize(nJ);
-    q.ocol.resize(nJ);
-    for (int64_t i = 0; i < nI; ++i) {
-      q.pr[i] = h->h_rinv[rows[i]];
-      const int64_t tau = leaf_of(G.rlp, q.pr[i]);
-      q.uoff[i] = F.u + G.u_off[tau] + (q.pr[i] - G.rlp[tau]);
-      q.ustr[i] = G.mt(tau);
-      q.orow[i] = i;
-    }
-    for (int64_t j = 0; j < nJ; ++j) {
-      q.pc[j] = h->h_cinv[cols[j]];
-      const int64_t nu = leaf_of(G.clp, q.pc[j]);
-      q.vtoff[j] = F.vt + G.vt_off[nu] + (q.pc[j] - G.clp[nu]) * G.c(0, nu);
-      q.ocol[j] = j;
-    }
-    std::vector<XPart> parts(1);
-    parts[0].G = &G;
-    parts[0].F = F;
-    parts[0].q = std::move(q);
+    std::vector<XPart> parts;
+    parts.push_back(bf_extract_part(h, nI, rows, nJ, cols));
     if (extract_legacy())
       extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
     else
       extract_compact(h->dtype, h->pool, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
+    return BF_OK;
+  } catch (const Err& e) {
+    return fail(e);
+  }
+}
+
+// Alg. 3's list form: every (I_k, J_k) of the list in one batched evaluation (all requests'
+// stage-s products in one launch per stage), K(I_k, J_k) into out[k] (column-major, ld ldo[k])
+int bf_extract_list(bf_handle h, int64_t npairs, const int64_t* nI, const int64_t* const* rows, const int64_t* nJ,
+                    const int64_t* const* cols, void* const* out, const int64_t* ldo, bf_stream_t stream) {
+  try {
+    require(h != nullptr, BF_ERR_ARG, "NULL handle");
+    require(!h->dist, BF_ERR_ARG, "bf_extract_list needs a single-device handle");
+    require(npairs >= 0, BF_ERR_ARG, "negative list length");
+    if (npairs == 0) return BF_OK;
+    require(nI && rows && nJ && cols && out && ldo, BF_ERR_ARG, "NULL argument");
+    DeviceGuard dg(h->device);
+    std::vector<XPart> parts;
+    for (int64_t k = 0; k < npairs; ++k) {
+      if (nI[k] == 0 || nJ[k] == 0) continue;
+      require(out[k] != nullptr && ldo[k] >= nI[k], BF_ERR_ARG, "bad output block in the list");
+      parts.push_back(bf_extract_part(h, nI[k], rows[k], nJ[k], cols[k]));
+      parts.back().out = out[k];
+      parts.back().ldo = ldo[k];
+    }
+    if (parts.empty()) return BF_OK;
+    extract_compact(h->dtype, h->pool, parts, nullptr, 0, static_cast<cudaStream_t>(stream), h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);

@@ -96,3 +96,29 @@ def test_extract_centre_edge_cases(L, lc):
     rng = np.random.default_rng(L + lc)
     I, J = rng.integers(0, bf.m, 23), rng.integers(0, bf.n, 17)
     assert oracle.rel_err(_get(h, I, J), oracle.bf_extract(bf, I, J)) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_extract_list(dtype):
+    """Alg. 3's list form (bf_extract_list): several (I, J) requests in one batched evaluation --
+    scattered, repeated, overlapping, single entries, empty ones -- each equals the oracle's entries
+    and the single-request bf_extract."""
+    bf = random_butterfly(L=7, leaf=16, r=16, seed=3, dtype=dtype)
+    rng = np.random.default_rng(7)
+    bf.row_perm = rng.permutation(bf.m).astype(np.int64)
+    bf.col_perm = rng.permutation(bf.n).astype(np.int64)
+    h = pkg.BFHandle(bf)
+    pairs = [(rng.integers(0, bf.m, 20), rng.integers(0, bf.n, 33)),
+             (np.arange(40, 90), np.arange(0, 16)),
+             ([3], [bf.n - 2]),
+             (rng.integers(0, bf.m, 20), rng.integers(0, bf.n, 33)),
+             ([], [1, 2]),
+             (np.arange(0, 16), rng.integers(0, bf.n, 200))]
+    got = h.extract_list(pairs)
+    for (I, J), G in zip(pairs, got):
+        assert G.shape == (len(I), len(J))
+        if len(I) == 0:
+            continue
+        ref = oracle.bf_extract(bf, I, J)
+        assert oracle.rel_err(G.cpu().numpy(), ref) <= TOL[dtype]
+        assert oracle.rel_err(G.cpu().numpy(), _get(h, I, J)) <= TOL[dtype]
