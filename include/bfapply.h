@@ -192,6 +192,12 @@ int bf_dist_exchange_blocks(bf_handle h, int op, int64_t* n_send, int64_t* send_
  * MMA-fragment order [r/8][re | im][lane][4] floats, see mma.cuh PolC64T); nrhs is padded to a
  * multiple of 32.  Either way the regions are moved as opaque bytes by the all-to-all. */
 int bf_dist_slab_format(bf_handle h, int32_t* fmt);
+/* The level whose slabs the split exchanges: lc for the generic split; for the fused split the
+ * level in [log2 nranks, L - log2 nranks] that minimises the window passes (plan.cu
+ * split_exchange_level; config 5 complex128: 6).  bf_dist_exchange_blocks' block indices are
+ * canonical indices at this level. */
+int bf_dist_exchange_level(bf_handle h, int op, int32_t* level);
+
 int bf_dist_local_rows(bf_handle h, int op, int64_t* rows_in, int64_t* rows_out,
                        int64_t* user_off_in, int64_t* user_off_out);
 int bf_dist_apply_pre(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx,

@@ -454,6 +454,7 @@ static void emit_C(PlanBuilder& pb, const Geom& G, const FBase& F, const Slabs& 
 // fused window-pass plan (fast.cuh) for uniform rank-16 butterflies
 // --------------------------------------------------------------------------------------
 struct FastPlan {
+  int lx = 0;  // split: the exchange level (split_exchange_level); lc otherwise
   std::vector<FastPass> passes;
   void* F = nullptr;
   int64_t entries = 0;
@@ -544,13 +545,39 @@ static void fill_step(CT* dst, int mg, int ki, Fn A, int mode) {
 }
 
 // op 0 = N (forward), 1 = C (adjoint; conjugate-transposed factor views)
+// The level at which a fused split exchanges its slabs.  Any level lx in [dp, L - dp] works: a
+// block (tau, nu) at level l depends only on X(S_nu) and feeds only Y(O_tau), so every level-l
+// block with nu (T_S level L - l >= dp) inside one column subtree can be computed by that
+// subtree's rank, and every one with tau (T_O level l >= dp) inside one row subtree by that
+// one's -- the paper's centre level lc is just one choice.  The exchange level splits the L
+// levels into the two sides' window passes, so it is chosen to minimise the pass count (each
+// pass is a slab round trip and a launch ramp): config 5 complex128 at 3-level windows exchanges
+// at level 6 (2 + 3 passes, as on one GPU) instead of 7 (3 + 3).  Ties: the level nearest lc.
+// Env BF_DIST_LX forces a level (A/B measurements).
+static int split_exchange_level(int L, int lc, int dp, int dmax) {
+  if (const char* e = getenv("BF_DIST_LX")) {
+    const int v = atoi(e);
+    if (v >= dp && v <= L - dp) return v;
+  }
+  int best = lc, bc = 1 << 30;
+  for (int lx = dp; lx <= L - dp; ++lx) {
+    const int c = (lx + dmax - 1) / dmax + (L - lx + dmax - 1) / dmax;
+    if (c < bc || (c == bc && std::abs(lx - lc) < std::abs(best - lc))) {
+      bc = c;
+      best = lx;
+    }
+  }
+  return best;
+}
+
 template <typename CT>
 static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, int opk, size_t* acct,
-                       int dp = -1, int dg = 0, bool x_contig = false) {
-  // dp >= 0: rank dg's share of the split over 2^dp GPUs: the W side (levels
-  // 0..lc, leaves of T_S) restricted to the column subtree dg at level dp, the R side (levels
-  // lc..L, leaves of T_O) to the row subtree dg; the pass that ends at the centre level writes
-  // the exchange layout and the pass that starts there reads it.
+                       int dp = -1, int dg = 0, bool x_contig = false, int lx_req = -1) {
+  // dp >= 0: rank dg's share of the split over 2^dp GPUs: the levels below the
+  // exchange level lx (W side and, when lx > lc, the first R stages; leaves of T_S) restricted
+  // to the column subtree dg at level dp, the levels above it (leaves of T_O) to the row subtree
+  // dg; the pass that ends at lx writes the exchange layout and the pass that starts there reads
+  // it (split_exchange_level).
   const int L = G.L, lc = G.lc;
   const bool split = dp >= 0;
   const int ks = fast_ks((int)sizeof(CT));
@@ -566,9 +593,11 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     }
   };
   lv.push_back(0);
+  const int lx = !split ? lc : (lx_req >= 0 ? lx_req : split_exchange_level(L, lc, dp, dmax));
+  FP.lx = lx;
   if (split) {
-    chunk(0, lc);
-    chunk(lc, L);
+    chunk(0, lx);
+    chunk(lx, L);
   } else {
     chunk(0, L);
     if (opk == 0 && sizeof(CT) == 16) {  // op N: the smaller passes first, so that the last pass
@@ -666,8 +695,8 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
     int d = 0;
     P.xin = P.xout = 0;
     if (split) {
-      P.wt_log = lc - dp;
-      P.wn_log = L - lc - dp;
+      P.wt_log = lx - dp;
+      P.wn_log = L - lx - dp;
     }
     if (k == 0 || k == np + 1) {
       // leaf launch (d = 0): window w = one leaf at level 0 (T_S leaf nu = b) or L (T_O leaf tau = a)
@@ -705,7 +734,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
       P.a_lo = 0;
       P.b_log = L - l1;
       P.b_lo = 0;
-      if (split && l1 <= lc) {  // W side: column subtree dg
+      if (split && l1 <= lx) {  // below the exchange: column subtree dg
         P.b_log = L - l1 - dp;
         P.b_lo = int64_t(dg) << P.b_log;
       } else if (split) {  // R side: row subtree dg
@@ -721,15 +750,15 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
         for (int l = std::max(l0, lc); l < l1; ++l) add(FK_PAIR_DOWN, l - l0, 0);      // R_l
         P.in_s = P.xleaf ? -1 : 0;
         P.out_s = d;
-        if (split && l1 == lc) P.xout = 1;  // send z^lc to the owner of tau
-        if (split && l0 == lc) P.xin = 2;   // receive from the owner of nu
+        if (split && l1 == lx) P.xout = 1;  // send the level-lx slabs to the owner of tau
+        if (split && l0 == lx) P.xin = 2;   // receive from the owner of nu
       } else {
         for (int l = l1 - 1; l >= l0 && l >= lc; --l) add(FK_PAIR_UP, l - l0, 0);        // R^H_l
         for (int l = std::min(l1, lc); l >= l0 + 1; --l) add(FK_PAIR_UP, l - 1 - l0, 0); // W^H_l
         P.in_s = P.xleaf ? -1 : d;
         P.out_s = 0;
-        if (split && l0 == lc) P.xout = 2;  // send to the owner of nu
-        if (split && l1 == lc) P.xin = 1;   // receive from the owner of tau
+        if (split && l0 == lx) P.xout = 2;  // send to the owner of nu
+        if (split && l1 == lx) P.xin = 1;   // receive from the owner of tau
       }
       if (P.xout || P.xin) FP.split = (int)passes.size() + (P.xout ? 1 : 0);
       if (fuse_out && k == np) {
@@ -2255,23 +2284,43 @@ int bf_dist_exchange_blocks(bf_handle h, int op, int64_t* n_send, int64_t* send_
   const int k = op == BF_OP_N ? 0 : 1;
   if (n_send) *n_send = (int64_t)h->send_blk[k].size();
   if (n_recv) *n_recv = (int64_t)h->recv_blk[k].size();
-  if (h->use_fast && k == 1) {
-    // fast format, op C: nu-major inside each peer's chunk
+  if (h->use_fast) {
+    // fast format: the blocks of the exchange level lx, per peer tau-major (op N) / nu-major (op C)
     const Geom& G = h->G;
+    const int lx = h->fast[k].lx;
     int p = 0;
     while ((1 << p) < h->nranks) ++p;
-    const int64_t wt = int64_t(1) << (G.lc - p), wn = int64_t(1) << (G.L - G.lc - p), g = h->rank;
+    const int64_t wt = int64_t(1) << (lx - p), wn = int64_t(1) << (G.L - lx - p), g = h->rank;
+    const int64_t nblk = (int64_t)h->nranks * wt * wn;
+    if (n_send) *n_send = nblk;
+    if (n_recv) *n_recv = nblk;
     int64_t is = 0, ir = 0;
-    for (int64_t q = 0; q < h->nranks; ++q)
-      for (int64_t j = 0; j < wn; ++j)
-        for (int64_t i = 0; i < wt; ++i) {
-          if (send_blocks) send_blocks[is++] = G.idx(G.lc, g * wt + i, q * wn + j);  // sender owns tau
-          if (recv_blocks) recv_blocks[ir++] = G.idx(G.lc, q * wt + i, g * wn + j);  // receiver owns nu
-        }
+    if (k == 0) {
+      for (int64_t q = 0; q < h->nranks; ++q)
+        for (int64_t i = 0; i < wt; ++i)
+          for (int64_t j = 0; j < wn; ++j) {
+            if (send_blocks) send_blocks[is++] = G.idx(lx, q * wt + i, g * wn + j);  // sender owns nu
+            if (recv_blocks) recv_blocks[ir++] = G.idx(lx, g * wt + i, q * wn + j);  // receiver owns tau
+          }
+    } else {
+      for (int64_t q = 0; q < h->nranks; ++q)
+        for (int64_t j = 0; j < wn; ++j)
+          for (int64_t i = 0; i < wt; ++i) {
+            if (send_blocks) send_blocks[is++] = G.idx(lx, g * wt + i, q * wn + j);  // sender owns tau
+            if (recv_blocks) recv_blocks[ir++] = G.idx(lx, q * wt + i, g * wn + j);  // receiver owns nu
+          }
+    }
     return BF_OK;
   }
   if (send_blocks) std::copy(h->send_blk[k].begin(), h->send_blk[k].end(), send_blocks);
   if (recv_blocks) std::copy(h->recv_blk[k].begin(), h->recv_blk[k].end(), recv_blocks);
+  return BF_OK;
+}
+
+int bf_dist_exchange_level(bf_handle h, int op, int32_t* level) {
+  if (!h || !level) return fail(Err{BF_ERR_ARG, "NULL argument"});
+  if (!h->dist) return fail(Err{BF_ERR_ARG, "not a distributed handle"});
+  *level = h->use_fast ? h->fast[op == BF_OP_N ? 0 : 1].lx : h->G.lc;
   return BF_OK;
 }
 

@@ -33,6 +33,7 @@ _SIGS = [
     ("bf_dist_exchange_blocks", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("bf_dist_slab_format", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    ("bf_dist_exchange_level", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
     ("bf_dist_apply_pre_p2p", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                         C.c_size_t, C.POINTER(C.c_void_p), C.c_void_p]),
 ]
@@ -101,6 +102,13 @@ class DistBFHandle:
             self.h, OPS[op], C.byref(ns), s.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(nr),
             r.ctypes.data_as(C.POINTER(C.c_int64))))
         return s[:ns.value], r[:nr.value]
+
+    def exchange_level(self, op: str = "N") -> int:
+        """The level whose slabs the exchange moves (bf_dist_exchange_level): lc on the generic
+        split, the pass-count-minimising level on the fused one."""
+        v = C.c_int32()
+        _check("bf_dist_exchange_level", _lib().bf_dist_exchange_level(self.h, OPS[op], C.byref(v)))
+        return v.value
 
     def slab_format(self) -> int:
         """0: generic block-contiguous send / recv regions; 1: fused-kernel half-slab chunks

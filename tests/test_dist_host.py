@@ -113,9 +113,12 @@ def _worker(rank, world, port, kind, q):
             wb, so, ro, sc, rc = h.layout(op, nrhs)
             sblk, rblk = h.exchange_blocks(op)
             size = rank_row if op == "N" else rank_col
-            if fmt == 1:
-                _check_fast(h, op, nrhs, wb, so, ro, sc, rc, sblk, rblk, L, lc, p, rank, world)
+            if fmt == 1:  # the fused split exchanges at the pass-count-minimising level
+                lx = h.exchange_level(op)
+                assert p <= lx <= L - p
+                _check_fast(h, op, nrhs, wb, so, ro, sc, rc, sblk, rblk, L, lx, p, rank, world)
                 continue
+            assert h.exchange_level(op) == lc
             tau, nu = sblk >> (L - lc), sblk & ((1 << (L - lc)) - 1)
             # sender owns the column subtree (op N) / row subtree (op C)
             own = (nu >> (L - lc - p)) if op == "N" else (tau >> (lc - p))
