@@ -89,6 +89,32 @@ struct XProd {
   int32_t a_rs, a_cs, m, kk, w, in_ld, out_ld, acc;
 };
 void launch_xprod(int dtype, int64_t np, const void* P, const void* pool, const void* S, void* O, cudaStream_t st);
+
+// One butterfly's share of a level-wise extraction (extract.cu k_xlevel; bf_extract / hodbf_extract,
+// Alg. 3): the handle's device geometry tables, the request's blob section and its two slab
+// buffers.  Slabs of level l are [pos of tau among the touched T_O nodes][rank row < Rl][request
+// column j], so every output element of every stage is one independent dot product.
+struct XLPart {
+  const int32_t* rr;    // row ranks, levels lc..L: rr[(l - lc) nb + idx]
+  const int32_t* rc;    // column ranks, levels 0..lc: rc[l nb + idx]
+  const int64_t* roff;  // R block offsets (pool, from fr), levels lc..L-1
+  const int64_t* woff;  // W block offsets (from fw), levels 1..lc: woff[(l - 1) nb + idx]
+  const int64_t* boff;  // B block offsets (from fb), level lc
+  int64_t fr, fb, fw;   // pool bases of the part's R / B / W sections
+  int32_t L, lc, nI, nJ;
+  void* out;            // out[orow[i] + ocol[j] ldo]
+  int64_t ldo;
+  int64_t slab[2];      // element offsets of the part's ping-pong slab buffers
+  // int64 offsets into the query blob: per column tj (leaf), vtoff, ocol; per row ti (leaf), uoff,
+  // ustr, orow, ypos (position of the row's leaf among the touched level-L nodes); per level l
+  // tau_off[l] (start of level l in taus / ppos), taus (touched T_O nodes, ascending), ppos (each
+  // one's parent position in level l - 1's list); Rz[l] (l <= lc) / Ry[l - lc] rows per slab
+  int64_t o_tj, o_vtoff, o_ocol, o_ti, o_uoff, o_ustr, o_orow, o_ypos, o_toff, o_taus, o_ppos, o_rz, o_ry;
+};
+// stage s of every part (0 = Vt gather, 1..lc W, lc+1 B, lc+2..L+1 R, L+2 U rows, scattered to out);
+// wpre: nparts + 1 prefix sums of the parts' work items (output elements) at stage s
+void launch_xlevel(int dtype, int s, int nparts, const XLPart* P, const int64_t* wpre, int64_t total,
+                   const int64_t* blob, const void* pool, void* S, cudaStream_t st);
 void launch_xgather_vt(int dtype, int64_t n, const int64_t* e, const void* pool, void* S, cudaStream_t st);
 void launch_xscatter(int dtype, int64_t nI, int64_t nJ, const int64_t* orow, const int64_t* ocol, const void* T, void* out,
                      int64_t ldo, cudaStream_t st);

@@ -1,5 +1,3 @@
-#include <map>
-#include <chrono>
 // Host side of libbfapply: descriptor validation, device upload, and the per-op plans
 // (Task / Term tables) that turn Eq. (3.3) into a short sequence of batched launches.
 //
@@ -16,9 +14,11 @@
 // owns rank x nrhs entries (nrhs fastest), so no stage ever overwrites another stage's
 // data and no atomics are needed (each output slab is written by exactly one task).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -273,10 +273,20 @@ struct Touch {
 };
 
 // grow-only device scratch of the extraction calls of one handle
+// Device copies of a butterfly geometry's rank and block-offset tables (the level-wise
+// extraction, k_xlevel), uploaded on a handle's first extraction.
+struct XGeomDev {
+  void* buf = nullptr;
+  const int32_t *rr = nullptr, *rc = nullptr;
+  const int64_t *roff = nullptr, *woff = nullptr, *boff = nullptr;
+  std::vector<int64_t> Rz, Ry;  // rows per slab: max column rank at l = 0..lc, max row rank at l = lc..L
+};
+
 struct XScratch {
   std::mutex mu;
   void* buf = nullptr;
   size_t bytes = 0;
+  std::map<const void*, XGeomDev> geo;  // keyed by the Geom (owned by the handle, never moved)
   void* get(size_t need) {
     if (bytes < need) {
       if (buf) cudaFree(buf);
@@ -287,8 +297,23 @@ struct XScratch {
     }
     return buf;
   }
+  void* hbuf = nullptr;  // pinned staging of the per-request tables (a pageable copy is staged)
+  size_t hbytes = 0;
+  void* host(size_t need) {
+    if (hbytes < need) {
+      if (hbuf) cudaFreeHost(hbuf);
+      hbuf = nullptr;
+      hbytes = 0;
+      BF_CK(cudaHostAlloc(&hbuf, need, cudaHostAllocDefault));
+      hbytes = need;
+    }
+    return hbuf;
+  }
   ~XScratch() {
     if (buf) cudaFree(buf);
+    if (hbuf) cudaFreeHost(hbuf);
+    for (auto& g : geo)
+      if (g.second.buf) cudaFree(g.second.buf);
   }
 };
 
@@ -2725,10 +2750,207 @@ static void extract_compact(int dtype, const void* pool, std::vector<XPart>& par
   }
 }
 
+// The device geometry tables of G (cached in xs; caller holds xs.mu).
+static const XGeomDev& xgeom_dev(XScratch& xs, const Geom& G) {
+  auto it = xs.geo.find(&G);
+  if (it != xs.geo.end()) return it->second;
+  const int L = G.L, lc = G.lc;
+  const int64_t nb = G.nb;
+  std::vector<int64_t> roff((size_t)std::max<int64_t>(1, (L - lc) * nb), 0), woff((size_t)std::max<int64_t>(1, lc * nb), 0);
+  for (int l = lc; l < L; ++l) std::copy(G.r_off[l].begin(), G.r_off[l].begin() + nb, roff.begin() + (l - lc) * nb);
+  for (int l = 1; l <= lc; ++l) std::copy(G.w_off[l].begin(), G.w_off[l].begin() + nb, woff.begin() + (l - 1) * nb);
+  const size_t brr = align256(G.rr.size() * 4), brc = align256(G.rc.size() * 4), bro = align256(roff.size() * 8),
+               bwo = align256(woff.size() * 8), bbo = align256(std::max<size_t>(1, G.b_off.size()) * 8);
+  XGeomDev d;
+  BF_CK(cudaMalloc(&d.buf, brr + brc + bro + bwo + bbo));
+  char* b = static_cast<char*>(d.buf);
+  BF_CK(cudaMemcpy(b, G.rr.data(), G.rr.size() * 4, cudaMemcpyHostToDevice));
+  BF_CK(cudaMemcpy(b + brr, G.rc.data(), G.rc.size() * 4, cudaMemcpyHostToDevice));
+  BF_CK(cudaMemcpy(b + brr + brc, roff.data(), roff.size() * 8, cudaMemcpyHostToDevice));
+  BF_CK(cudaMemcpy(b + brr + brc + bro, woff.data(), woff.size() * 8, cudaMemcpyHostToDevice));
+  if (!G.b_off.empty()) BF_CK(cudaMemcpy(b + brr + brc + bro + bwo, G.b_off.data(), G.b_off.size() * 8, cudaMemcpyHostToDevice));
+  d.rr = reinterpret_cast<const int32_t*>(b);
+  d.rc = reinterpret_cast<const int32_t*>(b + brr);
+  d.roff = reinterpret_cast<const int64_t*>(b + brr + brc);
+  d.woff = reinterpret_cast<const int64_t*>(b + brr + brc + bro);
+  d.boff = reinterpret_cast<const int64_t*>(b + brr + brc + bro + bwo);
+  d.Rz.assign(lc + 1, 0);
+  d.Ry.assign(L - lc + 1, 0);
+  for (int l = 0; l <= lc; ++l)
+    for (int64_t i = 0; i < nb; ++i) d.Rz[l] = std::max<int64_t>(d.Rz[l], G.c(l, i));
+  for (int l = lc; l <= L; ++l)
+    for (int64_t i = 0; i < nb; ++i) d.Ry[l - lc] = std::max<int64_t>(d.Ry[l - lc], G.r(l, i));
+  for (auto& v : d.Rz) v = std::max<int64_t>(v, 1);
+  for (auto& v : d.Ry) v = std::max<int64_t>(v, 1);
+  return xs.geo.emplace(&G, std::move(d)).first->second;
+}
+
+// Level-wise extraction (Alg. 3 extract_BF: only the blocks (l, tau, nu) with tau an
+// ancestor of a requested row's leaf and nu one of a requested column's leaf, each block multiplied
+// only at the request columns under it).  The host work per part is O((|I| + |J|) L):
+// the touched T_O nodes per level and a few index arrays; the products themselves are enumerated
+// on the device (k_xlevel: one launch per stage for all parts, one thread per output element of
+// the level's [touched tau][rank row][request column] slab).  Synchronous on `st`.
+static void extract_levels(int dtype, const void* pool, std::vector<XPart>& parts, void* out, int64_t ldo,
+                           cudaStream_t st, XScratch& xs) {
+  const size_t cs = csize(dtype);
+  static const bool timing = getenv("BF_EXTRACT_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::lock_guard<std::mutex> lk(xs.mu);
+  std::vector<XLPart> P;
+  std::vector<int64_t> blob;
+  std::vector<std::vector<int64_t>> work;  // per part: output elements per stage
+  int smax = 0;
+  int64_t slab = 0;
+  for (XPart& pt : parts) {
+    const Geom& G = *pt.G;
+    const XQuery& q = pt.q;
+    const int L = G.L, lc = G.lc;
+    const int64_t nI = (int64_t)q.pr.size(), nJ = (int64_t)q.pc.size();
+    if (nI == 0 || nJ == 0) continue;
+    const XGeomDev& D = xgeom_dev(xs, G);
+    XLPart x{};
+    x.rr = D.rr;
+    x.rc = D.rc;
+    x.roff = D.roff;
+    x.woff = D.woff;
+    x.boff = D.boff;
+    x.fr = pt.F.r;
+    x.fb = pt.F.b;
+    x.fw = pt.F.w;
+    x.L = L;
+    x.lc = lc;
+    x.nI = (int32_t)nI;
+    x.nJ = (int32_t)nJ;
+    x.out = pt.out ? pt.out : out;
+    x.ldo = pt.out ? pt.ldo : ldo;
+    auto put = [&](int64_t& off, const std::vector<int64_t>& v) {
+      off = (int64_t)blob.size();
+      blob.insert(blob.end(), v.begin(), v.end());
+    };
+    std::vector<int64_t> tj(nJ), ti(nI);
+    for (int64_t j = 0; j < nJ; ++j) tj[j] = leaf_of(G.clp, q.pc[j]);
+    for (int64_t i = 0; i < nI; ++i) ti[i] = leaf_of(G.rlp, q.pr[i]);
+    // touched T_O nodes per level (ascending) and each one's parent position one level up
+    std::vector<int64_t> srt(ti);
+    std::sort(srt.begin(), srt.end());
+    srt.erase(std::unique(srt.begin(), srt.end()), srt.end());
+    std::vector<int64_t> toff(L + 2, 0), taus, ppos;
+    std::vector<int64_t> prev;
+    for (int l = 0; l <= L; ++l) {
+      toff[l] = (int64_t)taus.size();
+      std::vector<int64_t> cur;
+      for (int64_t v : srt) {
+        const int64_t a = v >> (L - l);
+        if (cur.empty() || cur.back() != a) cur.push_back(a);
+      }
+      size_t k = 0;
+      for (int64_t a : cur) {  // parent a >> 1 in prev (both ascending)
+        int64_t pp = 0;
+        if (l > 0) {
+          while (k < prev.size() && prev[k] < (a >> 1)) ++k;
+          pp = (int64_t)k;
+        }
+        taus.push_back(a);
+        ppos.push_back(pp);
+      }
+      prev.swap(cur);
+    }
+    toff[L + 1] = (int64_t)taus.size();
+    std::vector<int64_t> ypos(nI);
+    for (int64_t i = 0; i < nI; ++i)
+      ypos[i] = (int64_t)(std::lower_bound(taus.begin() + toff[L], taus.begin() + toff[L + 1], ti[i]) -
+                          (taus.begin() + toff[L]));
+    put(x.o_tj, tj);
+    put(x.o_vtoff, q.vtoff);
+    put(x.o_ocol, q.ocol);
+    put(x.o_ti, ti);
+    put(x.o_uoff, q.uoff);
+    put(x.o_ustr, q.ustr);
+    put(x.o_orow, q.orow);
+    put(x.o_ypos, ypos);
+    put(x.o_toff, toff);
+    put(x.o_taus, taus);
+    put(x.o_ppos, ppos);
+    put(x.o_rz, D.Rz);
+    put(x.o_ry, D.Ry);
+    auto nt = [&](int l) { return toff[l + 1] - toff[l]; };
+    // stage s: slab elements written (sz) and threads (w: one per 8-row chunk of a slab column)
+    std::vector<int64_t> w((size_t)L + 3, 0), sz((size_t)L + 3, 0);
+    auto ch8 = [](int64_t R) { return (R + 7) / 8; };
+    sz[0] = w[0] = D.Rz[0] * nJ;
+    for (int l = 1; l <= lc; ++l) {
+      sz[l] = nt(l) * D.Rz[l] * nJ;
+      w[l] = nt(l) * ch8(D.Rz[l]) * nJ;
+    }
+    sz[lc + 1] = nt(lc) * D.Ry[0] * nJ;
+    w[lc + 1] = nt(lc) * ch8(D.Ry[0]) * nJ;
+    for (int l = lc; l < L; ++l) {
+      sz[l + 2] = nt(l + 1) * D.Ry[l + 1 - lc] * nJ;
+      w[l + 2] = nt(l + 1) * ch8(D.Ry[l + 1 - lc]) * nJ;
+    }
+    w[L + 2] = nI * nJ;
+    int64_t mx = 0;
+    for (int s2 = 0; s2 <= L + 1; ++s2) mx = std::max(mx, sz[s2]);
+    x.slab[0] = slab;
+    x.slab[1] = slab + mx;
+    slab += 2 * mx;
+    smax = std::max(smax, L + 2);
+    P.push_back(x);
+    work.push_back(std::move(w));
+  }
+  if (P.empty()) return;
+  const int np = (int)P.size(), ns = smax + 1;
+  // per stage: prefix sums of the parts' work
+  std::vector<int64_t> wpre((size_t)ns * (np + 1), 0), tot(ns, 0);
+  for (int s2 = 0; s2 < ns; ++s2) {
+    int64_t a = 0;
+    for (int k = 0; k < np; ++k) {
+      wpre[(size_t)s2 * (np + 1) + k] = a;
+      if (s2 < (int)work[k].size()) a += work[k][s2];
+    }
+    wpre[(size_t)s2 * (np + 1) + np] = a;
+    tot[s2] = a;
+  }
+  const size_t bS = align256((size_t)slab * cs), bP = align256(P.size() * sizeof(XLPart)),
+               bW = align256(wpre.size() * 8), bB = align256(blob.size() * 8);
+  char* base = static_cast<char*>(xs.get(bS + bP + bW + bB));
+  char* host = static_cast<char*>(xs.host(bP + bW + bB));  // the previous call synchronised: free
+  memcpy(host, P.data(), P.size() * sizeof(XLPart));
+  memcpy(host + bP, wpre.data(), wpre.size() * 8);
+  memcpy(host + bP + bW, blob.data(), blob.size() * 8);
+  BF_CK(cudaMemcpyAsync(base + bS, host, bP + bW + bB, cudaMemcpyHostToDevice, st));
+  const auto t1 = std::chrono::steady_clock::now();
+  const XLPart* dP = reinterpret_cast<const XLPart*>(base + bS);
+  const int64_t* dW = reinterpret_cast<const int64_t*>(base + bS + bP);
+  const int64_t* dB = reinterpret_cast<const int64_t*>(base + bS + bP + bW);
+  // one launch per stage (a cooperative single launch with grid barriers measured slower: every
+  // stage is a chain of dependent table loads either way)
+  for (int s2 = 0; s2 < ns; ++s2)
+    launch_xlevel(dtype, s2, np, dP, dW + (size_t)s2 * (np + 1), tot[s2], dB, pool, base, st);
+  BF_CK(cudaGetLastError());
+  BF_CK(cudaStreamSynchronize(st));
+  if (timing) {
+    const auto t2 = std::chrono::steady_clock::now();
+    int64_t all = 0;
+    for (int64_t v : tot) all += v;
+    fprintf(stderr, "bf_extract (levels): plan %.3f ms, upload + device %.3f ms, %d parts, %lld outputs, %lld slab entries\n",
+            std::chrono::duration<double, std::milli>(t1 - t0).count(),
+            std::chrono::duration<double, std::milli>(t2 - t1).count(), np, (long long)all, (long long)slab);
+  }
+}
+
 // BF_EXTRACT_LEGACY selects the round-1 plan (per-query generic rounds over full-width slabs)
 static bool extract_legacy() {
   static const bool v = getenv("BF_EXTRACT_LEGACY") != nullptr;
   return v;
+}
+// BF_EXTRACT_COMPACT selects the host-enumerated compact plan (extract_compact) over extract_levels
+static void extract_run(int dtype, const void* pool, std::vector<XPart>& parts, void* out, int64_t ldo, cudaStream_t st,
+                        XScratch& xs) {
+  static const bool compact = getenv("BF_EXTRACT_COMPACT") != nullptr;
+  if (compact) extract_compact(dtype, pool, parts, out, ldo, st, xs);
+  else extract_levels(dtype, pool, parts, out, ldo, st, xs);
 }
 
 // Sub-matrices of one or more butterflies stored in `pool`, as partial matvecs (Alg. 3
@@ -2941,7 +3163,7 @@ int bf_extract(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const i
     if (extract_legacy())
       extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
     else
-      extract_compact(h->dtype, h->pool, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
+      extract_run(h->dtype, h->pool, parts, out, ldo, static_cast<cudaStream_t>(stream), h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
@@ -2968,7 +3190,7 @@ int bf_extract_list(bf_handle h, int64_t npairs, const int64_t* nI, const int64_
       parts.back().ldo = ldo[k];
     }
     if (parts.empty()) return BF_OK;
-    extract_compact(h->dtype, h->pool, parts, nullptr, 0, static_cast<cudaStream_t>(stream), h->xs);
+    extract_run(h->dtype, h->pool, parts, nullptr, 0, static_cast<cudaStream_t>(stream), h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
@@ -3058,7 +3280,7 @@ int hodbf_extract(hodbf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, c
     if (extract_legacy())
       extract_multi(h->dtype, h->pool, h->m3, parts, out, ldo, st, h->xs);
     else
-      extract_compact(h->dtype, h->pool, parts, out, ldo, st, h->xs);
+      extract_run(h->dtype, h->pool, parts, out, ldo, st, h->xs);
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);

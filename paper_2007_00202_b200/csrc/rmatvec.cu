@@ -649,6 +649,137 @@ __global__ void k_xscatter(int64_t nI, int64_t nJ, const int64_t* __restrict__ o
   }
 }
 
+// Level-wise extraction (Alg. 3; every touched block multiplied once, at the columns
+// that need it): stage s of every part in one launch.  A part's slab at level l is
+// [pos][r < Rl][j < nJ]: request column j belongs to exactly one T_S node per level (nu = tj[j] >> l)
+// and, one level down, to exactly one of its children, so every slab column of a block is a small
+// matrix-vector product with that child's block.  One thread per (pos, 8-row chunk, column j):
+// the input column is read once per 8 output rows, the factor rows of a k are 8 consecutive
+// entries.  Rows r >= the block's rank are neither written nor read.
+constexpr int XL_RC = 8;
+template <typename V>
+__device__ __forceinline__ void xl_dot(const V* __restrict__ a, int64_t lda, int nr, const V* __restrict__ y, int K,
+                                       int64_t ldy, V* __restrict__ o, int64_t ldo) {
+  V acc[XL_RC];
+#pragma unroll
+  for (int q = 0; q < XL_RC; ++q) acc[q] = cmk<V>(0, 0);
+  for (int k = 0; k < K; ++k) {
+    const V yk = y[k * ldy];
+    const V* ak = a + k * lda;
+#pragma unroll
+    for (int q = 0; q < XL_RC; ++q)
+      if (q < nr) acc[q] = cadd(acc[q], cmul(ak[q], yk));
+  }
+#pragma unroll
+  for (int q = 0; q < XL_RC; ++q)
+    if (q < nr) o[q * ldo] = acc[q];
+}
+
+template <typename V>
+__device__ __forceinline__ void xl_stage(int s, int np, const XLPart* __restrict__ P, const int64_t* __restrict__ wpre,
+                                         const int64_t* __restrict__ B, const V* __restrict__ pool, V* __restrict__ S) {
+  const int64_t tot = wpre[np];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = np - 1;  // the part: last k with wpre[k] <= e
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (wpre[mid] <= e) lo = mid;
+      else hi = mid - 1;
+    }
+    const XLPart& p = P[lo];
+    int64_t x = e - wpre[lo];
+    const int nJ = p.nJ, L = p.L, lc = p.lc;
+    const int64_t nb = int64_t(1) << L;
+    const int j = (int)(x % nJ);
+    x /= nJ;
+    const V* in = S + p.slab[(s - 1) & 1];
+    V* o = S + p.slab[s & 1];
+    if (s == 0) {  // z^0_nu(r, j) = Vt_nu(r, column j)
+      const int64_t t = B[p.o_tj + j];
+      const int r = (int)x;
+      if (r >= p.rc[t]) continue;
+      o[(int64_t)r * nJ + j] = pool[B[p.o_vtoff + j] + r];
+    } else if (s <= L + 1) {
+      const int64_t t = B[p.o_tj + j];  // the column's leaf (T_S level-0 node)
+      const int l = s <= lc ? s : s == lc + 1 ? lc : s - 1;  // output level
+      const int64_t* rs = s <= lc ? B + p.o_rz : B + p.o_ry - lc;  // rows per slab, indexed by level
+      const int R = (int)rs[l];
+      const int nch = (R + XL_RC - 1) / XL_RC;
+      const int r0 = (int)(x % nch) * XL_RC;
+      const int64_t pos = x / nch;
+      const int64_t tau = (l == 0) ? 0 : B[p.o_taus + B[p.o_toff + l] + pos];
+      const int64_t nu = t >> l, io = (tau << (L - l)) | nu;
+      const V* a;
+      const V* y;
+      int64_t lda;
+      int K, rows;
+      if (s <= lc) {  // W stage l: z^l_{tau,nu} = W_{tau,nu} [z^{l-1}_{tau>>1,2nu}; z^{l-1}_{tau>>1,2nu+1}]
+        const int c = p.rc[l * nb + io];
+        if (r0 >= c) continue;
+        rows = c;
+        const int sb = (int)((t >> (l - 1)) & 1);
+        const int64_t tp = l == 1 ? 0 : tau >> 1, pp = l == 1 ? 0 : B[p.o_ppos + B[p.o_toff + l] + pos];
+        const int64_t ic0 = (tp << (L - l + 1)) | (2 * nu);
+        const int c0 = p.rc[(l - 1) * nb + ic0];
+        K = sb ? p.rc[(l - 1) * nb + ic0 + 1] : c0;
+        lda = c;
+        a = pool + p.fw + p.woff[(l - 1) * nb + io] + r0 + (int64_t)(sb ? c0 : 0) * c;
+        y = in + pp * B[p.o_rz + l - 1] * nJ + j;
+      } else if (s == lc + 1) {  // centre: y^lc_{tau,nu} = B_{tau,nu} z^lc_{tau,nu}
+        const int ri = p.rr[io];
+        if (r0 >= ri) continue;
+        rows = ri;
+        K = p.rc[lc * nb + io];
+        lda = ri;
+        a = pool + p.fb + p.boff[io] + r0;
+        y = in + pos * B[p.o_rz + lc] * nJ + j;
+      } else {  // R stage l - 1 -> l (gather form): y^l_{tau,nu} = R_{tau>>1, 2nu+s}[rows of child tau & 1] y^{l-1}
+        const int32_t* rr1 = p.rr + (int64_t)(l - lc) * nb;
+        const int ro = rr1[io];
+        if (r0 >= ro) continue;
+        rows = ro;
+        const int64_t a2 = tau >> 1, ch = t >> (l - 1), i = (a2 << (L - l + 1)) | ch;
+        const int rt = rr1[((2 * a2) << (L - l)) | nu], rb = rr1[((2 * a2 + 1) << (L - l)) | nu];
+        K = p.rr[(int64_t)(l - 1 - lc) * nb + i];
+        lda = rt + rb;
+        a = pool + p.fr + p.roff[(int64_t)(l - 1 - lc) * nb + i] + ((tau & 1) ? rt : 0) + r0;
+        const int64_t pp = B[p.o_ppos + B[p.o_toff + l] + pos];
+        y = in + pp * B[p.o_ry + l - 1 - lc] * nJ + j;
+      }
+      xl_dot(a, lda, min(XL_RC, rows - r0), y, K, (int64_t)nJ, o + (pos * R + r0) * nJ + j, (int64_t)nJ);
+    } else {  // U rows: K(row i, column j) = U_tau(row, :) y^L_tau(:, j)
+      const int i = (int)x;
+      const int64_t tau = B[p.o_ti + i];
+      const int kn = p.rr[(int64_t)(L - lc) * nb + tau];
+      const V* a = pool + B[p.o_uoff + i];
+      const int64_t us = B[p.o_ustr + i];
+      const V* y = in + B[p.o_ypos + i] * B[p.o_ry + L - lc] * nJ + j;
+      V acc = cmk<V>(0, 0);
+      for (int k = 0; k < kn; ++k) acc = cadd(acc, cmul(a[k * us], y[(int64_t)k * nJ]));
+      static_cast<V*>(p.out)[B[p.o_orow + i] + B[p.o_ocol + j] * p.ldo] = acc;
+    }
+  }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) k_xlevel(int s, int np, const XLPart* __restrict__ P,
+                                                const int64_t* __restrict__ wpre, const int64_t* __restrict__ B,
+                                                const V* __restrict__ pool, V* __restrict__ S) {
+  xl_stage(s, np, P, wpre, B, pool, S);
+}
+
+void launch_xlevel(int dtype, int s, int nparts, const XLPart* P, const int64_t* wpre, int64_t total,
+                   const int64_t* blob, const void* pool, void* S, cudaStream_t st) {
+  if (total <= 0 || nparts <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (dtype == BF_C128)
+    k_xlevel<double2><<<grid, 256, 0, st>>>(s, nparts, P, wpre, blob, static_cast<const double2*>(pool),
+                                            static_cast<double2*>(S));
+  else
+    k_xlevel<float2><<<grid, 256, 0, st>>>(s, nparts, P, wpre, blob, static_cast<const float2*>(pool),
+                                           static_cast<float2*>(S));
+}
+
 void launch_xprod(int dtype, int64_t np, const void* P, const void* pool, const void* S, void* O, cudaStream_t st) {
   if (np == 0) return;
   const int64_t blocks = std::min<int64_t>((np + 7) / 8, 65535 * 4);
