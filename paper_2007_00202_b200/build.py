@@ -8,7 +8,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRC = [os.path.join(PKG, "csrc", f) for f in ("kernels.cu", "fast.cu", "leaf.cu", "plan.cu", "rmatvec.cu")]
+SRC = [os.path.join(PKG, "csrc", f) for f in ("kernels.cu", "fast.cu", "leaf.cu", "plan.cu", "rmatvec.cu", "tile_umma.cu")]
 LIB = os.path.join(PKG, "libbfapply.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",

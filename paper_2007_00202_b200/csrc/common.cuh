@@ -81,6 +81,8 @@ struct StageArgs {
 };
 
 void launch_round(int dtype, const Round& r, StageArgs a, cudaStream_t st);
+// complex64 rounds on tcgen05 (tile_umma.cu): one CTA per (unit, 128-column rhs tile)
+void launch_tile_umma(const StageArgs& a, cudaStream_t st);
 // One product of the compact extraction (bf_extract, Alg. 3): out[out_off + i out_ld + j] (+ if acc)=
 // sum_k pool[a_off + i a_rs + k a_cs] in[in_off + k in_ld + j], i < m, j < w, k < kk (row-major
 // compact slabs, rmatvec.cu k_xprod)

@@ -16,8 +16,9 @@
 // Operand stream.  Every op is a sequence of MMA k-steps; the A operand (factor block) of one
 // k-step of one slot is one 1 KB fragment-ordered record.  At create time each op's factors are
 // laid out window-major as [step][slot][1 KB], so any run of consecutive k-steps of all slots
-// is one contiguous byte range that the producer warp streams into 16 KB pages of a shared-
-// memory ring with TMA bulk copies.
+// is one contiguous byte range, streamed into the 32 KB pages of a shared-memory ring with TMA
+// bulk copies.  There is no producer warp: whichever compute warp releases a page last re-arms it
+// with the page NP ahead (fast.cu).
 #pragma once
 
 #include <cuda.h>

@@ -550,6 +550,14 @@ static void launch_generic(const Round& r, StageArgs a, cudaStream_t st) {
     }
     return;
   }
+  // complex64 with >= 64 right-hand sides, rounds between slab levels: the tcgen05 kernel (M = 128
+  // rhs per CTA tile; env BF_UMMA = 0 keeps the mma.sync row tiles, for A/B measurements)
+  static const int umma = getenv("BF_UMMA") ? atoi(getenv("BF_UMMA")) : 1;
+  if (sizeof(V) == 8 && umma && mode && a.nrhs >= 64 && !a.cols &&
+      (umma == 2 || (r.out_kind == 0 && r.user_in == 0))) {
+    launch_tile_umma(a, st);
+    return;
+  }
   if (sizeof(V) == 16)
     launch_tile<PolC128<2>>(grid, a, st);
   else

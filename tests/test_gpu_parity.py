@@ -117,6 +117,25 @@ def test_ragged(L, lc, seed, rmin, rmax, dtype):
         assert err <= TOL[dtype], (op, err)
 
 
+@pytest.mark.parametrize("nrhs", [64, 100, 129, 256])
+def test_ragged_c64_wide(nrhs):
+    """complex64 with >= 64 right-hand sides runs on the tcgen05 tile kernel (tile_umma.cu):
+    ragged ranks 0..70 (K up to 140: several 16-row chunks, two terms per task), partial and
+    multiple 128-column tiles, ops N / C / T, against the dense definition."""
+    L, lc, seed = 5, 2, 7
+    rng = np.random.default_rng(seed)
+    nb = 1 << L
+    rows = rng.integers(0, 40, nb)
+    cols = rng.integers(1, 40, nb)
+    bf = random_ranks_butterfly(L, rows, cols, seed=seed, rmin=0, rmax=70, lc=lc, dtype=np.complex64)
+    h = pkg.BFHandle(bf)
+    K = oracle.bf_dense(bf)
+    for op in ("N", "C", "T"):
+        X = random_rhs(bf.n if op == "N" else bf.m, nrhs, seed=seed + nrhs, dtype=np.complex64)
+        err = oracle.rel_err(run(h, X, op), oracle.apply_op(K, X, op))
+        assert err <= TOL[np.complex64], (op, err)
+
+
 def test_L0_dense_block():
     rng = np.random.default_rng(0)
     Bm = rng.standard_normal((70, 50)) + 1j * rng.standard_normal((70, 50))
