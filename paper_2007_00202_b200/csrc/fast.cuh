@@ -1,5 +1,6 @@
-// Fast path for uniform-rank butterflies (rank 16, power-of-two leaves that are multiples of 16,
-// at most 256): one apply = a leaf launch, a few window passes, a leaf launch.
+// Fast path for rank-16 butterflies (power-of-two leaves that are multiples of 16, at most 256;
+// ranks <= 16 are zero-padded to 16 at create, plan.cu pad_rank16): one apply = a leaf launch, a
+// few window passes, a leaf launch.
 //
 // Leaf launches (leaf.cu): every leaf product of Eq. (3.3)'s outer factors
 // (V^0 = blkdiag(Vt_nu) on the input side, U^L = blkdiag(U_tau) on the output side)

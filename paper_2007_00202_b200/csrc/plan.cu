@@ -488,13 +488,15 @@ struct FastPlan {
   int split = -1;           // multi-GPU split: passes [0, split) before the exchange, the rest after
 };
 
-static bool fast_eligible(const Geom& G, int dtype) {
+// exact: every rank is 16 (the factors go to the fused kernels as they are); otherwise ranks
+// <= 16 are accepted and the factors are zero-padded to rank 16 at create (pad_rank16)
+static bool fast_eligible(const Geom& G, int dtype, bool exact = true) {
   (void)dtype;
   if (G.L < 1) return false;
   for (int32_t v : G.rr)
-    if (v != FAST_RANK) return false;
+    if (exact ? v != FAST_RANK : v > FAST_RANK) return false;
   for (int32_t v : G.rc)
-    if (v != FAST_RANK) return false;
+    if (exact ? v != FAST_RANK : v > FAST_RANK) return false;
   const int64_t lr = G.mt(0), lcn = G.nv(0);
   // power-of-two leaves, multiples of 16 (whole MMA row groups / k-steps), at most 256 rows
   if (lr < 16 || lcn < 16 || lr > 256 || lcn > 256) return false;
@@ -517,6 +519,85 @@ template <typename CT>
 struct HostFactors {
   const CT *U, *R, *B, *W, *Vt;
 };
+
+// A butterfly with ragged ranks <= 16 (and the fused path's uniform power-of-two leaves) as the
+// same linear map with every rank 16: each block zero-padded (U_tau and W / R blocks get zero
+// columns, Vt_nu / B / W / R zero rows; a W block's columns and an R block's rows keep their two
+// child parts at offsets 0 and 16), so the products only add exact zeros (Eq. 3.3 with padded
+// factors; ID-compressed butterflies of rank <= 16 on the level-fused kernels).
+template <typename CT>
+struct Padded16 {
+  std::vector<CT> U, R, B, W, Vt;
+  std::vector<int32_t> rr, rc;
+  bf_desc d{};
+  Geom G;
+};
+template <typename CT>
+static void pad_rank16(const bf_desc& d, const Geom& G, Padded16<CT>& P) {
+  const int L = G.L, lc = G.lc;
+  const int64_t nb = G.nb;
+  P.rr.assign((size_t)(L - lc + 1) * nb, FAST_RANK);
+  P.rc.assign((size_t)(lc + 1) * nb, FAST_RANK);
+  P.U.assign((size_t)G.m * 16, CT{});
+  P.R.assign((size_t)(L - lc) * nb * 32 * 16, CT{});
+  P.B.assign((size_t)nb * 16 * 16, CT{});
+  P.W.assign((size_t)lc * nb * 16 * 32, CT{});
+  P.Vt.assign((size_t)G.n * 16, CT{});
+  P.d = d;
+  P.d.rank_row = P.rr.data();
+  P.d.rank_col = P.rc.data();
+  P.d.U = P.U.data();
+  P.d.R = P.R.data();
+  P.d.B = P.B.data();
+  P.d.W = P.W.data();
+  P.d.Vt = P.Vt.data();
+  P.d.len_U = (int64_t)P.U.size();
+  P.d.len_R = (int64_t)P.R.size();
+  P.d.len_B = (int64_t)P.B.size();
+  P.d.len_W = (int64_t)P.W.size();
+  P.d.len_Vt = (int64_t)P.Vt.size();
+  P.G = make_geom(P.d);
+  const Geom& Q = P.G;
+  const CT *U = static_cast<const CT*>(d.U), *R = static_cast<const CT*>(d.R), *B = static_cast<const CT*>(d.B),
+           *W = static_cast<const CT*>(d.W), *Vt = static_cast<const CT*>(d.Vt);
+  for (int64_t t = 0; t < nb; ++t) {  // U_tau: mt x r -> mt x 16
+    const int64_t mt = G.mt(t);
+    const int r = G.r(L, t);
+    for (int k = 0; k < r; ++k)
+      for (int64_t i = 0; i < mt; ++i) P.U[Q.u_off[t] + i + k * mt] = U[G.u_off[t] + i + k * mt];
+  }
+  for (int l = lc; l < L; ++l)  // R^l_{tau,nu}: (rt + rb) x r -> 32 x 16, child rows at 0 / 16
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        const int64_t i = G.idx(l, tau, nu);
+        const int rt = G.r(l + 1, G.idx(l + 1, 2 * tau, nu >> 1)), rb = G.r(l + 1, G.idx(l + 1, 2 * tau + 1, nu >> 1));
+        const int r = G.r(l, i), ld = rt + rb;
+        for (int k = 0; k < r; ++k)
+          for (int row = 0; row < ld; ++row)
+            P.R[Q.r_off[l][i] + (row < rt ? row : 16 + row - rt) + k * 32] = R[G.r_off[l][i] + row + k * ld];
+      }
+  for (int64_t i = 0; i < nb; ++i) {  // B: r x c -> 16 x 16
+    const int r = G.r(lc, i), c = G.c(lc, i);
+    for (int k = 0; k < c; ++k)
+      for (int row = 0; row < r; ++row) P.B[Q.b_off[i] + row + k * 16] = B[G.b_off[i] + row + k * r];
+  }
+  for (int l = 1; l <= lc; ++l)  // W^l_{tau,nu}: c x (cl + cr) -> 16 x 32, child columns at 0 / 16
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        const int64_t i = G.idx(l, tau, nu);
+        const int cl = G.c(l - 1, G.idx(l - 1, tau >> 1, 2 * nu)), cr = G.c(l - 1, G.idx(l - 1, tau >> 1, 2 * nu + 1));
+        const int c = G.c(l, i);
+        for (int col = 0; col < cl + cr; ++col)
+          for (int row = 0; row < c; ++row)
+            P.W[Q.w_off[l][i] + row + (col < cl ? col : 16 + col - cl) * 16] = W[G.w_off[l][i] + row + col * c];
+      }
+  for (int64_t nu = 0; nu < nb; ++nu) {  // Vt_nu: c x nv -> 16 x nv
+    const int64_t nv = G.nv(nu);
+    const int c = G.c(0, nu);
+    for (int64_t col = 0; col < nv; ++col)
+      for (int row = 0; row < c; ++row) P.Vt[Q.vt_off[nu] + row + col * 16] = Vt[G.vt_off[nu] + row + col * c];
+  }
+}
 
 template <typename CT>
 static inline CT cj(CT v, bool c) {
@@ -1320,20 +1401,29 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
     }
     // the fused kernels use the 3M product; selection factors (every entry 0 / +-1 / +-i, the
     // identity pin) stay on the generic path, whose 4M product keeps their apply exact
-    if (fast_eligible(G, d->dtype) && h->m3 && !getenv("BF_DISABLE_FAST")) {
+    // the fused kernels: uniform rank 16 as given, ranks <= 16 zero-padded to 16 (pad_rank16; env
+    // BF_FAST_PAD = 0 keeps ragged ranks on the generic path, for A/B measurements)
+    static const bool pad_ok = !getenv("BF_FAST_PAD") || atoi(getenv("BF_FAST_PAD")) != 0;
+    if (fast_eligible(G, d->dtype, !pad_ok) && h->m3 && !getenv("BF_DISABLE_FAST")) {
       const bool cc = leaves_contiguous(d->col_perm, d->n, G.nv(0));
       const bool rc = leaves_contiguous(d->row_perm, d->m, G.mt(0));
-      if (d->dtype == BF_C128) {
-        HostFactors<double2> HF{static_cast<const double2*>(d->U), static_cast<const double2*>(d->R),
-                                static_cast<const double2*>(d->B), static_cast<const double2*>(d->W),
-                                static_cast<const double2*>(d->Vt)};
-        for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes, -1, 0, k == 0 ? cc : rc);
-      } else {
-        HostFactors<float2> HF{static_cast<const float2*>(d->U), static_cast<const float2*>(d->R),
-                               static_cast<const float2*>(d->B), static_cast<const float2*>(d->W),
-                               static_cast<const float2*>(d->Vt)};
-        for (int k = 0; k < 2; ++k) build_fast(h->fast[k], G, HF, k, &h->device_bytes);
-      }
+      const bool exact = fast_eligible(G, d->dtype, true);
+      auto build = [&](auto* tag) {
+        using CT = std::remove_pointer_t<decltype(tag)>;
+        Padded16<CT> P;
+        if (!exact) pad_rank16(*d, G, P);
+        const HostFactors<CT> HF = exact ? HostFactors<CT>{static_cast<const CT*>(d->U), static_cast<const CT*>(d->R),
+                                                           static_cast<const CT*>(d->B), static_cast<const CT*>(d->W),
+                                                           static_cast<const CT*>(d->Vt)}
+                                         : HostFactors<CT>{P.U.data(), P.R.data(), P.B.data(), P.W.data(), P.Vt.data()};
+        const Geom& GF = exact ? G : P.G;
+        for (int k = 0; k < 2; ++k) {
+          if (sizeof(CT) == 16) build_fast(h->fast[k], GF, HF, k, &h->device_bytes, -1, 0, k == 0 ? cc : rc);
+          else build_fast(h->fast[k], GF, HF, k, &h->device_bytes);
+        }
+      };
+      if (d->dtype == BF_C128) build((double2*)nullptr);
+      else build((float2*)nullptr);
       h->fast[0].contig_in = cc;
       h->fast[0].contig_out = rc;
       h->fast[1].contig_in = rc;

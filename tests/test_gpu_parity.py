@@ -44,7 +44,9 @@ def test_cfg1(dtype, op):
     if op != "N":
         X = random_rhs(bf.m, 16, seed=20, dtype=dtype)
     h = pkg.BFHandle(bf)
-    assert h.info["launches_n"] == bf.L + 3
+    # rank 8 on 32 leaves of 32: the fused path on factors padded to rank 16 (leaf-in, window
+    # passes, leaf-out) instead of the L + 3 rounds of the generic plan
+    assert h.rounds("N")[0]["name"].startswith("k_leaf") and h.info["launches_n"] < bf.L + 3
     err = oracle.rel_err(run(h, X, op), oracle.bf_apply(bf, X, op))
     assert err <= TOL[dtype], err
 
