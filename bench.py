@@ -251,7 +251,8 @@ def make_config(args, bf, cs, world):
             "l2": "inputs larger than L2 (factors %.2f GB >> 126 MB); no flush" % (bf.nnz() * cs / 1e9),
             "parallelism": "single GPU" if world == 1 else
             f"tree split over {world} GPUs (column subtrees -> "
-            + ("fused peer-memory exchange" if args.exchange == "p2p" else "NCCL all-to-all")
+            + {"p2p": "fused peer-memory exchange", "nccl": "NCCL all-to-all",
+               "nccl-lib": "library-owned NCCL send / recv"}[args.exchange]
             + " -> row subtrees)"}
 
 
@@ -297,9 +298,10 @@ def main():
     ap.add_argument("--nrhs", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
-                    help="N > 1: centre exchange by NCCL all-to-all, or fused into the kernel over peer "
-                         "memory (torch symmetric memory; bf_dist_apply_pre_p2p)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "nccl-lib"],
+                    help="N > 1: centre exchange by NCCL all-to-all (torch), fused into the kernel over peer "
+                         "memory (torch symmetric memory; bf_dist_apply_pre_p2p), or by the library's own "
+                         "NCCL communicator (bf_create_dist / bf_apply_dist: one C-ABI call per apply)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -340,8 +342,8 @@ def main():
             else:
                 h.apply_events(Xd, evs, args.op, out=Yd, work=work)
     else:
-        from paper_2007_00202_b200.dist import DistBFHandle
-        h = DistBFHandle(bf, rank, world, local)
+        from paper_2007_00202_b200.dist import DistBFHandle, NcclComm
+        h = DistBFHandle(bf, rank, world, local, comm=NcclComm(local) if args.exchange == "nccl-lib" else None)
         if args.exchange == "p2p":
             h.enable_p2p(args.nrhs, args.op)
         Xloc = h.local_input(X, args.op)

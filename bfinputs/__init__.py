@@ -4,9 +4,9 @@ Holds factor containers, generators (random / closed-form / kernel-compressed) a
 right-hand sides.  It contains no butterfly-apply arithmetic ("Inputs").
 """
 from .factors import (Butterfly, HODBF, Stage, bitrev, butterfly_from_blocks, dft_butterfly,
-                      identity_butterfly, random_butterfly, random_ranks_butterfly, random_rhs,
-                      uniform_leaf_ptr)
+                      identity_butterfly, random_butterfly, random_level_maps, random_ranks_butterfly,
+                      random_rhs, slot_ordered, uniform_leaf_ptr)
 
 __all__ = ["Butterfly", "HODBF", "Stage", "bitrev", "butterfly_from_blocks", "dft_butterfly",
-           "identity_butterfly", "random_butterfly", "random_ranks_butterfly", "random_rhs",
-           "uniform_leaf_ptr"]
+           "identity_butterfly", "random_butterfly", "random_level_maps", "random_ranks_butterfly",
+           "random_rhs", "slot_ordered", "uniform_leaf_ptr"]

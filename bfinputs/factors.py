@@ -398,3 +398,30 @@ def butterfly_from_blocks(L, lc, row_leaf_ptr, col_leaf_ptr, row_perm, col_perm,
                      Stage.from_blocks(U, dtype), [Stage.from_blocks(R[l], dtype) for l in range(lc, L)],
                      Stage.from_blocks(B, dtype), [Stage.from_blocks(W[l], dtype) for l in range(1, lc + 1)],
                      Stage.from_blocks(Vt, dtype), dtype, dict(meta or {}))
+
+
+# ----------------------------------------------------------------------------------
+# non-canonical block orderings (C-ABI bf_desc.level_maps; layout only, no arithmetic)
+# ----------------------------------------------------------------------------------
+def random_level_maps(L: int, seed: int, levels=None) -> list:
+    """L + 1 entries: a seeded random bijection of [0, 2^L) for every level in ``levels``
+    (default: all), None (canonical) for the others."""
+    rng = np.random.default_rng(seed)
+    nb = 1 << L
+    levels = range(L + 1) if levels is None else levels
+    return [rng.permutation(nb).astype(np.int32) if l in levels else None for l in range(L + 1)]
+
+
+def slot_ordered(bf: Butterfly, maps) -> Butterfly:
+    """The same butterfly with the blocks (and hence the ranks) of every mapped level packed in
+    storage-slot order: slot s of level l holds canonical block maps[l][s]."""
+    def perm(stage: Stage, mp) -> Stage:
+        if mp is None:
+            return stage
+        return Stage.from_blocks([stage.block(int(i)) for i in mp], bf.dtype)
+
+    L, lc = bf.L, bf.lc
+    return Butterfly(bf.m, bf.n, L, lc, bf.row_leaf_ptr, bf.col_leaf_ptr, bf.row_perm, bf.col_perm,
+                     perm(bf.U, maps[L]), [perm(s, maps[lc + k]) for k, s in enumerate(bf.R)],
+                     perm(bf.B, maps[lc]), [perm(s, maps[k + 1]) for k, s in enumerate(bf.W)],
+                     perm(bf.Vt, maps[0]), bf.dtype, dict(bf.meta))

@@ -79,7 +79,7 @@ typedef enum {
 /* Butterfly descriptor.  All pointers are HOST pointers. */
 typedef struct {
   int32_t dtype;                 /* bf_dtype                                                  */
-  int32_t L;                     /* number of levels, 0 <= L <= 24                           */
+  int32_t L;                     /* number of levels, 0 <= L <= 30                           */
   int32_t lc;                    /* centre level, 0 <= lc <= L; pass -1 for floor(L/2) (A2)  */
   int32_t reserved;
   int64_t m, n;                  /* rows (|O|) and columns (|S|)                             */
@@ -92,6 +92,15 @@ typedef struct {
   const void *U, *R, *B, *W, *Vt;/* packed factor arrays (see above)                          */
   int64_t len_U, len_R, len_B, len_W, len_Vt; /* element counts of the five arrays; must equal
                                                 the counts implied by the ranks (BF_ERR_RANK) */
+  /* Optional non-canonical block orderings ("level-by-level index permutations", north star;
+   * SURVEY 8(b)).  NULL = every level canonical.  Otherwise L + 1 pointers; entry l (NULL =
+   * canonical) is a 2^L int32 bijection  storage slot s -> canonical index tau * 2^(L-l) + nu
+   * of level l.  It orders everything stored per level-l block: the level-l ranks (rank_row
+   * if l >= lc, rank_col if l <= lc) and the level-l factor blocks (U at l = L, R at
+   * lc <= l < L, B at l = lc, W at 1 <= l <= lc, Vt at l = 0), which are then packed in slot
+   * order.  Leaf offsets and perms are unaffected.  Not a bijection: BF_ERR_PERM.  The
+   * library re-packs to canonical order at create (host copy; the apply is unchanged). */
+  const int32_t* const* level_maps;
 } bf_desc;
 
 /* HOD-BF descriptor.  offdiag has sum_{l=1..LH} 2^l entries, level-major:
@@ -214,6 +223,34 @@ int bf_dist_apply_pre_p2p(bf_handle h, int op, int64_t nrhs, const void* X_loc, 
                           void* work, size_t work_bytes, void* const* peer_recv, bf_stream_t stream);
 int bf_dist_apply_post(bf_handle h, int op, int64_t nrhs, void* Y_loc, int64_t ldy,
                        void* work, size_t work_bytes, bf_stream_t stream);
+
+/* ---- distributed apply with a library-owned NCCL communicator (SURVEY 8(b) stretch goal;
+ * north star: "the middle-level redistribution is an NCCL all-to-all over NVLink") ----------
+ * NCCL is loaded at run time (dlopen "libnccl.so.2", env BF_NCCL_LIB overrides; inside a
+ * PyTorch process that is the NCCL torch already loaded); when it cannot be loaded these calls
+ * return BF_ERR_NCCL.
+ *   bf_nccl_available     1 when NCCL is loadable, else 0.
+ *   bf_nccl_get_unique_id writes the 128-byte ncclUniqueId (call on one rank, send the bytes to
+ *                         every rank by any means, e.g. torch.distributed.broadcast).
+ *   bf_nccl_comm_init     ncclCommInitRank on `device` (collective over the nranks processes);
+ *                         *comm is an ncclComm_t owned by the caller: free it with
+ *                         bf_nccl_comm_destroy after every handle using it is destroyed.
+ *   bf_create_dist        bf_dist_create plus the communicator (checked: its size / rank /
+ *                         device equal nranks / rank / device; NULL only when nranks == 1 or
+ *                         device < 0).  The handle does not own the communicator.
+ *   bf_apply_dist         one whole distributed apply on `stream`: bf_dist_apply_pre, the
+ *                         exchange of the send region's per-peer chunks into every peer's
+ *                         recv region (grouped ncclSend / ncclRecv; one rank: a device copy),
+ *                         bf_dist_apply_post.  Arguments as bf_dist_apply_pre / _post (X_loc,
+ *                         Y_loc and work are device buffers; work >= bf_dist_layout's
+ *                         work_bytes).  Every rank must call it with the same op and nrhs. */
+int bf_nccl_available(void);
+int bf_nccl_get_unique_id(void* id);
+int bf_nccl_comm_init(int nranks, const void* id, int rank, int device, void** comm);
+int bf_nccl_comm_destroy(void* comm);
+int bf_create_dist(const bf_desc* desc, int rank, int nranks, void* nccl_comm, int device, bf_handle* out);
+int bf_apply_dist(bf_handle h, int op, int64_t nrhs, const void* X_loc, int64_t ldx, void* Y_loc, int64_t ldy,
+                  void* work, size_t work_bytes, bf_stream_t stream);
 
 /* Sub-matrix extraction (Alg. 3 extract_BF): out(i, j) =
  * K(rows[i], cols[j]) for user row / column indices (HOST arrays of nI / nJ int64, any order,

@@ -41,7 +41,8 @@ class bf_desc(C.Structure):
                 ("U", C.c_void_p), ("R", C.c_void_p), ("B", C.c_void_p), ("W", C.c_void_p),
                 ("Vt", C.c_void_p),
                 ("len_U", C.c_int64), ("len_R", C.c_int64), ("len_B", C.c_int64),
-                ("len_W", C.c_int64), ("len_Vt", C.c_int64)]
+                ("len_W", C.c_int64), ("len_Vt", C.c_int64),
+                ("level_maps", C.POINTER(_i32p))]
 
 
 class hodbf_desc(C.Structure):
@@ -178,8 +179,12 @@ class _Keep:
         return a
 
 
-def make_desc(bf, keep: _Keep, tree_local: bool = False) -> bf_desc:
-    """bf_desc for a bfinputs.Butterfly (packed arrays are passed straight through)."""
+def make_desc(bf, keep: _Keep, tree_local: bool = False, level_maps=None) -> bf_desc:
+    """bf_desc for a bfinputs.Butterfly (packed arrays are passed straight through).
+
+    ``level_maps``: optional list of L + 1 entries (None or a 2^L int array: storage slot ->
+    canonical block index of that level); the stages of ``bf`` are then in slot order
+    (include/bfapply.h, bf_desc.level_maps)."""
     code = _np_dtype_code(bf.dtype)
     d = bf_desc()
     d.dtype, d.L, d.lc, d.m, d.n = code, bf.L, bf.lc, bf.m, bf.n
@@ -201,6 +206,14 @@ def make_desc(bf, keep: _Keep, tree_local: bool = False) -> bf_desc:
     Vt = keep(bf.Vt.data, cdt)
     d.U, d.R, d.B, d.W, d.Vt = _ptr(U), _ptr(Rr), _ptr(Bb), _ptr(Ww), _ptr(Vt)
     d.len_U, d.len_R, d.len_B, d.len_W, d.len_Vt = U.size, Rr.size, Bb.size, Ww.size, Vt.size
+    if level_maps is not None:
+        if len(level_maps) != bf.L + 1:
+            raise ValueError(f"level_maps needs L + 1 = {bf.L + 1} entries")
+        arr = (_i32p * (bf.L + 1))()
+        for l, mp in enumerate(level_maps):
+            arr[l] = None if mp is None else _ptr(keep(mp, np.int32), C.c_int32)
+        keep.arrs.append(arr)
+        d.level_maps = C.cast(arr, C.POINTER(_i32p))
     return d
 
 
@@ -248,9 +261,9 @@ class Workspace:
 class BFHandle:
     """A butterfly uploaded to one device (bf_create)."""
 
-    def __init__(self, bf, device: int = 0):
+    def __init__(self, bf, device: int = 0, level_maps=None):
         keep = _Keep()
-        d = make_desc(bf, keep)
+        d = make_desc(bf, keep, level_maps=level_maps)
         h = C.c_void_p()
         _check("bf_create", lib().bf_create(C.byref(d), device, C.byref(h)))
         self.h, self.device, self.code = h, device, d.dtype

@@ -110,7 +110,8 @@ static void check_perm(const int64_t* p, int64_t n, const char* what) {
 static Geom make_geom(const bf_desc& d) {
   Geom g;
   require(d.dtype == BF_C64 || d.dtype == BF_C128, BF_ERR_ARG, "dtype must be BF_C64 or BF_C128");
-  require(d.L >= 0 && d.L <= 24, BF_ERR_SHAPE, "L out of range [0, 24]");
+  require(d.L >= 0 && d.L <= 30, BF_ERR_SHAPE, "L out of range [0, 30]");
+  require(d.level_maps == nullptr, BF_ERR_ARG, "internal: level_maps not canonicalised");
   g.L = d.L;
   g.lc = d.lc < 0 ? d.L / 2 : d.lc;
   require(g.lc >= 0 && g.lc <= g.L, BF_ERR_SHAPE, "lc out of range [0, L]");
@@ -179,6 +180,86 @@ static Geom make_geom(const bf_desc& d) {
               (g.len_W == 0 || d.W) && (g.len_Vt == 0 || d.Vt),
           BF_ERR_ARG, "factor array is NULL");
   return g;
+}
+
+// --------------------------------------------------------------------------------------
+// bf_desc.level_maps: per-level block orderings other than the canonical
+// idx = tau * 2^(L-l) + nu.  The descriptor is re-packed on the host into canonical order
+// (ranks and factor blocks of every mapped level), so everything after create sees only
+// canonical descriptors.  Canon owns the re-packed arrays.
+// --------------------------------------------------------------------------------------
+struct Canon {
+  bf_desc d{};
+  std::vector<int32_t> rr, rc;
+  std::vector<char> f[5];  // U, R, B, W, Vt
+};
+
+static const bf_desc& canonical(const bf_desc& in, Canon& cn) {
+  if (!in.level_maps) return in;
+  require(in.dtype == BF_C64 || in.dtype == BF_C128, BF_ERR_ARG, "dtype must be BF_C64 or BF_C128");
+  require(in.L >= 0 && in.L <= 30, BF_ERR_SHAPE, "L out of range [0, 30]");
+  const int L = in.L, lc = in.lc < 0 ? in.L / 2 : in.lc;
+  require(lc >= 0 && lc <= L, BF_ERR_SHAPE, "lc out of range [0, L]");
+  require(in.rank_row && in.rank_col, BF_ERR_ARG, "rank arrays are NULL");
+  const int64_t nb = int64_t(1) << L;
+  const int32_t* const* M = in.level_maps;
+  for (int l = 0; l <= L; ++l) {
+    if (!M[l]) continue;
+    std::vector<char> seen((size_t)nb, 0);
+    for (int64_t s = 0; s < nb; ++s) {
+      const int64_t i = M[l][s];
+      require(i >= 0 && i < nb && !seen[(size_t)i], BF_ERR_PERM,
+              "level_maps[" + std::to_string(l) + "] is not a bijection of [0, 2^L)");
+      seen[(size_t)i] = 1;
+    }
+  }
+  auto slot_to = [&](int l, int64_t s) -> int64_t { return M[l] ? M[l][s] : s; };
+  cn.rr.assign(in.rank_row, in.rank_row + (size_t)(L - lc + 1) * nb);
+  cn.rc.assign(in.rank_col, in.rank_col + (size_t)(lc + 1) * nb);
+  for (int l = lc; l <= L; ++l)
+    for (int64_t s = 0; s < nb; ++s) cn.rr[(size_t)(l - lc) * nb + slot_to(l, s)] = in.rank_row[(l - lc) * nb + s];
+  for (int l = 0; l <= lc; ++l)
+    for (int64_t s = 0; s < nb; ++s) cn.rc[(size_t)l * nb + slot_to(l, s)] = in.rank_col[l * nb + s];
+  cn.d = in;
+  cn.d.level_maps = nullptr;
+  cn.d.rank_row = cn.rr.data();
+  cn.d.rank_col = cn.rc.data();
+  // canonical geometry (validates leaves, ranks and array lengths; the lengths do not depend
+  // on the order of the blocks)
+  const Geom g = make_geom(cn.d);
+  const size_t cs = csize(in.dtype);
+  const void* src[5] = {in.U, in.R, in.B, in.W, in.Vt};
+  const int64_t len[5] = {g.len_U, g.len_R, g.len_B, g.len_W, g.len_Vt};
+  for (int a = 0; a < 5; ++a) cn.f[a].resize((size_t)len[a] * cs);
+  // one level of one array: storage slots in order, each copied to its canonical offset
+  auto level = [&](int a, int l, const std::vector<int64_t>& coff, auto size_of, int64_t& in_off) {
+    for (int64_t s = 0; s < nb; ++s) {
+      const int64_t i = slot_to(l, s);
+      const int64_t sz = size_of(i);
+      if (sz) std::memcpy(cn.f[a].data() + coff[i] * cs, static_cast<const char*>(src[a]) + in_off * cs, sz * cs);
+      in_off += sz;
+    }
+  };
+  auto tau_of = [&](int l, int64_t i) { return i >> (L - l); };
+  auto nu_of = [&](int l, int64_t i) { return i & ((int64_t(1) << (L - l)) - 1); };
+  int64_t o = 0;
+  level(0, L, g.u_off, [&](int64_t i) { return g.mt(i) * g.r(L, i); }, o);
+  o = 0;
+  for (int l = lc; l < L; ++l)
+    level(1, l, g.r_off[l], [&](int64_t i) { return int64_t(g.R_rows(l, tau_of(l, i), nu_of(l, i))) * g.r(l, i); }, o);
+  o = 0;
+  level(2, lc, g.b_off, [&](int64_t i) { return int64_t(g.r(lc, i)) * g.c(lc, i); }, o);
+  o = 0;
+  for (int l = 1; l <= lc; ++l)
+    level(3, l, g.w_off[l], [&](int64_t i) { return int64_t(g.c(l, i)) * g.W_cols(l, tau_of(l, i), nu_of(l, i)); }, o);
+  o = 0;
+  level(4, 0, g.vt_off, [&](int64_t i) { return int64_t(g.c(0, i)) * g.nv(i); }, o);
+  cn.d.U = cn.f[0].data();
+  cn.d.R = cn.f[1].data();
+  cn.d.B = cn.f[2].data();
+  cn.d.W = cn.f[3].data();
+  cn.d.Vt = cn.f[4].data();
+  return cn.d;
 }
 
 // factor-pool base offsets (elements) of one butterfly's five arrays
@@ -1157,6 +1238,7 @@ struct bf_s {
   // distributed
   bool dist = false;
   int rank = 0, nranks = 1;
+  void* nccl = nullptr;  // bf_create_dist: the caller's ncclComm_t (not owned)
   Plan pre[2], post[2];
   int64_t send_rows[2] = {0, 0}, recv_rows[2] = {0, 0};
   int64_t send_base[2] = {0, 0}, recv_base[2] = {0, 0};  // slab rows
@@ -1349,6 +1431,8 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
   if (!d || !out) return fail(Err{BF_ERR_ARG, "NULL argument"});
   *out = nullptr;
   try {
+    Canon cn_;
+    d = &canonical(*d, cn_);
     Geom G = make_geom(*d);
     check_perm(d->row_perm, d->m, "row_perm");
     check_perm(d->col_perm, d->n, "col_perm");
@@ -1807,6 +1891,21 @@ int hodbf_create(const hodbf_desc* d, int device, hodbf_handle* out) {
     require(d->len_D == lenD && (lenD == 0 || d->D), BF_ERR_SHAPE, "len_D does not match the leaf sizes");
     const int64_t nbf = 2 * nleaf - 2;
     require(nbf == 0 || d->offdiag, BF_ERR_ARG, "offdiag is NULL");
+    // off-diagonal butterflies with level_maps: re-packed to canonical order (the rest of the
+    // create reads d->offdiag only)
+    std::vector<Canon> cns;
+    std::vector<bf_desc> offc;
+    hodbf_desc dc;
+    for (int64_t k = 0; k < nbf; ++k)
+      if (d->offdiag[k].level_maps) {
+        cns.resize((size_t)nbf);
+        offc.resize((size_t)nbf);
+        for (int64_t q = 0; q < nbf; ++q) offc[q] = canonical(d->offdiag[q], cns[q]);
+        dc = *d;
+        dc.offdiag = offc.data();
+        d = &dc;
+        break;
+      }
     // geometry of every off-diagonal butterfly, checked against the HOD-BF tree
     std::vector<Geom> G(nbf);
     for (int l = 1; l <= LH; ++l)
@@ -2187,6 +2286,8 @@ int bf_dist_create(const bf_desc* d, int rank, int nranks, int device, bf_handle
   if (!d || !out) return fail(Err{BF_ERR_ARG, "NULL argument"});
   *out = nullptr;
   try {
+    Canon cn_;
+    d = &canonical(*d, cn_);
     require(nranks >= 1 && (nranks & (nranks - 1)) == 0, BF_ERR_NCCL, "nranks must be a power of two");
     require(rank >= 0 && rank < nranks, BF_ERR_ARG, "rank out of range");
     Geom G = make_geom(*d);
@@ -3398,3 +3499,4 @@ int bf_accumulate(int dtype, int64_t rows, int64_t nrhs, const void* A, int64_t 
 #include "rmatvec_host.inc"
 #include "hinv_host.inc"
 #include "mf_host.inc"
+#include "nccl_host.inc"

@@ -36,6 +36,13 @@ _SIGS = [
     ("bf_dist_exchange_level", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
     ("bf_dist_apply_pre_p2p", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                         C.c_size_t, C.POINTER(C.c_void_p), C.c_void_p]),
+    ("bf_nccl_available", C.c_int, []),
+    ("bf_nccl_get_unique_id", C.c_int, [C.c_void_p]),
+    ("bf_nccl_comm_init", C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("bf_nccl_comm_destroy", C.c_int, [C.c_void_p]),
+    ("bf_create_dist", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    ("bf_apply_dist", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                C.c_void_p, C.c_size_t, C.c_void_p]),
 ]
 
 
@@ -51,17 +58,53 @@ def _opk(op: str) -> int:
     return 0 if op == "N" else 1
 
 
-class DistBFHandle:
-    """This rank's share of a butterfly split over ``world`` processes (bf_dist_create)."""
+class NcclComm:
+    """A library-owned NCCL communicator (bf_nccl_comm_init) over the ranks of ``group``: rank 0
+    draws the ncclUniqueId, the process group carries its 128 bytes to the others (any backend,
+    gloo included), then every rank joins on its device.  Used by DistBFHandle(comm=...), whose
+    apply is then the single C-ABI call bf_apply_dist (pre, grouped ncclSend / ncclRecv, post)."""
 
-    def __init__(self, bf, rank: int, world: int, device: Optional[int] = 0, group=None):
+    def __init__(self, device: int, group=None):
+        L = _lib()
+        if not L.bf_nccl_available():
+            raise BFError("bf_nccl_available", -7, "NCCL cannot be loaded")
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _check("bf_nccl_get_unique_id", L.bf_nccl_get_unique_id(uid))
+        if world > 1:
+            obj = [bytes(uid) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            C.memmove(uid, obj[0], 128)
+        c = C.c_void_p()
+        _check("bf_nccl_comm_init", L.bf_nccl_comm_init(world, uid, rank, int(device), C.byref(c)))
+        self.ptr, self.rank, self.world, self.device = c, rank, world, device
+
+    def close(self):
+        if getattr(self, "ptr", None) is not None and self.ptr.value:
+            _lib().bf_nccl_comm_destroy(self.ptr)
+        self.ptr = None
+
+
+class DistBFHandle:
+    """This rank's share of a butterfly split over ``world`` processes (bf_dist_create; with
+    ``comm`` an NcclComm, bf_create_dist: the library then runs the exchange itself)."""
+
+    def __init__(self, bf, rank: int, world: int, device: Optional[int] = 0, group=None,
+                 comm: Optional[NcclComm] = None):
         keep = _Keep()
         d = make_desc(bf, keep)
         h = C.c_void_p()
         dev = -1 if device is None else int(device)
-        _check("bf_dist_create", _lib().bf_dist_create(C.byref(d), rank, world, dev, C.byref(h)))
+        if comm is not None:
+            _check("bf_create_dist", _lib().bf_create_dist(C.byref(d), rank, world, comm.ptr, dev, C.byref(h)))
+        else:
+            _check("bf_dist_create", _lib().bf_dist_create(C.byref(d), rank, world, dev, C.byref(h)))
         self.h, self.rank, self.world, self.device, self.code = h, rank, world, device, d.dtype
         self.group = group
+        self.comm = comm
         self.cs = 16 if d.dtype == 2 else 8
         self.m, self.n = bf.m, bf.n
         self.ws = Workspace(torch.device("cuda", device)) if device is not None else None
@@ -180,6 +223,11 @@ class DistBFHandle:
         if work is None:
             work = self.ws.get(wb, stream)
         st = _stream_handle(stream)
+        if self.comm is not None:  # library-owned NCCL: one C-ABI call, exchange included
+            _check("bf_apply_dist", _lib().bf_apply_dist(self.h, OPS[op], nrhs, C.c_void_p(Xloc.data_ptr()), ldx,
+                                                         C.c_void_p(out.data_ptr()), ldy, C.c_void_p(work.data_ptr()),
+                                                         work.numel(), st))
+            return out
         _check("bf_dist_apply_pre", lib().bf_dist_apply_pre(self.h, OPS[op], nrhs, C.c_void_p(Xloc.data_ptr()), ldx,
                                                              C.c_void_p(work.data_ptr()), work.numel(), st))
         # NCCL orders the all-to-all against torch's current stream: make that the apply's stream,

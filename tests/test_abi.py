@@ -155,3 +155,79 @@ def test_construction_calls_need_a_device():
     rc = L.bf_random_matvec(C.byref(d), C.cast(L.bf_operator_apply, C.c_void_p), None, 0, None, C.byref(h),
                             C.byref(st))
     assert rc == -8 and not h.value
+
+
+# ---- bf_desc.level_maps ("level-by-level index permutations") and L <= 30 ----
+def _create_maps(bf, maps, mutate=None, dist=False):
+    keep = B._Keep()
+    d = B.make_desc(bf, keep, level_maps=maps)
+    if mutate:
+        mutate(d, keep)
+    h = C.c_void_p()
+    if dist:  # host-only distributed plan (device < 0): the whole create runs, nothing uploads
+        rc = pkg.lib().bf_dist_create(C.byref(d), 0, 1, -1, C.byref(h))
+    else:
+        rc = pkg.lib().bf_create(C.byref(d), 0, C.byref(h))
+    if rc == 0:
+        pkg.lib().bf_destroy(h)
+    return rc
+
+
+def test_level_maps_not_bijection_is_perm_error():
+    from bfinputs import random_level_maps, slot_ordered
+    bf = random_ranks_butterfly(3, [3, 2, 4, 1, 5, 2, 2, 3], [2, 2, 3, 5, 1, 1, 4, 2], seed=0)
+    maps = random_level_maps(bf.L, seed=1)
+    bad = [m.copy() for m in maps]
+    bad[2][0] = bad[2][1]
+    assert _create_maps(slot_ordered(bf, maps), bad) == -4
+    bad = [m.copy() for m in maps]
+    bad[0][3] = 1 << bf.L
+    assert _create_maps(slot_ordered(bf, maps), bad) == -4
+
+
+def test_level_maps_accepted_by_a_host_plan():
+    """A slot-ordered descriptor with its maps passes every create-time check (ranks, lengths)
+    through the canonical re-pack; the same packing without maps, with ragged ranks whose block
+    sizes differ per slot, fails the rank-chain length check."""
+    from bfinputs import random_level_maps, slot_ordered
+    rng = np.random.default_rng(3)
+    bf = random_ranks_butterfly(4, rng.integers(0, 9, 16), rng.integers(1, 9, 16), seed=3, rmin=0, rmax=7)
+    for lv in (None, [0], [bf.L], [bf.lc], [1, 3]):
+        maps = random_level_maps(bf.L, seed=5, levels=lv)
+        assert _create_maps(slot_ordered(bf, maps), maps, dist=True) == 0
+    maps = random_level_maps(bf.L, seed=5)
+    assert _create_maps(slot_ordered(bf, maps), None, dist=True) in (0, -3)
+    assert _create_maps(bf, [None] * (bf.L + 1), dist=True) == 0
+
+
+def test_L_limit_is_30():
+    bf = random_butterfly(L=2, leaf=4, r=2, seed=0)
+
+    def mut(d, keep):
+        d.L = 31
+    assert _create(bf, mut) == -2
+
+
+def test_create_dist_needs_a_comm_for_several_ranks():
+    """bf_create_dist (library-owned NCCL): NULL communicator with nranks > 1 on a device is
+    BF_ERR_ARG; a host-only plan (device < 0) needs none and has bf_dist_create's layout."""
+    from paper_2007_00202_b200.dist import _lib
+    L = _lib()
+    assert L.bf_nccl_available() in (0, 1)
+    bf = random_butterfly(L=4, leaf=8, r=4, seed=0)
+    keep = B._Keep()
+    d = B.make_desc(bf, keep)
+    h = C.c_void_p()
+    assert L.bf_create_dist(C.byref(d), 0, 2, None, 0, C.byref(h)) == -1
+    assert L.bf_create_dist(C.byref(d), 1, 2, None, -1, C.byref(h)) == 0
+    h2 = C.c_void_p()
+    assert L.bf_dist_create(C.byref(d), 1, 2, -1, C.byref(h2)) == 0
+    lay = []
+    for hh in (h, h2):
+        wb, so, ro = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        sc, rc = (C.c_int64 * 2)(), (C.c_int64 * 2)()
+        assert L.bf_dist_layout(hh, 0, 8, C.byref(wb), C.byref(so), C.byref(ro), sc, rc) == 0
+        lay.append((wb.value, so.value, ro.value, list(sc), list(rc)))
+        L.bf_destroy(hh)
+    assert lay[0] == lay[1]
+    assert L.bf_apply_dist(None, 0, 1, None, 1, None, 1, None, 0, None) == -1

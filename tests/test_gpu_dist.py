@@ -224,3 +224,62 @@ def test_tree_hodbf_emulated(P, dtype):
         X = random_rhs(H.n, 19, seed=P, dtype=dtype)
         err = oracle.rel_err(emulate_tree_hodbf(H, X, op, P), oracle.hodbf_apply(H, X, op))
         assert err <= TOL[dtype], (op, err)
+
+
+# ---- library-owned NCCL communicator (bf_create_dist / bf_apply_dist) -----------------------
+@pytest.mark.parametrize("fast", [False, True])
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_library_nccl_world1(fast, dtype):
+    """bf_apply_dist with a communicator the library created (bf_nccl_comm_init over one rank):
+    pre, grouped ncclSend / ncclRecv to itself, post -- one C-ABI call per apply.  It must equal
+    the pre / torch exchange / post path bit for bit, and the oracle within the bar.  (One GPU: a
+    multi-rank NCCL communicator needs one device per rank.)"""
+    from paper_2007_00202_b200.dist import NcclComm
+    if fast:
+        bf = random_butterfly(L=6, leaf=32, r=16, seed=3, dtype=dtype)
+    else:
+        rng = np.random.default_rng(2)
+        bf = random_ranks_butterfly(5, rng.integers(1, 20, 32), rng.integers(1, 20, 32), seed=2, rmin=1, rmax=12,
+                                    dtype=dtype)
+    comm = NcclComm(0)
+    try:
+        h1 = DistBFHandle(bf, 0, 1, 0, comm=comm)
+        h0 = DistBFHandle(bf, 0, 1, 0)
+        K = oracle.bf_dense(bf)
+        for op, nr in (("N", 32), ("C", 7)):
+            X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=4, dtype=dtype)
+            Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+            Y1 = h1.apply(Xd, op)
+            Y0 = h0.apply(Xd, op)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(Y1.cpu().numpy(), Y0.cpu().numpy())
+            assert oracle.rel_err(Y1.cpu().numpy().T, oracle.apply_op(K, X, op)) <= TOL[dtype]
+        h1.close()
+    finally:
+        comm.close()
+
+
+def test_apply_dist_one_rank_without_comm():
+    """bf_create_dist with a NULL communicator is legal for one rank: bf_apply_dist's exchange is
+    then a device copy inside the workspace."""
+    import ctypes as C
+    from paper_2007_00202_b200.bfapply import _Keep, make_desc, lib, OPS
+    from paper_2007_00202_b200.dist import _lib
+    bf = random_butterfly(L=4, leaf=16, r=16, seed=5)
+    keep = _Keep()
+    d = make_desc(bf, keep)
+    h = C.c_void_p()
+    assert _lib().bf_create_dist(C.byref(d), 0, 1, None, 0, C.byref(h)) == 0
+    ref = DistBFHandle(bf, 0, 1, 0)
+    X = random_rhs(bf.n, 5, seed=6)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+    Y = torch.empty((5, bf.m), dtype=torch.complex128, device="cuda")
+    wb = ref.layout("N", 5)[0]
+    w = torch.empty(max(wb, 1), dtype=torch.uint8, device="cuda")
+    rc = _lib().bf_apply_dist(h, OPS["N"], 5, C.c_void_p(Xd.data_ptr()), bf.n, C.c_void_p(Y.data_ptr()), bf.m,
+                              C.c_void_p(w.data_ptr()), w.numel(), None)
+    assert rc == 0, lib().bf_last_error()
+    Y0 = ref.apply(Xd, "N")
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(Y.cpu().numpy(), Y0.cpu().numpy())
+    lib().bf_destroy(h)

@@ -437,3 +437,30 @@ def test_overlapping_x_y_rejected():
     h.apply(big[:16], out=big[16:])
     torch.cuda.synchronize()
     assert oracle.rel_err(host(big[16:]), oracle.bf_apply(bf, X)) <= 1e-12
+
+
+# ------------------------------------------------------------------ level_maps (bf_desc)
+@pytest.mark.parametrize("fast", [False, True])
+@pytest.mark.parametrize("levels", [None, "some"])
+def test_level_maps_same_result(fast, levels):
+    """A butterfly given with non-canonical per-level block orderings (bf_desc.level_maps) is
+    the same operator: bit-identical applies to the canonical descriptor (the library re-packs at
+    create), and within the bar of the oracle.  Ragged ranks (generic kernels) and rank 16
+    (fused kernels)."""
+    from bfinputs import random_level_maps, slot_ordered
+    if fast:
+        bf = random_butterfly(L=5, leaf=32, r=16, seed=4)
+    else:
+        rng = np.random.default_rng(7)
+        bf = random_ranks_butterfly(5, rng.integers(0, 30, 32), rng.integers(1, 30, 32), seed=7, rmin=0, rmax=20)
+    lv = None if levels is None else [0, 2, bf.lc, bf.L]
+    maps = random_level_maps(bf.L, seed=11, levels=lv)
+    h0 = pkg.BFHandle(bf)
+    h1 = pkg.BFHandle(slot_ordered(bf, maps), level_maps=maps)
+    assert h1.info["launches_n"] == h0.info["launches_n"]
+    K = oracle.bf_dense(bf)
+    for op, nr in (("N", 33), ("C", 16), ("T", 3)):
+        X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=12)
+        Y0, Y1 = run(h0, X, op), run(h1, X, op)
+        np.testing.assert_array_equal(Y1, Y0)
+        assert oracle.rel_err(Y1, oracle.apply_op(K, X, op)) <= 1e-12
