@@ -76,12 +76,19 @@ typedef enum {
   BF_ERR_DEVICE = -8  /* no CUDA device / wrong device / not an sm_100 device             */
 } bf_status;
 
+/* bf_desc.flags.  BF_CREATE_FUSED_ONLY: when the butterfly runs on the fused kernels (uniform
+ * power-of-two leaves of 16-256, ranks <= 16), keep only their per-op factor records and release
+ * the generic factor pool after create -- two copies of the factors on the device instead of
+ * three (config 5 complex128: 4.96 instead of 7.45 GB).  bf_extract / bf_extract_list and
+ * bf_export's factor copies then return BF_ERR_ARG.  No effect on other butterflies. */
+typedef enum { BF_CREATE_FUSED_ONLY = 1 } bf_create_flags;
+
 /* Butterfly descriptor.  All pointers are HOST pointers. */
 typedef struct {
   int32_t dtype;                 /* bf_dtype                                                  */
   int32_t L;                     /* number of levels, 0 <= L <= 30                           */
   int32_t lc;                    /* centre level, 0 <= lc <= L; pass -1 for floor(L/2) (A2)  */
-  int32_t reserved;
+  int32_t flags;                 /* bf_create_flags (0 = default)                            */
   int64_t m, n;                  /* rows (|O|) and columns (|S|)                             */
   const int64_t* row_leaf_ptr;   /* 2^L + 1 offsets of T_O leaves in tree order              */
   const int64_t* col_leaf_ptr;   /* 2^L + 1 offsets of T_S leaves                            */

@@ -24,6 +24,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BF_LIB") or os.path.join(_PKG, "libbfapply.so")
 
 BF_C64, BF_C128 = 1, 2
+BF_CREATE_FUSED_ONLY = 1  # bf_desc.flags (include/bfapply.h)
 OPS = {"N": 0, "T": 1, "C": 2}
 STATUS = {0: "BF_OK", -1: "BF_ERR_ARG", -2: "BF_ERR_SHAPE", -3: "BF_ERR_RANK", -4: "BF_ERR_PERM",
           -5: "BF_ERR_CUDA", -6: "BF_ERR_OOM", -7: "BF_ERR_NCCL", -8: "BF_ERR_DEVICE"}
@@ -33,7 +34,7 @@ _i32p = C.POINTER(C.c_int32)
 
 
 class bf_desc(C.Structure):
-    _fields_ = [("dtype", C.c_int32), ("L", C.c_int32), ("lc", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("dtype", C.c_int32), ("L", C.c_int32), ("lc", C.c_int32), ("flags", C.c_int32),
                 ("m", C.c_int64), ("n", C.c_int64),
                 ("row_leaf_ptr", _i64p), ("col_leaf_ptr", _i64p),
                 ("row_perm", _i64p), ("col_perm", _i64p),
@@ -261,9 +262,10 @@ class Workspace:
 class BFHandle:
     """A butterfly uploaded to one device (bf_create)."""
 
-    def __init__(self, bf, device: int = 0, level_maps=None):
+    def __init__(self, bf, device: int = 0, level_maps=None, fused_only: bool = False):
         keep = _Keep()
         d = make_desc(bf, keep, level_maps=level_maps)
+        d.flags = BF_CREATE_FUSED_ONLY if fused_only else 0
         h = C.c_void_p()
         _check("bf_create", lib().bf_create(C.byref(d), device, C.byref(h)))
         self.h, self.device, self.code = h, device, d.dtype

@@ -587,6 +587,18 @@ static bool fast_eligible(const Geom& G, int dtype, bool exact = true) {
   return true;
 }
 
+// Padding ragged ranks <= 16 up to 16 multiplies the streamed entries (a rank-r block of a W / R
+// stage by (16 / r)^2): it pays while the padded butterfly streams at most 3x the given entries
+// (the fused kernels run at ~3x the generic kernels' rate), or while it is small enough (<= 16 MB
+// padded) that the generic plan's launch count, not bytes, sets its time (config 1: 31 vs 45 us).
+// Beyond that a ragged butterfly stays on the generic kernels -- also a memory bound: a rank-1
+// butterfly would otherwise be stored 256x larger (once per op).
+static bool pad_pays(const Geom& G, int64_t entries, size_t cs) {
+  if (fast_eligible(G, 0, true)) return true;  // uniform rank 16: nothing to pad
+  const int64_t padded = 16 * (G.m + G.n) + G.nb * (int64_t)G.L * 512 + G.nb * 256;
+  return padded <= 3 * entries || (double)padded * (double)cs <= 16.0 * (1 << 20);
+}
+
 // every leaf of size `leaf` maps to a run of consecutive user rows (so whole rows can be copied)
 static bool leaves_contiguous(const int64_t* perm, int64_t n, int64_t leaf) {
   if (!perm) return true;
@@ -1234,6 +1246,7 @@ struct bf_s {
   size_t device_bytes = 0;
   Plan plan[2];  // [0] op N, [1] op C/T
   bool use_fast = false;
+  bool fused_only = false;  // BF_CREATE_FUSED_ONLY: the generic pool was released after the fused build
   FastPlan fast[2];
   // distributed
   bool dist = false;
@@ -1488,7 +1501,7 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
     // the fused kernels: uniform rank 16 as given, ranks <= 16 zero-padded to 16 (pad_rank16; env
     // BF_FAST_PAD = 0 keeps ragged ranks on the generic path, for A/B measurements)
     static const bool pad_ok = !getenv("BF_FAST_PAD") || atoi(getenv("BF_FAST_PAD")) != 0;
-    if (fast_eligible(G, d->dtype, !pad_ok) && h->m3 && !getenv("BF_DISABLE_FAST")) {
+    if (fast_eligible(G, d->dtype, !pad_ok) && h->m3 && !getenv("BF_DISABLE_FAST") && pad_pays(G, tot, cs)) {
       const bool cc = leaves_contiguous(d->col_perm, d->n, G.nv(0));
       const bool rc = leaves_contiguous(d->row_perm, d->m, G.mt(0));
       const bool exact = fast_eligible(G, d->dtype, true);
@@ -1513,6 +1526,14 @@ int bf_create(const bf_desc* d, int device, bf_handle* out) {
       h->fast[1].contig_in = rc;
       h->fast[1].contig_out = cc;
       h->use_fast = true;
+      if ((d->flags & BF_CREATE_FUSED_ONLY) && h->pool) {
+        // every op now runs on the fused records: release the generic pool (one of the three
+        // copies of the factors; extraction and export need it and then return BF_ERR_ARG)
+        BF_CK(cudaFree(h->pool));
+        h->pool = nullptr;
+        h->device_bytes -= (size_t)tot * cs;
+        h->fused_only = true;
+      }
     }
     h->G = std::move(G);
     *out = h.release();
@@ -1566,6 +1587,8 @@ int bf_export(bf_handle h, int64_t* lens, int32_t* rank_row, int32_t* rank_col, 
     DeviceGuard dg(h->device);
     const size_t cs = csize(h->dtype);
     void* dst[5] = {U, R, B, W, Vt};
+    require(!h->fused_only || !(U || R || B || W || Vt), BF_ERR_ARG,
+            "handle created with BF_CREATE_FUSED_ONLY keeps no factor pool to export");
     int64_t off = 0;
     for (int q = 0; q < 5; ++q) {
       if (dst[q] && L5[q]) BF_CK(cudaMemcpy(dst[q], static_cast<char*>(h->pool) + off * cs, L5[q] * cs, cudaMemcpyDeviceToHost));
@@ -3282,6 +3305,7 @@ namespace bfa {
 // the pool locations of the requested U rows / Vt columns).  Validates the indices.
 static XPart bf_extract_part(bf_handle h, int64_t nI, const int64_t* rows, int64_t nJ, const int64_t* cols) {
   const Geom& G = h->G;
+  require(!h->fused_only, BF_ERR_ARG, "handle created with BF_CREATE_FUSED_ONLY keeps no factor pool to extract from");
   require(nI >= 0 && nJ >= 0, BF_ERR_ARG, "negative size");
   require((nI == 0 || rows != nullptr) && (nJ == 0 || cols != nullptr), BF_ERR_ARG, "NULL index list");
   require(nJ <= (int64_t)65535 * 32, BF_ERR_ARG, "too many columns for one launch");

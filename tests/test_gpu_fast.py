@@ -239,3 +239,49 @@ def test_fused_leaf_in_equals_separate(monkeypatch, L, leaf):
         torch.cuda.synchronize()
         assert oracle.rel_err(host(Y1), oracle.apply_op(K, host(X), op)) <= 1e-12, op
         assert torch.equal(Y1, Y2), op
+
+
+def test_pad_policy_keeps_large_low_rank_generic():
+    """pad_pays (plan.cu): a large butterfly of ranks 1-2 would stream ~100x its entries once
+    padded to rank 16, so it stays on the generic kernels (and is stored once, unpadded); a
+    small one is padded onto the fused kernels.  Both against the level-by-level oracle."""
+    from oracle.stagewise import bf_apply_stagewise
+    for L, expect_fused in ((9, False), (4, True)):
+        nb = 1 << L
+        bf = random_ranks_butterfly(L, np.full(nb, 16), np.full(nb, 16), seed=L, rmin=1, rmax=2)
+        h = pkg.BFHandle(bf)
+        fused = h.rounds("N")[0]["name"].startswith("k_leaf")
+        assert fused == expect_fused, (L, h.rounds("N")[0]["name"])
+        if not fused:
+            assert h.info["device_bytes"] < 4 * bf.nnz() * 16 + (64 << 20)
+        for op in "NC":
+            X = random_rhs(bf.n if op == "N" else bf.m, 9, seed=3)
+            err = oracle.rel_err(host(h.apply(dev(X), op)), bf_apply_stagewise(bf, X, op))
+            assert err <= 1e-12, (L, op, err)
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_fused_only_releases_the_pool(dtype):
+    """BF_CREATE_FUSED_ONLY: the fused records alone serve every op (bit-identical applies), the
+    generic factor pool is gone from the device (device_bytes drops by the factor bytes) and
+    extraction / export refuse the handle."""
+    import ctypes as C
+    from paper_2007_00202_b200.bfapply import BFError
+    bf = random_butterfly(L=6, leaf=32, r=16, seed=9, dtype=dtype)
+    cs = 16 if dtype == np.complex128 else 8
+    h0 = pkg.BFHandle(bf)
+    h1 = pkg.BFHandle(bf, fused_only=True)
+    assert h0.info["device_bytes"] - h1.info["device_bytes"] == bf.nnz() * cs
+    for op, nr in (("N", 32), ("C", 5), ("T", 16)):
+        X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=4, dtype=dtype)
+        np.testing.assert_array_equal(host(h1.apply(dev(X), op)), host(h0.apply(dev(X), op)))
+    with pytest.raises(BFError):
+        h1.extract(np.arange(3), np.arange(4))
+    # a ragged butterfly that stays on the generic kernels keeps its pool
+    rng = np.random.default_rng(1)
+    bfr = random_ranks_butterfly(4, rng.integers(1, 20, 16), rng.integers(1, 20, 16), seed=1, rmin=1, rmax=30,
+                                 dtype=dtype)
+    hr = pkg.BFHandle(bfr, fused_only=True)
+    X = random_rhs(bfr.n, 3, seed=2, dtype=dtype)
+    assert oracle.rel_err(host(hr.apply(dev(X))), oracle.bf_apply(bfr, X)) <= TOL[dtype]
+    assert hr.extract(np.arange(2), np.arange(3)).shape == (2, 3)
