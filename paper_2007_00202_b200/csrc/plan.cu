@@ -1264,8 +1264,9 @@ struct bf_s {
   int64_t* d_lperm_out[2] = {nullptr, nullptr};
   // bf_apply_host pipelining: copy streams, per-buffer-set events, call counter
   std::mutex hmu;
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_cmp = nullptr;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  cudaEvent_t ev_st = nullptr;  // the caller's stream at the start of a call
   int64_t hcalls = 0;
   int h_last_op = -1;              // (op, nrhs, workspace) of the previous call: a change relocates
   int64_t h_last_nrhs = -1;        // the buffer sets inside the workspace
@@ -1277,9 +1278,12 @@ struct bf_s {
     cudaSetDevice(device);
     if (s_h2d) {
       cudaStreamSynchronize(s_h2d);
+      cudaStreamSynchronize(s_cmp);
       cudaStreamSynchronize(s_d2h);
       cudaStreamDestroy(s_h2d);
+      cudaStreamDestroy(s_cmp);
       cudaStreamDestroy(s_d2h);
+      cudaEventDestroy(ev_st);
       for (int k = 0; k < 2; ++k) {
         cudaEventDestroy(ev_h2d[k]);
         cudaEventDestroy(ev_cmp[k]);
@@ -1845,7 +1849,9 @@ int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx
     std::lock_guard<std::mutex> lk(h->hmu);
     if (!h->s_h2d) {
       BF_CK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+      BF_CK(cudaStreamCreateWithFlags(&h->s_cmp, cudaStreamNonBlocking));
       BF_CK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+      BF_CK(cudaEventCreateWithFlags(&h->ev_st, cudaEventDisableTiming));
       for (int k = 0; k < 2; ++k) {
         BF_CK(cudaEventCreateWithFlags(&h->ev_h2d[k], cudaEventDisableTiming));
         BF_CK(cudaEventCreateWithFlags(&h->ev_cmp[k], cudaEventDisableTiming));
@@ -1865,6 +1871,16 @@ int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx
     const bool relayout = h->hcalls > 0 && (op != h->h_last_op || nrhs != h->h_last_nrhs || work != h->h_last_work);
     if (h->hcalls >= 2) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_d2h[set], 0));
     if (relayout) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_d2h[set ^ 1], 0));
+    // The apply runs on a third handle-owned stream, so call k+1's apply needs only its own H2D
+    // (not call k's D2H, which `stream` waits for): in steady state the step takes max(H2D, apply,
+    // D2H), not max(H2D, D2H) + apply.  The workspace belongs to this pipeline between calls; on
+    // the first call and whenever it moves (relayout), the copies and the apply also wait for the
+    // caller's earlier work on `stream` (e.g. the allocation of `work`).
+    if (h->hcalls == 0 || relayout) {
+      BF_CK(cudaEventRecord(h->ev_st, st));
+      BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_st, 0));
+      BF_CK(cudaStreamWaitEvent(h->s_cmp, h->ev_st, 0));
+    }
     h->h_last_op = op;
     h->h_last_nrhs = nrhs;
     h->h_last_work = work;
@@ -1876,10 +1892,10 @@ int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx
     BF_CK(cudaEventRecord(h->ev_h2d[set], h->s_h2d));
     // the apply: after this call's H2D; its Y set was last read by call k - 2's D2H, which
     // `stream` already waited for
-    BF_CK(cudaStreamWaitEvent(st, h->ev_h2d[set], 0));
-    int rc = bf_apply_op(h, op, nrhs, dX, std::max<int64_t>(rx, 1), dY, std::max<int64_t>(ry, 1), work, s, stream);
+    BF_CK(cudaStreamWaitEvent(h->s_cmp, h->ev_h2d[set], 0));
+    int rc = bf_apply_op(h, op, nrhs, dX, std::max<int64_t>(rx, 1), dY, std::max<int64_t>(ry, 1), work, s, h->s_cmp);
     if (rc != BF_OK) return rc;
-    BF_CK(cudaEventRecord(h->ev_cmp[set], st));
+    BF_CK(cudaEventRecord(h->ev_cmp[set], h->s_cmp));
     BF_CK(cudaStreamWaitEvent(h->s_d2h, h->ev_cmp[set], 0));
     if (ldy == ry) {
       BF_CK(cudaMemcpyAsync(Yh, dY, (size_t)ry * nrhs * cs, cudaMemcpyDeviceToHost, h->s_d2h));
