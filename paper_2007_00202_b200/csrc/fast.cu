@@ -53,6 +53,15 @@ struct Stream {
   static constexpr int SPP = Cfg::PG / (S * FAST_FRAG);  // k-steps per page
   static constexpr int SPL = fast_spl((int)sizeof(E), S); // k-steps per page of the column-leaf op
   static constexpr int XT = SPL * Pol::KS * FAST_NB * (int)sizeof(E);  // X tile bytes per slot
+  // pages ahead of the ring's newest page whose factor records are prefetched into L2
+  // (cp.async.bulk.prefetch.L2; ncu of the complex64 4-level pass: half of the page waits found
+  // the page not yet landed).  Measured slower on config 5 (tools/gpurun_scripts/r2_g30.sh):
+  // c128 1.346 / 1.364 ms and c64 0.738 / 0.738 ms at 2 / 4 pages ahead against 1.258 / 0.676 ms
+  // without, so it is off (-DBF_PASS_PF=n for the A/B).
+#ifndef BF_PASS_PF
+#define BF_PASS_PF 0
+#endif
+  static constexpr int PF = BF_PASS_PF;
   __host__ __device__ static int steps_per_page(int kind) { return kind == FK_LEAF_IN ? SPL : SPP; }
   const FastArgs& A;
   unsigned char* ring;
@@ -62,12 +71,14 @@ struct Stream {
   int64_t nitems;
   int ppi;  // pages per item
   __device__ __forceinline__ int64_t item_of(int64_t i) const { return blockIdx.x + i * gridDim.x; }
-  __device__ void issue_page(int64_t j) const {
+  // factor bytes of page j (A records only): source, byte count, op, first k-step; false past the end
+  __device__ bool page_src(int64_t j, const unsigned char*& src, uint32_t& bytes, int& q, int& s0) const {
     const FastPass& P = A.p;
     const int64_t i = j / ppi;
     const int64_t item = item_of(i);
-    if (item >= nitems) return;
-    int r = (int)(j - i * ppi), q = 0;
+    if (item >= nitems) return false;
+    int r = (int)(j - i * ppi);
+    q = 0;
     for (;; ++q) {
       const int sp = steps_per_page(P.ops[q].kind);
       const int np = (P.ops[q].nsteps + sp - 1) / sp;
@@ -76,13 +87,32 @@ struct Stream {
     }
     const FastOp& op = P.ops[q];
     const int sp = steps_per_page(op.kind);
-    const int s0 = r * sp, nst = min(sp, op.nsteps - s0);
+    s0 = r * sp;
+    const int nst = min(sp, op.nsteps - s0);
     const int64_t w = item & (P.nwin - 1);  // local window index (records of this rank only)
-    const unsigned char* src =
-        static_cast<const unsigned char*>(A.F) + P.fbase + w * P.win_bytes + op.off + (int64_t)s0 * S * FAST_FRAG;
+    src = static_cast<const unsigned char*>(A.F) + P.fbase + w * P.win_bytes + op.off + (int64_t)s0 * S * FAST_FRAG;
+    bytes = (uint32_t)(nst * S * FAST_FRAG);
+    return true;
+  }
+  __device__ void issue_page(int64_t j) const {
+    const FastPass& P = A.p;
+    const unsigned char* src;
+    uint32_t bytes;
+    int q, s0;
+    if (!page_src(j, src, bytes, q, s0)) return;
+    // warm L2 with page j + PF (its factor records) while page j streams into the ring
+    if (PF > 0) {
+      const unsigned char* ps;
+      uint32_t pb;
+      int pq, ps0;
+      if (page_src(j + PF, ps, pb, pq, ps0)) bulk_prefetch_l2(ps, pb);
+    }
+    const int64_t i = j / ppi;
+    const int64_t item = item_of(i);
+    const FastOp& op = P.ops[q];
+    const int64_t w = item & (P.nwin - 1);
     const int slot = (int)(j % Cfg::NP);
     unsigned char* pg = ring + (size_t)slot * Cfg::PG;
-    const uint32_t bytes = (uint32_t)(nst * S * FAST_FRAG);
     if (op.kind != FK_LEAF_IN) {
       mbar_expect_tx(&full[slot], bytes);
       bulk_g2s(pg, src, bytes, &full[slot]);

@@ -221,6 +221,12 @@ __global__ void __launch_bounds__(256, MINB) k_stage_tile(StageArgs a) {
 //   B frag (4 x 8, [k][row])  of lane (g, t) = A(8 nt + g, k0 + t)
 //   C (8 x 8)  c[g][2t + e]   = out(row 8 nt + 2t + e, column 8w + g)
 // ------------------------------------------------------------------------------------
+// A/B knob (build with -DBF_TILE_BRANCHY=1): the round-2 first-cut k-loop with a per-n-tile branch
+#ifndef BF_TILE_BRANCHY
+#define BF_TILE_BRANCHY 0
+#endif
+__device__ __forceinline__ constexpr bool tile_branchy() { return BF_TILE_BRANCHY != 0; }
+
 template <bool M3, int NST, int MINB = 2>
 __global__ void __launch_bounds__(256, MINB) k_stage_tileT(StageArgs a) {
   using E = double2;
@@ -342,6 +348,50 @@ __global__ void __launch_bounds__(256, MINB) k_stage_tileT(StageArgs a) {
         __syncthreads();
         const E* sA = sm + (c % NST) * STAGE;
         const E* sB = sA + KC * SA;
+        // one chunk with the n-tile count a compile-time constant: every fragment of a k-step
+        // is loaded (and its 3M sum formed) before its DMMAs issue, with no per-n-tile branch
+        // between them (the branchy form left the DMMAs waiting on each load / DADD in turn --
+        // ncu: "wait" and short-scoreboard stalls led, DMMA 45 % active)
+        auto chunk = [&](auto ntc) {
+          constexpr int NTL = decltype(ntc)::value;
+#pragma unroll
+          for (int k0 = 0; k0 < KC; k0 += 4) {
+            const E x = sB[(k0 + t) * SB + cw + g];  // In^T fragment
+            E f[NTL];
+            double fs[NTL];
+#pragma unroll
+            for (int nt = 0; nt < NTL; ++nt) {
+              f[nt] = sA[(k0 + t) * SA + 8 * nt + g];  // A^T fragment
+              f[nt].y = conj_im(f[nt].y, cj);
+              fs[nt] = f[nt].x + f[nt].y;
+            }
+            const double xs = x.x + x.y;
+#pragma unroll
+            for (int nt = 0; nt < NTL; ++nt) {
+              if (M3) {
+                PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], x.x, f[nt].x);
+                PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.y, f[nt].y);
+              } else {  // 4M: re += xr fr - xi fi, im += xr fi + xi fr (exact on selection factors)
+                PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], x.x, f[nt].x);
+                PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], -x.y, f[nt].y);
+                PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.x, f[nt].y);
+                PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.y, f[nt].x);
+              }
+            }
+            if (M3) {
+#pragma unroll
+              for (int nt = 0; nt < NTL; ++nt) PolC128<1>::mma(acc[2][nt][0], acc[2][nt][1], xs, fs[nt]);
+            }
+          }
+        };
+        if (!tile_branchy()) {
+          switch (ntiles) {
+            case 1: chunk(std::integral_constant<int, 1>{}); break;
+            case 2: chunk(std::integral_constant<int, 2>{}); break;
+            case 3: chunk(std::integral_constant<int, 3>{}); break;
+            default: chunk(std::integral_constant<int, 4>{}); break;
+          }
+        } else {
 #pragma unroll
         for (int k0 = 0; k0 < KC; k0 += 4) {
           const E x = sB[(k0 + t) * SB + cw + g];  // In^T fragment
@@ -355,7 +405,7 @@ __global__ void __launch_bounds__(256, MINB) k_stage_tileT(StageArgs a) {
                 PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], x.x, f.x);
                 PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.y, f.y);
                 PolC128<1>::mma(acc[2][nt][0], acc[2][nt][1], xs, f.x + f.y);
-              } else {  // 4M: re += xr fr - xi fi, im += xr fi + xi fr (exact on selection factors)
+              } else {
                 PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], x.x, f.x);
                 PolC128<1>::mma(acc[0][nt][0], acc[0][nt][1], -x.y, f.y);
                 PolC128<1>::mma(acc[1][nt][0], acc[1][nt][1], x.x, f.y);
@@ -363,6 +413,7 @@ __global__ void __launch_bounds__(256, MINB) k_stage_tileT(StageArgs a) {
               }
             }
           }
+        }
         }
         __syncthreads();
       }
