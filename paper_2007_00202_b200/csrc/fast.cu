@@ -23,7 +23,7 @@
 
 namespace bfa {
 
-template <class Pol, int D, int HV = 2>
+template <class Pol, int D, int HV = 2, int PGB = 32768>
 struct PassCfg {
   using E = typename Pol::E;
   static constexpr int WINH = (1 << (D > 3 ? D : 3)) * FAST_HSLAB;  // half window (elements)
@@ -31,24 +31,24 @@ struct PassCfg {
   // padding and is neither loaded nor stored, so a buffer holds one half
   static constexpr int HALVES = HV == 2 ? 2 : 1;
   static constexpr int WIN = HALVES * WINH;
-  static constexpr int PG = 32768;                            // ring page (bytes)
+  static constexpr int PG = PGB;                              // ring page (bytes)
   // ring pages: complex128 3 (2 x 64 KB windows), complex64 4 (3-level windows) or 3 (4-level).
   // (Measured on complex64: a 5th page or a third window buffer, which lets the next window load
   // a whole item ahead, made the 3-level pass slower: 0.1156 / 0.1168 vs 0.1136 ms.)  With one
   // window half (nrhs <= 16) the freed shared memory could deepen the ring to 5-6 pages: measured
   // neutral at nrhs 1 / 8 / 16 for both dtypes (0.639 vs 0.636 ms c128 at nrhs 1,
   // tools/gpurun_scripts/r2_g9.sh), so the ring keeps its depth.
-  static constexpr int NP = sizeof(E) == 16 ? 3 : D > 3 ? 3 : 4;
+  static constexpr int NP = (sizeof(E) == 16 ? 3 : D > 3 ? 3 : 4) * (32768 / PGB);
   __host__ __device__ static constexpr size_t bars_off() { return 2 * WIN * sizeof(E) + (size_t)NP * PG; }
   __host__ __device__ static constexpr size_t smem() { return bars_off() + (1 + NP) * 8 + (1 + NP) * 4; }
 };
 
 // The operand stream of one CTA: page j (0, 1, 2, ...) is k-steps [s0, s0 + nst) of op q of the
 // CTA's item j / PPI.
-template <class Pol, int D, int HV = 2>
+template <class Pol, int D, int HV = 2, int PGB = 32768>
 struct Stream {
   using E = typename Pol::E;
-  using Cfg = PassCfg<Pol, D, HV>;
+  using Cfg = PassCfg<Pol, D, HV, PGB>;
   static constexpr int S = 1 << D;
   static constexpr int SPP = Cfg::PG / (S * FAST_FRAG);  // k-steps per page
   static constexpr int SPL = fast_spl((int)sizeof(E), S); // k-steps per page of the column-leaf op
@@ -165,11 +165,14 @@ struct Stream {
 // HV: column halves with work (1 when nrhs <= 16, the second half of the only tile being padding;
 // 0 = narrow, nrhs <= 8: one half, one 8-column n-tile per warp (Pol::NT == 1), a warp per slot).
 // A compile-time choice, so that the two-half instantiation keeps its code generation.
-template <class Pol, int D, int HV = 2>
+template <class Pol, int D, int HV = 2, int PGB = 32768>
 __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_constant__ FastArgs A) {
   using E = typename Pol::E;
-  using Cfg = PassCfg<Pol, D, HV>;
-  using St = Stream<Pol, D, HV>;
+  using Cfg = PassCfg<Pol, D, HV, PGB>;
+  using St = Stream<Pol, D, HV, PGB>;
+  // the fused leaf ops assume 32 KB pages (whole 16-row groups / the X tiles of fast_spl); the
+  // small-page instantiation serves window passes without them (launch_fast_pass)
+  constexpr bool LEAF_OK = Pol::LEAF_OPS && PGB == 32768;
   constexpr int NT = Pol::NT;
   constexpr int S = 1 << D;                          // slots of the window
   constexpr int CT = HV == 0 ? 1 : 2 / NT;           // column tiles per slot (in a half)
@@ -283,8 +286,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         sp0 = win + (((2 * tt) << (ds - 1)) + (u >> 1)) * FAST_HSLAB;
         sp1 = win + (((2 * tt + 1) << (ds - 1)) + (u >> 1)) * FAST_HSLAB;
       }
-      if (Pol::LEAF_OPS && op.kind == FK_LEAF_OUT) {
-        if constexpr (Pol::LEAF_OPS) {
+      if (LEAF_OK && op.kind == FK_LEAF_OUT) {
+        if constexpr (LEAF_OK) {
         // fused row leaf (a5): Y(rows of this slot's leaf) = A (leaf x 16) y (16 x 32), one 16-row
         // group at a time; A records stream through the ring like any op, y is this slot's slab
         const int ds2 = P.d - op.s;
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
           __syncwarp();
           if (lane == 0 && !(diag & 1)) {
-            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
+            if (atom_add_release_page(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
           }
           ++j;
           if (++slot == NP) {
@@ -341,8 +344,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         cur = rd ^ 1;
         continue;  // (always the last op; one slot per warp)
       }
-      if (Pol::LEAF_OPS && op.kind == FK_LEAF_IN) {
-        if constexpr (Pol::LEAF_OPS) {
+      if (LEAF_OK && op.kind == FK_LEAF_IN) {
+        if constexpr (LEAF_OK) {
         // fused column leaf (a1): z = A (16 x leaf) X(rows of this slot's leaf, tile); every page
         // carries SPL k-steps of A records and of X rows (the 2-D TMA tiles of Stream::issue_page)
         constexpr int SPL = St::SPL;
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           }
           __syncwarp();
           if (lane == 0 && !(diag & 1)) {
-            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
+            if (atom_add_release_page(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
           }
           ++j;
           if (++slot == NP) {
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
           // release the page; the last warp out re-arms it with page j + NP
           __syncwarp();
           if (lane == 0 && !(diag & 1)) {
-            if (atom_add_acqrel(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
+            if (atom_add_release_page(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
           }
           ++j;
           if (++slot == NP) {
@@ -458,13 +461,13 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
 
 const char* fast_kernel_name(int dtype) { return dtype == BF_C128 ? "k_bf_pass<c128>" : "k_bf_pass<c64>"; }
 
-template <class Pol, int D, int HV>
+template <class Pol, int D, int HV, int PGB = 32768>
 static void launch_hv(const FastArgs& a, unsigned grid, cudaStream_t st) {
   static std::atomic<size_t> attr[BF_MAX_DEVICES];
-  const size_t smem = PassCfg<Pol, D, HV>::smem();
-  static_assert(PassCfg<Pol, D, HV>::smem() <= 227 * 1024, "pass kernel shared memory");
-  ensure_smem_attr(attr, (const void*)k_bf_pass<Pol, D, HV>, smem);
-  launch_pdl(k_bf_pass<Pol, D, HV>, grid, FAST_THREADS, smem, st, a);
+  const size_t smem = PassCfg<Pol, D, HV, PGB>::smem();
+  static_assert(PassCfg<Pol, D, HV, PGB>::smem() <= 227 * 1024, "pass kernel shared memory");
+  ensure_smem_attr(attr, (const void*)k_bf_pass<Pol, D, HV, PGB>, smem);
+  launch_pdl(k_bf_pass<Pol, D, HV, PGB>, grid, FAST_THREADS, smem, st, a);
 }
 
 template <class Pol, int D>
@@ -483,6 +486,15 @@ void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
     else if (d == 2) launch_hv<PolC128<1>, 2, 0>(a, grid, st);
     else launch_hv<PolC128<1>, 1, 0>(a, grid, st);
   } else if (dtype == BF_C128) {
+    // 16 KB ring pages (six instead of three 32 KB ones: a page is released after 2 k-steps, so
+    // the two column halves may drift further apart) for 3-level passes without leaf ops; env
+    // BF_PASS_SMALLPG = 1 (A/B measurement)
+    static const bool small_pg = getenv("BF_PASS_SMALLPG") && atoi(getenv("BF_PASS_SMALLPG")) != 0;
+    const bool leaf_ops = a.p.xleaf || a.p.ops[a.p.nops - 1].kind == FK_LEAF_OUT;
+    if (small_pg && d == 3 && a.halves == 2 && !leaf_ops) {
+      launch_hv<PolC128<2>, 3, 2, 16384>(a, grid, st);
+      return;
+    }
     if (d == 3) launch_one<PolC128<2>, 3>(a, grid, st);
     else if (d == 2) launch_one<PolC128<2>, 2>(a, grid, st);  // 8 warps x 16 columns: 3 % faster than 16 x 8
     else launch_one<PolC128<1>, 1>(a, grid, st);

@@ -86,6 +86,24 @@ __device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
   asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;\n" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
   return old;
 }
+// Page-release counter increment without the acquire-release fence (SASS: MEMBAR.ALL.CTA before
+// the ATOMS, which also waits for the thread's in-flight global stores).  Sufficient for the
+// ring pages: a warp releases a page only after the DMMAs / HMMAs of its last k-step on that page
+// have issued, and those read the registers its LDS wrote, so every shared-memory read of the
+// page is complete when the counter moves; the last arriver's TMA then overwrites it.
+// (-DBF_RELEASE_ACQREL=1 restores the fenced form, for the A/B.)
+#ifndef BF_RELEASE_ACQREL
+#define BF_RELEASE_ACQREL 0
+#endif
+__device__ __forceinline__ int atom_add_release_page(int* p, int v) {
+#if BF_RELEASE_ACQREL
+  return atom_add_acqrel(p, v);
+#else
+  int old;
+  asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], %2;\n" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+#endif
+}
 // conditional negation by flipping the sign bit on the integer pipe (a select of -x would cost
 // an FP64-pipe DADD next to the DMMAs)
 __device__ __forceinline__ double conj_im(double x, bool cj) {
