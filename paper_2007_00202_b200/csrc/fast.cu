@@ -72,10 +72,13 @@ struct Stream {
   int ppi;  // pages per item
   __device__ __forceinline__ int64_t item_of(int64_t i) const { return blockIdx.x + i * gridDim.x; }
   // factor bytes of page j (A records only): source, byte count, op, first k-step; false past the end
-  __device__ bool page_src(int64_t j, const unsigned char*& src, uint32_t& bytes, int& q, int& s0) const {
+  __device__ bool page_src(int64_t j, const unsigned char*& src, uint32_t& bytes, int& q, int& s0,
+                           int64_t& item) const {
     const FastPass& P = A.p;
-    const int64_t i = j / ppi;
-    const int64_t item = item_of(i);
+    // (32-bit division whenever the page index fits: it runs on the ring's critical path, in
+    // the thread that re-arms the page)
+    const int64_t i = j < 0xffffffffll ? (int64_t)((uint32_t)j / (uint32_t)ppi) : j / ppi;
+    item = item_of(i);
     if (item >= nitems) return false;
     int r = (int)(j - i * ppi);
     q = 0;
@@ -99,16 +102,16 @@ struct Stream {
     const unsigned char* src;
     uint32_t bytes;
     int q, s0;
-    if (!page_src(j, src, bytes, q, s0)) return;
+    int64_t item;
+    if (!page_src(j, src, bytes, q, s0, item)) return;
     // warm L2 with page j + PF (its factor records) while page j streams into the ring
     if (PF > 0) {
       const unsigned char* ps;
       uint32_t pb;
       int pq, ps0;
-      if (page_src(j + PF, ps, pb, pq, ps0)) bulk_prefetch_l2(ps, pb);
+      int64_t pit;
+      if (page_src(j + PF, ps, pb, pq, ps0, pit)) bulk_prefetch_l2(ps, pb);
     }
-    const int64_t i = j / ppi;
-    const int64_t item = item_of(i);
     const FastOp& op = P.ops[q];
     const int64_t w = item & (P.nwin - 1);
     const int slot = (int)(j % Cfg::NP);
