@@ -31,5 +31,4 @@ timeout 900 python tools/time_next.py > $O/time_next.jsonl 2> $O/time_next.err
 timeout 600 python tools/time_extract.py c128 > $O/extract_c128.txt 2>&1
 for f in $O/*.ncu-rep; do python tools/ncu_summary.py $f > ${f%.ncu-rep}.txt 2>&1; done
 timeout 300 python tools/pcie_bw.py > $O/pcie_bw.txt 2>&1
-BF_TILE_BRANCHY_NOTE=1 true
 echo done
