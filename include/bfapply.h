@@ -152,10 +152,11 @@ int bf_apply_op(bf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, v
                 int64_t ldy, void* work, size_t work_bytes, bf_stream_t stream);
 /* End-to-end form with HOST X / Y (pinned for full speed): H2D copy of X, apply, D2H copy
  * of Y.  Y_host is complete once the caller synchronises `stream`; X_host must stay unchanged
- * until then.  The copies run on two streams owned by the handle and consecutive calls
- * alternate between two sets of device X / Y copies, so call k+1's H2D overlaps call k's D2H
- * (the two PCIe directions are independent); calls on one handle are serialised (internal
- * lock).  The workspace must be at least bf_workspace_size_host bytes (it also holds the two
+ * until then.  The copies and the apply run on three streams owned by the handle and
+ * consecutive calls alternate between two sets of device X / Y copies, so call k+1's H2D and
+ * apply overlap call k's D2H (the two PCIe directions are independent); calls on one handle are
+ * serialised (internal lock); on the first call, and when op, nrhs or the workspace change, the
+ * pipeline also waits for the caller's earlier work on `stream`.  The workspace must be at least bf_workspace_size_host bytes (it also holds the two
  * sets of device copies) and the same workspace must be passed to consecutive calls. */
 int bf_workspace_size_host(bf_handle h, int op, int64_t nrhs, size_t* bytes);
 int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* X_host, int64_t ldx,
@@ -169,6 +170,8 @@ int hodbf_workspace_size(hodbf_handle h, int64_t nrhs, size_t* bytes);
 /* Y (n x nrhs) <- A X, A^T X or A^H X. */
 int hodbf_apply(hodbf_handle h, int op, int64_t nrhs, const void* X, int64_t ldx, void* Y,
                 int64_t ldy, void* work, size_t work_bytes, bf_stream_t stream);
+/* hodbf_apply_host: as bf_apply_host (same three-stream pipeline; workspace from
+ * hodbf_workspace_size_host, the same one passed to consecutive calls). */
 int hodbf_workspace_size_host(hodbf_handle h, int64_t nrhs, size_t* bytes);
 int hodbf_apply_host(hodbf_handle h, int op, int64_t nrhs, const void* X_host, int64_t ldx,
                      void* Y_host, int64_t ldy, void* work, size_t work_bytes,

@@ -1233,6 +1233,36 @@ static bool selection_only(const void* p, int64_t entries, size_t cs) {
   return true;
 }
 
+// bf_apply_host / hodbf_apply_host pipelining: H2D on one handle-owned stream, the apply on a
+// second, D2H on a third, with two alternating device X / Y buffer sets inside the workspace, so
+// call k+1's H2D and apply overlap call k's D2H (the two PCIe directions are independent).
+struct HostPipe {
+  std::mutex mu;  // calls on one handle are serialised
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_cmp = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  cudaEvent_t ev_st = nullptr;  // the caller's stream at the start of a call
+  int64_t calls = 0;
+  int last_op = -1;              // (op, nrhs, workspace) of the previous call: a change relocates
+  int64_t last_nrhs = -1;        // the buffer sets inside the workspace
+  const void* last_work = nullptr;
+  void release() {
+    if (!s_h2d) return;
+    cudaStreamSynchronize(s_h2d);
+    cudaStreamSynchronize(s_cmp);
+    cudaStreamSynchronize(s_d2h);
+    cudaStreamDestroy(s_h2d);
+    cudaStreamDestroy(s_cmp);
+    cudaStreamDestroy(s_d2h);
+    cudaEventDestroy(ev_st);
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(ev_h2d[k]);
+      cudaEventDestroy(ev_cmp[k]);
+      cudaEventDestroy(ev_d2h[k]);
+    }
+    s_h2d = nullptr;
+  }
+};
+
 struct bf_s {
   int dtype = BF_C128;
   int device = 0;
@@ -1264,32 +1294,13 @@ struct bf_s {
   int64_t* d_lperm_out[2] = {nullptr, nullptr};
   // bf_apply_host pipelining: copy streams, per-buffer-set events, call counter
   std::mutex hmu;
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_cmp = nullptr;
-  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
-  cudaEvent_t ev_st = nullptr;  // the caller's stream at the start of a call
-  int64_t hcalls = 0;
-  int h_last_op = -1;              // (op, nrhs, workspace) of the previous call: a change relocates
-  int64_t h_last_nrhs = -1;        // the buffer sets inside the workspace
-  const void* h_last_work = nullptr;
+  HostPipe hp;
   std::vector<int64_t> h_rinv, h_cinv;  // bf_extract: user index -> tree position (filled on first use)
   XScratch xs;                          // bf_extract's device scratch
   ~bf_s() {
     if (host_only) return;
     cudaSetDevice(device);
-    if (s_h2d) {
-      cudaStreamSynchronize(s_h2d);
-      cudaStreamSynchronize(s_cmp);
-      cudaStreamSynchronize(s_d2h);
-      cudaStreamDestroy(s_h2d);
-      cudaStreamDestroy(s_cmp);
-      cudaStreamDestroy(s_d2h);
-      cudaEventDestroy(ev_st);
-      for (int k = 0; k < 2; ++k) {
-        cudaEventDestroy(ev_h2d[k]);
-        cudaEventDestroy(ev_cmp[k]);
-        cudaEventDestroy(ev_d2h[k]);
-      }
-    }
+    hp.release();
     for (int k = 0; k < 2; ++k) {
       free_plan(plan[k]);
       free_plan(pre[k]);
@@ -1324,8 +1335,10 @@ struct hodbf_s {
   int64_t factor_entries = 0;
   size_t device_bytes = 0;
   Plan plan[2];
+  HostPipe hp;  // hodbf_apply_host
   ~hodbf_s() {
     cudaSetDevice(device);
+    hp.release();
     free_plan(plan[0]);
     free_plan(plan[1]);
     if (pool) cudaFree(pool);
@@ -1829,11 +1842,72 @@ int bf_workspace_size_host(bf_handle h, int op, int64_t nrhs, size_t* bytes) {
   return BF_OK;
 }
 
-// Host-memory apply, pipelined across calls: the H2D copy of X and the D2H copy of Y run on the
-// handle's two copy streams (the two PCIe directions are independent), the apply on `stream`.
-// Call k uses device buffer set k % 2, so the H2D copy of call k+1 overlaps the D2H copy of call
-// k; every call's own copies are still inside it: `stream` waits for this call's D2H before
-// anything later on it, so Y_host is complete when the caller synchronises `stream`.
+}  // extern "C"
+
+namespace bfa {
+// One host-to-host apply through the HostPipe: H2D of X into buffer set k & 1 (after call k - 2's
+// D2H released it; after a relayout, after both sets' D2H), the apply on the compute stream (after
+// this call's H2D only), D2H of Y; the caller's stream waits for the D2H, so Y_host is complete
+// in its order.  The workspace belongs to this pipeline between calls; on the first call and
+// after a relayout the copies and the apply also wait for the caller's earlier work on `st` (e.g.
+// the workspace's allocation).  Layout of `work`: [apply workspace s][set 0: X | Y][set 1: X | Y].
+template <class Apply>
+static void host_pipeline(HostPipe& hp, int op, int64_t nrhs, const void* Xh, int64_t ldx, int64_t rx, void* Yh,
+                          int64_t ldy, int64_t ry, void* work, size_t s, size_t cs, cudaStream_t st, Apply apply) {
+  std::lock_guard<std::mutex> lk(hp.mu);
+  if (!hp.s_h2d) {
+    BF_CK(cudaStreamCreateWithFlags(&hp.s_h2d, cudaStreamNonBlocking));
+    BF_CK(cudaStreamCreateWithFlags(&hp.s_cmp, cudaStreamNonBlocking));
+    BF_CK(cudaStreamCreateWithFlags(&hp.s_d2h, cudaStreamNonBlocking));
+    BF_CK(cudaEventCreateWithFlags(&hp.ev_st, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k) {
+      BF_CK(cudaEventCreateWithFlags(&hp.ev_h2d[k], cudaEventDisableTiming));
+      BF_CK(cudaEventCreateWithFlags(&hp.ev_cmp[k], cudaEventDisableTiming));
+      BF_CK(cudaEventCreateWithFlags(&hp.ev_d2h[k], cudaEventDisableTiming));
+    }
+  }
+  const size_t bx = align256((size_t)rx * nrhs * cs), by = align256((size_t)ry * nrhs * cs);
+  const int set = (int)(hp.calls & 1);
+  char* dX = static_cast<char*>(work) + s + set * (bx + by);
+  char* dY = dX + bx;
+  // The X / Y regions of a set move with (op, nrhs) -- the slab workspace grows with nrhs and rx /
+  // ry swap with op -- and with the workspace pointer, so after such a change this call's regions
+  // may overlap the other set's: wait for both.
+  const bool relayout = hp.calls > 0 && (op != hp.last_op || nrhs != hp.last_nrhs || work != hp.last_work);
+  if (hp.calls >= 2) BF_CK(cudaStreamWaitEvent(hp.s_h2d, hp.ev_d2h[set], 0));
+  if (relayout) BF_CK(cudaStreamWaitEvent(hp.s_h2d, hp.ev_d2h[set ^ 1], 0));
+  if (hp.calls == 0 || relayout) {
+    BF_CK(cudaEventRecord(hp.ev_st, st));
+    BF_CK(cudaStreamWaitEvent(hp.s_h2d, hp.ev_st, 0));
+    BF_CK(cudaStreamWaitEvent(hp.s_cmp, hp.ev_st, 0));
+  }
+  hp.last_op = op;
+  hp.last_nrhs = nrhs;
+  hp.last_work = work;
+  if (ldx == rx)
+    BF_CK(cudaMemcpyAsync(dX, Xh, (size_t)rx * nrhs * cs, cudaMemcpyHostToDevice, hp.s_h2d));
+  else
+    BF_CK(cudaMemcpy2DAsync(dX, rx * cs, Xh, ldx * cs, rx * cs, nrhs, cudaMemcpyHostToDevice, hp.s_h2d));
+  BF_CK(cudaEventRecord(hp.ev_h2d[set], hp.s_h2d));
+  BF_CK(cudaStreamWaitEvent(hp.s_cmp, hp.ev_h2d[set], 0));
+  const int rc = apply(dX, dY, hp.s_cmp);
+  if (rc != BF_OK) throw Err{rc, bf_last_error()};
+  BF_CK(cudaEventRecord(hp.ev_cmp[set], hp.s_cmp));
+  BF_CK(cudaStreamWaitEvent(hp.s_d2h, hp.ev_cmp[set], 0));
+  if (ldy == ry)
+    BF_CK(cudaMemcpyAsync(Yh, dY, (size_t)ry * nrhs * cs, cudaMemcpyDeviceToHost, hp.s_d2h));
+  else
+    BF_CK(cudaMemcpy2DAsync(Yh, ldy * cs, dY, ry * cs, ry * cs, nrhs, cudaMemcpyDeviceToHost, hp.s_d2h));
+  BF_CK(cudaEventRecord(hp.ev_d2h[set], hp.s_d2h));
+  BF_CK(cudaStreamWaitEvent(st, hp.ev_d2h[set], 0));
+  ++hp.calls;
+}
+}  // namespace bfa
+
+extern "C" {
+
+// Host-memory apply, pipelined across calls (host_pipeline): every call's own copies are inside
+// it, and `stream` waits for this call's D2H, so Y_host is complete when the caller synchronises it.
 int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx, void* Yh, int64_t ldy,
                   void* work, size_t work_bytes, bf_stream_t stream) {
   if (!h) return fail(Err{BF_ERR_ARG, "NULL handle"});
@@ -1846,65 +1920,11 @@ int bf_apply_host(bf_handle h, int op, int64_t nrhs, const void* Xh, int64_t ldx
     validate_apply(nrhs, Xh, ldx, rx, Yh, ldy, ry, work_bytes, need, csize(h->dtype));
     if (nrhs == 0) return BF_OK;
     DeviceGuard dg(h->device);
-    std::lock_guard<std::mutex> lk(h->hmu);
-    if (!h->s_h2d) {
-      BF_CK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
-      BF_CK(cudaStreamCreateWithFlags(&h->s_cmp, cudaStreamNonBlocking));
-      BF_CK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
-      BF_CK(cudaEventCreateWithFlags(&h->ev_st, cudaEventDisableTiming));
-      for (int k = 0; k < 2; ++k) {
-        BF_CK(cudaEventCreateWithFlags(&h->ev_h2d[k], cudaEventDisableTiming));
-        BF_CK(cudaEventCreateWithFlags(&h->ev_cmp[k], cudaEventDisableTiming));
-        BF_CK(cudaEventCreateWithFlags(&h->ev_d2h[k], cudaEventDisableTiming));
-      }
-    }
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t cs = csize(h->dtype);
-    const size_t bx = align256((size_t)rx * nrhs * cs), by = align256((size_t)ry * nrhs * cs);
-    const int set = (int)(h->hcalls & 1);
-    char* dX = static_cast<char*>(work) + s + set * (bx + by);
-    char* dY = dX + bx;
-    // H2D into this set once call k - 2 is done with it: its apply read dX and its D2H read dY
-    // (ev_d2h follows ev_cmp).  The X / Y regions of a set move with (op, nrhs) -- the slab
-    // workspace grows with nrhs and rx / ry swap with op -- and with the workspace pointer, so
-    // after such a change this call's regions may overlap the other set's: wait for both.
-    const bool relayout = h->hcalls > 0 && (op != h->h_last_op || nrhs != h->h_last_nrhs || work != h->h_last_work);
-    if (h->hcalls >= 2) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_d2h[set], 0));
-    if (relayout) BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_d2h[set ^ 1], 0));
-    // The apply runs on a third handle-owned stream, so call k+1's apply needs only its own H2D
-    // (not call k's D2H, which `stream` waits for): in steady state the step takes max(H2D, apply,
-    // D2H), not max(H2D, D2H) + apply.  The workspace belongs to this pipeline between calls; on
-    // the first call and whenever it moves (relayout), the copies and the apply also wait for the
-    // caller's earlier work on `stream` (e.g. the allocation of `work`).
-    if (h->hcalls == 0 || relayout) {
-      BF_CK(cudaEventRecord(h->ev_st, st));
-      BF_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_st, 0));
-      BF_CK(cudaStreamWaitEvent(h->s_cmp, h->ev_st, 0));
-    }
-    h->h_last_op = op;
-    h->h_last_nrhs = nrhs;
-    h->h_last_work = work;
-    if (ldx == rx) {
-      BF_CK(cudaMemcpyAsync(dX, Xh, (size_t)rx * nrhs * cs, cudaMemcpyHostToDevice, h->s_h2d));
-    } else {
-      BF_CK(cudaMemcpy2DAsync(dX, rx * cs, Xh, ldx * cs, rx * cs, nrhs, cudaMemcpyHostToDevice, h->s_h2d));
-    }
-    BF_CK(cudaEventRecord(h->ev_h2d[set], h->s_h2d));
-    // the apply: after this call's H2D; its Y set was last read by call k - 2's D2H, which
-    // `stream` already waited for
-    BF_CK(cudaStreamWaitEvent(h->s_cmp, h->ev_h2d[set], 0));
-    int rc = bf_apply_op(h, op, nrhs, dX, std::max<int64_t>(rx, 1), dY, std::max<int64_t>(ry, 1), work, s, h->s_cmp);
-    if (rc != BF_OK) return rc;
-    BF_CK(cudaEventRecord(h->ev_cmp[set], h->s_cmp));
-    BF_CK(cudaStreamWaitEvent(h->s_d2h, h->ev_cmp[set], 0));
-    if (ldy == ry) {
-      BF_CK(cudaMemcpyAsync(Yh, dY, (size_t)ry * nrhs * cs, cudaMemcpyDeviceToHost, h->s_d2h));
-    } else {
-      BF_CK(cudaMemcpy2DAsync(Yh, ldy * cs, dY, ry * cs, ry * cs, nrhs, cudaMemcpyDeviceToHost, h->s_d2h));
-    }
-    BF_CK(cudaEventRecord(h->ev_d2h[set], h->s_d2h));
-    BF_CK(cudaStreamWaitEvent(st, h->ev_d2h[set], 0));  // Y_host complete in `stream` order
-    ++h->hcalls;
+    host_pipeline(h->hp, op, nrhs, Xh, ldx, rx, Yh, ldy, ry, work, s, csize(h->dtype), static_cast<cudaStream_t>(stream),
+                  [&](void* dX, void* dY, cudaStream_t sc) {
+                    return bf_apply_op(h, op, nrhs, dX, std::max<int64_t>(rx, 1), dY, std::max<int64_t>(ry, 1), work,
+                                       s, sc);
+                  });
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
@@ -2231,7 +2251,7 @@ int hodbf_workspace_size_host(hodbf_handle h, int64_t nrhs, size_t* bytes) {
   if (!h || !bytes || nrhs < 0) return fail(Err{BF_ERR_ARG, "bad argument"});
   size_t s = 0;
   hodbf_workspace_size(h, nrhs, &s);
-  *bytes = s + 2 * align256((size_t)h->n * nrhs * csize(h->dtype));
+  *bytes = s + 4 * align256((size_t)h->n * nrhs * csize(h->dtype));  // two X / Y sets (HostPipe)
   return BF_OK;
 }
 
@@ -2245,14 +2265,10 @@ int hodbf_apply_host(hodbf_handle h, int op, int64_t nrhs, const void* Xh, int64
     validate_apply(nrhs, Xh, ldx, h->n, Yh, ldy, h->n, work_bytes, need, csize(h->dtype));
     if (nrhs == 0 || h->n == 0) return BF_OK;
     DeviceGuard dg(h->device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t cs = csize(h->dtype);
-    char* dX = static_cast<char*>(work) + s;
-    char* dY = dX + align256((size_t)h->n * nrhs * cs);
-    BF_CK(cudaMemcpy2DAsync(dX, h->n * cs, Xh, ldx * cs, h->n * cs, nrhs, cudaMemcpyHostToDevice, st));
-    int rc = hodbf_apply(h, op, nrhs, dX, h->n, dY, h->n, work, s, stream);
-    if (rc != BF_OK) return rc;
-    BF_CK(cudaMemcpy2DAsync(Yh, ldy * cs, dY, h->n * cs, h->n * cs, nrhs, cudaMemcpyDeviceToHost, st));
+    host_pipeline(h->hp, op, nrhs, Xh, ldx, h->n, Yh, ldy, h->n, work, s, csize(h->dtype),
+                  static_cast<cudaStream_t>(stream), [&](void* dX, void* dY, cudaStream_t sc) {
+                    return hodbf_apply(h, op, nrhs, dX, h->n, dY, h->n, work, s, sc);
+                  });
     return BF_OK;
   } catch (const Err& e) {
     return fail(e);
