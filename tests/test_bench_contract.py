@@ -56,6 +56,8 @@ def test_gpu_arm_line(dtype, nrhs):
     assert 0 < r["other_bound"]["frac"] <= 1.0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     e = d["e2e"]
-    assert e["unit"] == "GB/s" and 0 < e["value"] < d["value"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    # e2e overlaps the copies with the applies (three streams), so with small transfers (nrhs 1)
+    # it approaches the device-resident rate; it cannot beat it beyond timing noise
+    assert e["unit"] == "GB/s" and 0 < e["value"] < 1.1 * d["value"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 3 * len(d["per_round"]) > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
