@@ -166,7 +166,8 @@ struct Stream {
 };
 
 // HV: column halves with work (1 when nrhs <= 16, the second half of the only tile being padding;
-// 0 = narrow, nrhs <= 8: one half, one 8-column n-tile per warp (Pol::NT == 1), a warp per slot).
+// 0 = narrow, nrhs <= 8: one half, one 8-column n-tile per warp (Pol::NT == 1), a warp per slot;
+// 3 = nrhs 9-16: one half worked by all 16 warps).
 // A compile-time choice, so that the two-half instantiation keeps its code generation.
 template <class Pol, int D, int HV = 2, int PGB = 32768>
 __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_constant__ FastArgs A) {
@@ -180,11 +181,13 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   constexpr int S = 1 << D;                          // slots of the window
   constexpr int CT = HV == 0 ? 1 : 2 / NT;           // column tiles per slot (in a half)
   static_assert(HV != 0 || NT == 1, "narrow passes use one 8-column n-tile per warp");
+  // warps per working half: 8, or all 16 on the one half of nrhs 9-16 (HV = 3)
+  constexpr int NCH = HV == 3 ? FAST_NCONS : FAST_NCONS_HALF;
   // slots per warp: 2 for 4-level windows (16 slots, 8 warps per half), else 1
-  constexpr int SPW = S * CT > FAST_NCONS_HALF ? S * CT / FAST_NCONS_HALF : 1;
+  constexpr int SPW = S * CT > NCH ? S * CT / NCH : 1;
   static_assert(SPW == 1 || CT == 1, "several slots per warp need whole-slot warps");
   constexpr int NACTH = S * CT / SPW;                // active warps per half
-  constexpr int NACT = 2 * NACTH;                    // active warps
+  constexpr int NACT = (HV == 3 ? 1 : 2) * NACTH;    // active warps
   constexpr int SPP = St::SPP;                       // k-steps per page
   constexpr int NP = Cfg::NP;
   constexpr int WIN = Cfg::WIN;
@@ -233,11 +236,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
     }
   }
   __syncthreads();
-  const int half = warp / FAST_NCONS_HALF, hw = warp % FAST_NCONS_HALF;
+  const int half = HV == 3 ? 0 : warp / FAST_NCONS_HALF, hw = HV == 3 ? warp : warp % FAST_NCONS_HALF;
   if (hw >= NACTH) return;  // idle warps (d = 1)
   // nrhs <= 16 (HV = 1): the second column half of the (only) tile is padding -- its warps skip
-  // the work, and every release count waits for the first half's warps only
-  constexpr int HVN = HV == 0 ? 1 : HV;  // halves with work
+  // the work, and every release count waits for the first half's warps only; HV = 3: all 16 warps
+  // work on that half, a warp per (slot, 8-column tile)
+  constexpr int HVN = HV == 0 || HV == 3 ? 1 : HV;  // halves with work
   if (half >= HVN) return;
   constexpr int nact = HVN * NACTH;
 
@@ -479,6 +483,13 @@ static void launch_one(const FastArgs& a, unsigned grid, cudaStream_t st) {
   else launch_hv<Pol, D, 2>(a, grid, st);
 }
 
+// nrhs 9-16 (one column half): all 16 warps on it (HV = 3) instead of 8 (HV = 1, the other 8 idle);
+// env BF_NO_HV3 keeps HV = 1 (A/B)
+static bool use_hv3(const FastArgs& a) {
+  static const bool off = getenv("BF_NO_HV3") != nullptr;
+  return a.halves == 1 && !off;
+}
+
 void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
   const int nsm = device_sm_count();
   const int64_t items = a.p.nwin * ((a.nrhs + FAST_NB - 1) / FAST_NB);  // (window, rhs tile)
@@ -498,10 +509,23 @@ void launch_fast_pass(int dtype, const FastArgs& a, cudaStream_t st) {
       launch_hv<PolC128<2>, 3, 2, 16384>(a, grid, st);
       return;
     }
+    if (use_hv3(a)) {
+      if (d == 3) launch_hv<PolC128<1>, 3, 3>(a, grid, st);
+      else if (d == 2) launch_hv<PolC128<1>, 2, 3>(a, grid, st);
+      else launch_hv<PolC128<1>, 1, 3>(a, grid, st);
+      return;
+    }
     if (d == 3) launch_one<PolC128<2>, 3>(a, grid, st);
     else if (d == 2) launch_one<PolC128<2>, 2>(a, grid, st);  // 8 warps x 16 columns: 3 % faster than 16 x 8
     else launch_one<PolC128<1>, 1>(a, grid, st);
   } else {
+    if (use_hv3(a)) {
+      if (d == 4) launch_hv<PolC64T<2>, 4, 3>(a, grid, st);
+      else if (d == 3) launch_hv<PolC64T<2>, 3, 3>(a, grid, st);
+      else if (d == 2) launch_hv<PolC64T<1>, 2, 3>(a, grid, st);
+      else launch_hv<PolC64T<1>, 1, 3>(a, grid, st);
+      return;
+    }
     if (d == 4) launch_one<PolC64T<2>, 4>(a, grid, st);
     else if (d == 3) launch_one<PolC64T<2>, 3>(a, grid, st);
     else if (d == 2) launch_one<PolC64T<1>, 2>(a, grid, st);
