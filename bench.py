@@ -341,7 +341,10 @@ def main():
     ab = alg_bytes(bf, args.nrhs, cs)
     nrhs = args.nrhs
     stream = torch.cuda.current_stream()
-    if world == 1:
+    # BF_BENCH_SPLIT1=1: one GPU through the multi-GPU code path (DistBFHandle over a world of 1,
+    # the exchange a local copy) -- a smoke of the N > 1 branch on a single device, not a bench line
+    split = world > 1 or os.environ.get("BF_BENCH_SPLIT1") == "1"
+    if not split:
         h = pkg.BFHandle(bf, local)
         rin, rout = (bf.n, bf.m) if args.op == "N" else (bf.m, bf.n)
         assert bf.m == bf.n, "config 5 is square: the same X block serves op N and op C"
@@ -431,7 +434,7 @@ def main():
         roofline = dominant_roofline(args.dtype, name, rounds, mean, nrhs, cs, peaks)
         roofline["kernels"] = {k: {"ms_per_step": v[0], "launches_per_step": v[2], "alg_bytes_per_step": v[1]}
                                for k, v in by_kernel.items()}
-    elif world > 1:
+    elif split:
         # N > 1: per rank, the whole split apply (its leaf / pass launches and the exchange) against
         # the HBM roofline of one GPU -- each rank streams 1/N of the factors and its subtrees' rows
         # (per-launch events are not exposed by the split's pre / post calls, so this is step-level)
@@ -443,7 +446,7 @@ def main():
                     "note": "max over ranks of the step time; algorithmic bytes / N per rank"}
 
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not split:
         Xp = Xh.pin_memory()
         Yp = torch.empty((nrhs, Yd.shape[1]), dtype=Xd.dtype).pin_memory()
         wh = torch.empty(max(h.workspace_size_host(nrhs, args.op), 1), dtype=torch.uint8, device="cuda")
@@ -462,7 +465,7 @@ def main():
                "h2d_bytes_per_step": int(Xp.numel() * cs), "d2h_bytes_per_step": int(Yp.numel() * cs),
                "api": "bf_apply_host (pinned host X/Y; every step's H2D and D2H inside the timed region, "
                       "consecutive calls overlap one's D2H with the next one's H2D on the handle's copy streams)"}
-    elif not args.no_e2e and world > 1:
+    elif not args.no_e2e and split:
         e2e = h.time_e2e(X_loc_host=Xd.cpu(), op=args.op, steps=max(3, min(args.steps, 10)), alg_bytes=ab)
 
     cpu = cpu_m = None

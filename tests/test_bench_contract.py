@@ -61,3 +61,18 @@ def test_gpu_arm_line(dtype, nrhs):
     assert e["unit"] == "GB/s" and 0 < e["value"] < 1.1 * d["value"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 3 * len(d["per_round"]) > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exchange", ["nccl", "nccl-lib"])
+def test_gpu_split_code_path_world1(exchange, monkeypatch):
+    """The N > 1 branch of bench.py (DistBFHandle, step-level roofline, DistBFHandle.time_e2e, the
+    library-owned NCCL communicator for --exchange nccl-lib) run end to end on one device with a
+    world of 1 (BF_BENCH_SPLIT1): the line parses, its value is consistent, e2e carries copies."""
+    monkeypatch.setenv("BF_BENCH_SPLIT1", "1")
+    d = run_bench("--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--exchange", exchange)
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and 0 < r["frac"] <= 1.0 and "step-level" in r["kernel"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
