@@ -265,28 +265,50 @@ class DistBFHandle:
 
     def time_e2e(self, X_loc_host: torch.Tensor, op: str, steps: int, alg_bytes: int):
         """End-to-end timing through the public API: pinned host X_loc -> device, apply,
-        device -> pinned host Y_loc, every step; max over ranks of the CUDA-event time."""
-        Xp = X_loc_host.contiguous().pin_memory()
-        nrhs = Xp.shape[0]
+        device -> pinned host Y_loc, every step; max over ranks of the CUDA-event time.  The copies
+        are pipelined like bf_apply_host: two device / host buffer sets, H2D and D2H on their own
+        streams, so step k+1's H2D and apply overlap step k's D2H (the apply and its collective stay
+        on the current stream, in the same order on every rank)."""
+        Xp = [X_loc_host.contiguous().pin_memory() for _ in range(2)]
+        nrhs = Xp[0].shape[0]
         _, ro, _, _ = self._rows[op]
-        Yp = torch.empty((nrhs, ro), dtype=Xp.dtype).pin_memory()
-        Xd = torch.empty_like(Xp, device=torch.device("cuda", self.device))
-        Yd = self.empty_output(nrhs, op)
-        for _ in range(2):
-            Xd.copy_(Xp, non_blocking=True)
-            self.apply(Xd, op, out=Yd)
-            Yp.copy_(Yd, non_blocking=True)
+        Yp = [torch.empty((nrhs, ro), dtype=Xp[0].dtype).pin_memory() for _ in range(2)]
+        Xd = [torch.empty_like(Xp[0], device=torch.device("cuda", self.device)) for _ in range(2)]
+        Yd = [self.empty_output(nrhs, op) for _ in range(2)]
+        cur = torch.cuda.current_stream(self.device)
+        s_in, s_out = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_cmp = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+
+        def run(n):
+            s_in.wait_stream(cur)
+            for k in range(n):
+                b = k & 1
+                if k >= 2:
+                    s_in.wait_event(ev_out[b])  # step k - 2's D2H (after its apply) freed set b
+                with torch.cuda.stream(s_in):
+                    Xd[b].copy_(Xp[b], non_blocking=True)
+                    ev_in[b].record(s_in)
+                cur.wait_event(ev_in[b])
+                self.apply(Xd[b], op, out=Yd[b])
+                ev_cmp[b].record(cur)
+                s_out.wait_event(ev_cmp[b])
+                with torch.cuda.stream(s_out):
+                    Yp[b].copy_(Yd[b], non_blocking=True)
+                    ev_out[b].record(s_out)
+            cur.wait_stream(s_out)
+
+        run(2)
         torch.cuda.synchronize()
         if self.world > 1:
             dist.barrier(group=self.group)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            Xd.copy_(Xp, non_blocking=True)
-            self.apply(Xd, op, out=Yd)
-            Yp.copy_(Yd, non_blocking=True)
-        e1.record()
+        e0.record(cur)
+        run(steps)
+        e1.record(cur)
         torch.cuda.synchronize()
+        Xp, Yp = Xp[0], Yp[0]
         ms = e0.elapsed_time(e1) / steps
         if self.world > 1:
             t = torch.tensor([ms], dtype=torch.float64, device=torch.device("cuda", self.device))
@@ -300,7 +322,7 @@ class DistBFHandle:
             h2d, d2h = Xp.numel() * self.cs, Yp.numel() * self.cs
         return {"value": alg_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "DistBFHandle.apply (pinned host X_loc/Y_loc per rank, copies inside the timed region)"}
+                "api": "DistBFHandle.apply (pinned host X_loc/Y_loc per rank, copies inside the timed region, H2D / D2H pipelined with the applies on two copy streams)"}
 
 
 def rhs_shard(nrhs: int, rank: int, world: int):
