@@ -468,7 +468,10 @@ int hodbf_inv_info(hodbf_inv_handle h, int64_t* factor_entries, int32_t* nbutter
  *   forward (children first): z_s = F11^{-1} y_s; y_u -= F21 z_s   (y starts as B)
  *   backward (root first):    x_s = z_s - F11^{-1} F12 x_u
  * bf_mf_solve writes X = M^{-1} B (N x nrhs, column-major DEVICE blocks, non-overlapping) with a
- * workspace of bf_mf_workspace_size bytes; asynchronous on `stream`, no allocation. */
+ * workspace of bf_mf_workspace_size bytes; asynchronous on `stream`, no allocation.  The fronts of
+ * one height (forward) / depth (backward) run concurrently on streams owned by the handle, forked
+ * from and joined back into `stream` (so the call is stream-ordered and graph-capturable);
+ * concurrent solves on one handle are serialised (internal lock).  Results are deterministic. */
 typedef struct bf_mf_s* bf_mf_handle;
 typedef struct {
   int32_t parent, reserved;      /* parent front (-1: a root)                                      */

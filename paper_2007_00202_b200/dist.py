@@ -83,9 +83,15 @@ class NcclComm:
         self.ptr, self.rank, self.world, self.device = c, rank, world, device
 
     def close(self):
+        """Destroy the communicator (after every DistBFHandle using it: each holds a reference)."""
         if getattr(self, "ptr", None) is not None and self.ptr.value:
-            _lib().bf_nccl_comm_destroy(self.ptr)
+            try:
+                _lib().bf_nccl_comm_destroy(self.ptr)
+            except Exception:  # interpreter shutdown: the library may already be gone
+                pass
         self.ptr = None
+
+    __del__ = close
 
 
 class DistBFHandle:
