@@ -419,7 +419,10 @@ def _rounds(fn_count, fn_info, h, op):
     return out
 
 
-def make_hodbf_desc(H, keep: _Keep) -> hodbf_desc:
+def make_hodbf_desc(H, keep: _Keep, level_maps=None) -> hodbf_desc:
+    """hodbf_desc of a bfinputs.HODBF.  ``level_maps``: optional {(l, tau): maps} for off-diagonal
+    butterflies given in slot order (bf_desc.level_maps; H.offdiag[l-1][tau] then holds the
+    slot-ordered butterfly)."""
     code = _np_dtype_code(H.dtype)
     cdt = np.complex128 if code == BF_C128 else np.complex64
     d = hodbf_desc()
@@ -431,9 +434,10 @@ def make_hodbf_desc(H, keep: _Keep) -> hodbf_desc:
     nbf = sum(len(lev) for lev in H.offdiag)
     arr = (bf_desc * max(nbf, 1))()
     k = 0
-    for lev in H.offdiag:
-        for b in lev:
-            arr[k] = make_desc(b, keep, tree_local=True)
+    for l, lev in enumerate(H.offdiag, start=1):
+        for tau, b in enumerate(lev):
+            maps = (level_maps or {}).get((l, tau))
+            arr[k] = make_desc(b, keep, tree_local=True, level_maps=maps)
             k += 1
     keep.arrs.append(arr)
     d.offdiag = C.cast(arr, C.POINTER(bf_desc))
@@ -467,9 +471,9 @@ class ApplyGraph:
 class HODBFHandle:
     """An HOD-BF matrix uploaded to one device (hodbf_create)."""
 
-    def __init__(self, H, device: int = 0):
+    def __init__(self, H, device: int = 0, level_maps=None):
         keep = _Keep()
-        d = make_hodbf_desc(H, keep)
+        d = make_hodbf_desc(H, keep, level_maps)
         h = C.c_void_p()
         _check("hodbf_create", lib().hodbf_create(C.byref(d), device, C.byref(h)))
         self.h, self.device, self.code, self.n = h, device, d.dtype, H.n

@@ -479,3 +479,26 @@ def test_hodbf_host_apply_pipelined():
     torch.cuda.synchronize()
     for X, y, (op, _) in zip(Xs, Yh, plan):
         assert oracle.rel_err(y.numpy().T, oracle.apply_op(K, X, op)) <= 1e-12, op
+
+
+def test_hodbf_level_maps_same_result():
+    """hodbf_create re-packs off-diagonal butterflies given with level_maps: the HOD-BF applies bit
+    for bit like the canonical one."""
+    from bfinputs import HODBF, random_level_maps, slot_ordered
+    H = helmholtz_plane_hodbf(16, 16, 10.0, 1e-4)
+    maps, off = {}, []
+    for l, lev in enumerate(H.offdiag, start=1):
+        row = []
+        for tau, b in enumerate(lev):
+            if b.L >= 1 and (l + tau) % 2 == 0:
+                maps[(l, tau)] = random_level_maps(b.L, seed=100 * l + tau)
+                row.append(slot_ordered(b, maps[(l, tau)]))
+            else:
+                row.append(b)
+        off.append(row)
+    assert maps
+    H2 = HODBF(H.n, H.LH, H.leaf_ptr, H.perm, H.D, off, H.dtype, dict(H.meta))
+    h0, h1 = pkg.HODBFHandle(H), pkg.HODBFHandle(H2, level_maps=maps)
+    for op, nr in (("N", 9), ("C", 4)):
+        X = random_rhs(H.n, nr, seed=31)
+        np.testing.assert_array_equal(run(h1, X, op), run(h0, X, op))
