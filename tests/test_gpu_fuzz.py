@@ -86,3 +86,52 @@ def test_fuzz_hodbf(seed):
         torch.cuda.synchronize()
         err = oracle.rel_err(Y.cpu().numpy().T, oracle.apply_op(A, X, op))
         assert err <= TOL[dtype], (seed, nx, ny, tol, op, nr, err)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_extract(seed):
+    """bf_extract / bf_extract_list (Alg. 3) on random butterflies: random lists of scattered
+    (rows, cols) requests (duplicates and empty requests included) against the dense gather."""
+    bf, maps, dtype, kind, rng = _case(10_000 + seed)
+    h = pkg.BFHandle(bf)
+    K = oracle.bf_dense(bf)
+    pairs = []
+    for _ in range(int(rng.integers(1, 5))):
+        nI, nJ = int(rng.integers(0, min(bf.m, 70) + 1)), int(rng.integers(0, min(bf.n, 70) + 1))
+        pairs.append((rng.integers(0, max(bf.m, 1), nI), rng.integers(0, max(bf.n, 1), nJ)))
+    outs = h.extract_list(pairs)
+    torch.cuda.synchronize()
+    for (I, J), E in zip(pairs, outs):
+        ref = K[np.ix_(I, J)]
+        if ref.size:
+            assert oracle.rel_err(E.cpu().numpy(), ref) <= TOL[dtype], (seed, kind, len(I), len(J))
+    I, J = pairs[0]
+    if len(I) and len(J):
+        assert oracle.rel_err(h.extract(I, J).cpu().numpy(), K[np.ix_(I, J)]) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_fuzz_split_emulated(seed):
+    """The multi-GPU split (bf_dist_*) on random shapes and rank counts, the P rank-local plans run
+    in turn on one device with the exchange replayed as copies (tests/test_gpu_dist.emulate)."""
+    from test_gpu_dist import _subtree_perm, emulate
+    rng = np.random.default_rng(20_000 + seed)
+    dtype = np.complex128 if seed % 4 else np.complex64
+    P = int(rng.choice([2, 4, 8]))
+    p = P.bit_length() - 1
+    L = int(rng.integers(2 * p, 9))
+    lc = int(rng.integers(p, L - p + 1))
+    if seed % 2:
+        bf = random_butterfly(L=L, leaf=16, r=16, seed=seed, dtype=dtype, lc=lc)
+    else:
+        nb = 1 << L
+        bf = random_ranks_butterfly(L, rng.integers(0, 9, nb), rng.integers(1, 9, nb), seed=seed, rmin=1,
+                                    rmax=int(rng.integers(2, 12)), lc=lc, dtype=dtype)
+    bf.row_perm = _subtree_perm(bf.m, bf.row_leaf_ptr, bf.L, p, seed)
+    bf.col_perm = _subtree_perm(bf.n, bf.col_leaf_ptr, bf.L, p, seed + 1)
+    K = oracle.bf_dense(bf)
+    for op in ("N", "C", "T"):
+        nr = int(rng.choice(NRHS))
+        X = random_rhs(bf.n if op == "N" else bf.m, nr, seed=seed + 5, dtype=dtype)
+        err = oracle.rel_err(emulate(bf, X, op, P), oracle.apply_op(K, X, op))
+        assert err <= TOL[dtype], (seed, P, L, lc, op, nr, err)
