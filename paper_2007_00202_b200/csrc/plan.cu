@@ -784,6 +784,7 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   // window levels per pass: 3 (complex128), 4 (complex64; env BF_C64_DMAX = 3 for A/B)
   int dmax = sizeof(CT) == 16 ? FAST_DMAX : FAST_DMAX_C64;
   if (sizeof(CT) == 8 && getenv("BF_C64_DMAX")) dmax = std::max(1, std::min(FAST_DMAX_C64, atoi(getenv("BF_C64_DMAX"))));
+  if (sizeof(CT) == 16 && getenv("BF_C128_DMAX")) dmax = std::max(1, std::min(FAST_DMAX, atoi(getenv("BF_C128_DMAX"))));
   auto chunk = [&](int lo, int hi) {  // split [lo, hi] into near-equal passes of <= dmax levels
     const int n = hi - lo, k = (n + dmax - 1) / dmax;
     for (int p = 0, at = lo; p < k; ++p) {
