@@ -86,6 +86,13 @@ __device__ __forceinline__ void tile_frags(PolC64<NT>, typename PolC64<NT>::Frag
   }
 }
 
+// A/B knob (build with -DBF_TILE_KSKIP=0): run every k-step of a K chunk, including the zero-filled
+// rows past a term's K
+#ifndef BF_TILE_KSKIP
+#define BF_TILE_KSKIP 1
+#endif
+__device__ __forceinline__ constexpr bool tile_kskip() { return BF_TILE_KSKIP != 0; }
+
 template <class Pol, bool M3, int MINB = 2>
 __global__ void __launch_bounds__(256, MINB) k_stage_tile(StageArgs a) {
   using E = typename Pol::E;
@@ -177,8 +184,10 @@ __global__ void __launch_bounds__(256, MINB) k_stage_tile(StageArgs a) {
       __syncthreads();
       const E* sA = sm + (c % C::NST) * C::STAGE;
       const E* sB = sA + KC * SA;
+      const int kvalid = tile_kskip() ? tm.k - kc : KC;  // k-steps past the term's K only add zeros
 #pragma unroll
       for (int k0 = 0; k0 < KC; k0 += KS) {
+        if (k0 >= kvalid) break;
         typename Pol::Frags f;
         tile_frags<M3>(Pol{}, f, sA, sB, wr, wc, k0, g, t, cj);
         acc.mac(f);
@@ -352,10 +361,14 @@ __global__ void __launch_bounds__(256, MINB) k_stage_tileT(StageArgs a) {
         // is loaded (and its 3M sum formed) before its DMMAs issue, with no per-n-tile branch
         // between them (the branchy form left the DMMAs waiting on each load / DADD in turn --
         // ncu: "wait" and short-scoreboard stalls led, DMMA 45 % active)
+        // k-steps holding term rows: the chunk's tail beyond tm.k is zero-filled shared memory, whose
+        // DMMAs would only add zeros (ragged K = r1 + r2 pads up to 15 rows per term otherwise)
+        const int kvalid = tile_kskip() ? tm.k - kc : KC;
         auto chunk = [&](auto ntc) {
           constexpr int NTL = decltype(ntc)::value;
 #pragma unroll
           for (int k0 = 0; k0 < KC; k0 += 4) {
+            if (k0 >= kvalid) break;
             const E x = sB[(k0 + t) * SB + cw + g];  // In^T fragment
             E f[NTL];
             double fs[NTL];
