@@ -16,7 +16,8 @@
 //     op's reads of other slots.  The last op writes the output slabs straight to HBM; when
 //     every warp has reached it, the other buffer takes the next window.
 //   * complex64 windows may span 4 levels (16 slots per half): each warp then runs every op for
-//     two slots, one after the other.
+//     two slots -- the two outputs of one input pair, in one k-loop, so that the 3xTF32 split of
+//     each slab fragment is computed once for both (PAIRW; the slot pair changes with the op).
 #include <cstdio>
 
 #include "mma.cuh"
@@ -186,6 +187,9 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
   // slots per warp: 2 for 4-level windows (16 slots, 8 warps per half), else 1
   constexpr int SPW = S * CT > NCH ? S * CT / NCH : 1;
   static_assert(SPW == 1 || CT == 1, "several slots per warp need whole-slot warps");
+  // two slots per warp (complex64 4-level windows): the warp's slots of a pair op are the two
+  // outputs of one input pair, sharing the slab fragments' 3xTF32 split (Pol::PAIR_SHARE)
+  constexpr bool PAIRW = Pol::PAIR_SHARE && SPW == 2;
   constexpr int NACTH = S * CT / SPW;                // active warps per half
   constexpr int NACT = (HV == 3 ? 1 : 2) * NACTH;    // active warps
   constexpr int SPP = St::SPP;                       // k-steps per page
@@ -274,6 +278,111 @@ __global__ void __launch_bounds__(FAST_THREADS, 1) k_bf_pass(const __grid_consta
         if (atom_add_acqrel(wcnt, 1) == (int)(i + 1) * nact - 1) str.issue_window(i + 1, rd ^ 1);
       }
       const E* win = winbuf + rd * WIN + half * Cfg::WINH;
+      if constexpr (PAIRW) {
+        if (!A.no_pairw && (op.kind == FK_PAIR_DOWN || op.kind == FK_PAIR_UP)) {
+          // the warp's two slots are the outputs that read the same input pair (they differ in
+          // bit pb: the top bit of the T_O index for a W stage, bit 0 for an R stage), so one k-loop
+          // splits each slab fragment once for both of them
+          const int ds = P.d - op.s;
+          const int pb = op.kind == FK_PAIR_DOWN ? ds - 1 : 0;
+          const int oA = ((hw >> pb) << (pb + 1)) | (hw & ((1 << pb) - 1)), oB = oA | (1 << pb);
+          const E* sp0;
+          if (op.kind == FK_PAIR_DOWN) {
+            const int tp = oA >> (ds - 1), up = oA & ((1 << (ds - 1)) - 1);
+            sp0 = win + (((tp >> 1) << ds) + 2 * up) * FAST_HSLAB;
+          } else {
+            const int tt = oA >> ds, u = oA & ((1 << ds) - 1);
+            sp0 = win + (((2 * tt) << (ds - 1)) + (u >> 1)) * FAST_HSLAB;
+          }
+          const E* sp1 = op.kind == FK_PAIR_DOWN ? sp0 + FAST_HSLAB
+                                                 : win + (((2 * (oA >> ds) + 1) << (ds - 1)) + ((oA & ((1 << ds) - 1)) >> 1)) * FAST_HSLAB;
+          typename Pol::FAcc accA, accB;
+          accA.zero();
+          accB.zero();
+          constexpr int NSTEP = 2 * FAST_RANK / Pol::KS;
+          constexpr int SPO = SPP < NSTEP ? SPP : NSTEP;
+          static_assert(NSTEP % SPO == 0, "pages must split ops evenly");
+          auto bsrc = [&](int k) { return (k < KPS ? sp0 : sp1) + (k & (KPS - 1)) * Pol::KS * FAST_HC; };
+          if (!(diag & 1)) mbar_wait(&full[slot], ph, 4);
+          const int roffA = oA * FAST_FRAG + Pol::rec_off(c0w), droff = (oB - oA) * FAST_FRAG;
+          const unsigned char* pgn = ring + (size_t)slot * Cfg::PG + roffA;
+          int nslot = slot;
+          uint32_t nph = ph;
+          typename Pol::FFrags f[2];
+          float4 fb[2][NT];
+          Pol::load_fa(f[0], pgn, lane);
+          Pol::load_fa2(fb[0], pgn + droff, lane);
+          Pol::load_b(f[0], bsrc(0), bo);
+#pragma unroll
+          for (int k = 0; k < NSTEP; ++k) {
+            if (k + 1 < NSTEP) {
+              const int k1 = k + 1;
+              if (k1 % SPO == 0) {
+                if (++nslot == NP) {
+                  nslot = 0;
+                  nph ^= 1;
+                }
+                if (!(diag & 1)) mbar_wait(&full[nslot], nph, 4);
+                pgn = ring + (size_t)nslot * Cfg::PG + roffA;
+              }
+              Pol::load_fa(f[k1 & 1], pgn + (k1 % SPO) * S * FAST_FRAG, lane);
+              Pol::load_fa2(fb[k1 & 1], pgn + (k1 % SPO) * S * FAST_FRAG + droff, lane);
+              Pol::load_b(f[k1 & 1], bsrc(k1), bo);
+            }
+            {
+              typename Pol::ASplit sa;
+              Pol::split_a(f[k & 1], sa);
+              accA.mac_split(sa, f[k & 1].f);
+              accB.mac_split(sa, fb[k & 1]);
+            }
+            if ((k + 1) % SPO == 0) {
+              __syncwarp();
+              if (lane == 0 && !(diag & 1)) {
+                if (atom_add_release_page(&pcnt[slot], 1) == (rnd + 1) * nact - 1) str.issue_page(j + NP);
+              }
+              ++j;
+              if (++slot == NP) {
+                slot = 0;
+                ph ^= 1;
+                ++rnd;
+              }
+            }
+          }
+          if (last) {
+            if (!(diag & 2)) {
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int o = v ? oB : oA;
+                E* dst;
+                if (P.xout && A.p2p) {
+                  int peer = 0;
+                  const int64_t off =
+                      pass_slab_off(P, P.xout, jt, half, A.nlev, A.ntiles, a, b, P.out_s, o, A.myrank, &peer);
+                  dst = static_cast<E*>(A.peer[peer]) + off;
+                } else {
+                  dst = Sout + pass_slab_off(P, P.xout, jt, half, A.nlev, A.ntiles, a, b, P.out_s, o);
+                }
+                Pol::store_slab(v ? accB : accA, dst, c0w, g, t, lane);
+              }
+            }
+            cur = rd ^ 1;
+          } else {
+            if (!(diag & 4)) {
+              if (q == 0) named_sync(hbar, NACTH * 32);
+              E* dst = winbuf + (rd ^ 1) * WIN + half * Cfg::WINH;
+              Pol::store_slab(accA, dst + oA * FAST_HSLAB, c0w, g, t, lane);
+              Pol::store_slab(accB, dst + oB * FAST_HSLAB, c0w, g, t, lane);
+              named_sync(hbar, NACTH * 32);
+            } else {
+              E* dst = winbuf + (rd ^ 1) * WIN + half * Cfg::WINH;
+              Pol::store_slab(accA, dst + oA * FAST_HSLAB, c0w, g, t, lane);
+              Pol::store_slab(accB, dst + oB * FAST_HSLAB, c0w, g, t, lane);
+            }
+            rd ^= 1;
+          }
+          continue;
+        }
+      }
 #pragma unroll
       for (int sl = 0; sl < SPW; ++sl) {
       const int o = o0 + sl * (S / SPW);  // slot

@@ -91,6 +91,7 @@ struct FastArgs {
   int32_t p2p;   // xout pass: write each slab straight into its receiver's recv region
   int32_t myrank;
   void* peer[FAST_MAXPEER];  // p2p: every rank's recv-region base (peer memory over NVLink)
+  int32_t no_pairw;  // 4-level complex64 passes: one slot per k-loop (env BF_NO_PAIRW, A/B of PAIRW)
   int32_t diag;  // profiling only (env BF_FAST_DIAG, results are garbage): bit 0 = no operand
                  // streaming (compute only), bit 1 = output slabs not written to HBM, bit 2 = no
                  // intermediate epilogue / barriers, bit 3 (with 2) = epilogue stores, no barriers

@@ -151,6 +151,7 @@ struct PolC128 {
     double bs[NT];
   };
   static constexpr bool LEAF_OPS = true;  // the pass kernel may run the fused leaf ops
+  static constexpr bool PAIR_SHARE = false;  // see PolC64T
   // lane-constant element offset of B row t, n-tile ni (k0 = 0) inside a half slab
   __device__ static __forceinline__ int boff(int t, int g, int c0w, int ni) {
     return t * FAST_HC + ((c0w + 8 * ni + g) ^ swz(t));
@@ -500,6 +501,9 @@ struct PolC64T {
   static constexpr int KS = 8;
   static constexpr int NT = NT_;  // 8-row n-tiles per warp (NT = 1: the warp's c0w / 8 selects which)
   static constexpr bool LEAF_OPS = false;
+  // a warp may run the two output slots that share an input pair in one k-loop, splitting the
+  // slab fragment (A role) once for both (fast.cu, 4-level windows)
+  static constexpr bool PAIR_SHARE = true;
   __device__ static __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) { PolC64<1>::split(x, hi, lo); }
   __device__ static __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
     PolC64<1>::mma(c, a, b);
@@ -523,6 +527,25 @@ struct PolC64T {
     f.sr = p[bo[0]];
     f.si = p[32 + bo[0]];
   }
+  // the 3xTF32 split of a slab fragment (A role): (re, im, re + im) x (hi, lo)
+  struct ASplit {
+    uint32_t h[3][4], l[3][4];
+  };
+  __device__ static __forceinline__ void split_a(const Frags& f, ASplit& s) {
+    const float re[4] = {f.sr.x, f.sr.y, f.sr.z, f.sr.w}, im[4] = {f.si.x, f.si.y, f.si.z, f.si.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      split(re[e], s.h[0][e], s.l[0][e]);
+      split(im[e], s.h[1][e], s.l[1][e]);
+      split(re[e] + im[e], s.h[2][e], s.l[2][e]);
+    }
+  }
+  // the factor fragments of a second output slot (pair-shared ops, fast.cu PAIRW)
+  __device__ static __forceinline__ void load_fa2(float4 (&g)[NT], const unsigned char* rec, int lane) {
+    const float4* p = reinterpret_cast<const float4*>(rec);
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) g[ni] = p[ni * 32 + lane];
+  }
   struct Acc {
     float p[3][NT][4];
     __device__ __forceinline__ void zero() {
@@ -533,19 +556,12 @@ struct PolC64T {
 #pragma unroll
           for (int e = 0; e < 4; ++e) p[q][ni][e] = 0.f;
     }
-    __device__ __forceinline__ void mac(const Frags& f) {
-      uint32_t ah[3][4], al[3][4];
-      const float re[4] = {f.sr.x, f.sr.y, f.sr.z, f.sr.w}, im[4] = {f.si.x, f.si.y, f.si.z, f.si.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        split(re[e], ah[0][e], al[0][e]);
-        split(im[e], ah[1][e], al[1][e]);
-        split(re[e] + im[e], ah[2][e], al[2][e]);
-      }
+    // one k-step on an already split slab fragment with the factor fragments fb
+    __device__ __forceinline__ void mac_split(const ASplit& s, const float4 (&fb)[NT]) {
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) {
         uint32_t bh[3][2], bl[3][2];
-        const float br[2] = {f.f[ni].x, f.f[ni].y}, bi[2] = {f.f[ni].z, f.f[ni].w};
+        const float br[2] = {fb[ni].x, fb[ni].y}, bi[2] = {fb[ni].z, fb[ni].w};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           split(br[e], bh[0][e], bl[0][e]);
@@ -554,11 +570,16 @@ struct PolC64T {
         }
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          mma(p[q][ni], ah[q], bl[q]);
-          mma(p[q][ni], al[q], bh[q]);
-          mma(p[q][ni], ah[q], bh[q]);
+          mma(p[q][ni], s.h[q], bl[q]);
+          mma(p[q][ni], s.l[q], bh[q]);
+          mma(p[q][ni], s.h[q], bh[q]);
         }
       }
+    }
+    __device__ __forceinline__ void mac(const Frags& f) {
+      ASplit s;
+      split_a(f, s);
+      mac_split(s, f.f);
     }
     // every output element: fn(row of the warp's n-tiles, column in the half, value)
     template <typename Fn>

@@ -1656,6 +1656,7 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
   char* recvb = sendb + xb;
   const bool fwd = k == 0;
   const int diag = getenv("BF_FAST_DIAG") ? atoi(getenv("BF_FAST_DIAG")) : 0;
+  const int32_t no_pairw = getenv("BF_NO_PAIRW") ? 1 : 0;
   const int32_t ntiles = (int32_t)((nrhs + FAST_NB - 1) / FAST_NB);
   for (int i = lo; i < hi; ++i) {
     const FastPass& P = FP.passes[i];
@@ -1687,6 +1688,7 @@ static void run_fast(bf_handle h, int k, int op, int64_t nrhs, const void* X, in
       FastArgs a{};
       a.p = P;
       a.diag = diag;
+      a.no_pairw = no_pairw;
       a.skew = getenv("BF_FAST_SKEW") ? atoi(getenv("BF_FAST_SKEW")) : 0;
       // column halves with work: 2; 1 when nrhs <= 16; 0 (narrow, 8 columns) when nrhs <= 8
       a.halves = getenv("BF_NO_HALF_SKIP") ? 2 : nrhs <= 8 && !getenv("BF_NO_NARROW") ? 0 : nrhs <= FAST_HC ? 1 : 2;

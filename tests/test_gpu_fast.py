@@ -285,3 +285,30 @@ def test_fused_only_releases_the_pool(dtype):
     X = random_rhs(bfr.n, 3, seed=2, dtype=dtype)
     assert oracle.rel_err(host(hr.apply(dev(X))), oracle.bf_apply(bfr, X)) <= TOL[dtype]
     assert hr.extract(np.arange(2), np.arange(3)).shape == (2, 3)
+
+
+@pytest.mark.parametrize("L,leaf,lc", [(8, 16, None), (9, 16, 3), (8, 32, 6), (6, 16, 2)])
+@pytest.mark.parametrize("nrhs", [5, 16, 40])
+def test_c64_pair_shared_split(monkeypatch, L, leaf, lc, nrhs):
+    """complex64 4-level windows: a warp runs the two outputs of one input pair in one k-loop
+    (PAIRW, fast.cu), splitting each slab fragment once.  Same MMAs in the same order per
+    accumulator as one slot per k-loop (BF_NO_PAIRW), so the results are bit-identical; both
+    agree with the oracle (ops N / C / T)."""
+    dtype = np.complex64
+    bf = random_butterfly(L=L, leaf=leaf, r=16, seed=11 + L, dtype=dtype, lc=lc)
+    Xh = random_rhs(bf.n, nrhs, seed=5, dtype=dtype)
+    Xc = random_rhs(bf.m, nrhs, seed=6, dtype=dtype)
+    h = pkg.BFHandle(bf)
+    K = oracle.bf_dense(bf)
+    outs = {}
+    for v in (0, 1):
+        if v:
+            monkeypatch.setenv("BF_NO_PAIRW", "1")
+        outs[v] = (host(h.apply(dev(Xh), "N")), host(h.apply(dev(Xc), "C")), host(h.apply(dev(Xc), "T")))
+    monkeypatch.delenv("BF_NO_PAIRW", raising=False)
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    Y, Yc, Yt = outs[0]
+    assert oracle.rel_err(Y, oracle.apply_op(K, Xh, "N")) <= TOL[dtype]
+    assert oracle.rel_err(Yc, oracle.apply_op(K, Xc, "C")) <= TOL[dtype]
+    assert oracle.rel_err(Yt, oracle.apply_op(K, Xc, "T")) <= TOL[dtype]
