@@ -785,8 +785,17 @@ static void build_fast(FastPlan& FP, const Geom& G, const HostFactors<CT>& H, in
   int dmax = sizeof(CT) == 16 ? FAST_DMAX : FAST_DMAX_C64;
   if (sizeof(CT) == 8 && getenv("BF_C64_DMAX")) dmax = std::max(1, std::min(FAST_DMAX_C64, atoi(getenv("BF_C64_DMAX"))));
   if (sizeof(CT) == 16 && getenv("BF_C128_DMAX")) dmax = std::max(1, std::min(FAST_DMAX, atoi(getenv("BF_C128_DMAX"))));
+  // env BF_PASS_FILL (A/B): 1 = full dmax-level passes with the remainder last, 2 = remainder first
+  const int fill = getenv("BF_PASS_FILL") ? atoi(getenv("BF_PASS_FILL")) : 0;
   auto chunk = [&](int lo, int hi) {  // split [lo, hi] into near-equal passes of <= dmax levels
     const int n = hi - lo, k = (n + dmax - 1) / dmax;
+    if (fill && n % dmax) {
+      int at = lo;
+      if (fill == 2) lv.push_back(at += n % dmax);
+      while (at + dmax <= hi) lv.push_back(at += dmax);
+      if (fill == 1) lv.push_back(hi);
+      return;
+    }
     for (int p = 0, at = lo; p < k; ++p) {
       at += n / k + (p < n % k ? 1 : 0);
       lv.push_back(at);
