@@ -303,6 +303,17 @@ def test_cfg3(dtype):
     assert oracle.rel_err(run(h, X, "N"), oracle.hodbf_apply(H, X, "N")) <= TOL[dtype]
     Z = random_rhs(H.n, 64, seed=31, dtype=dtype)
     assert oracle.rel_err(run(h, Z, "C"), oracle.hodbf_apply(H, Z, "C")) <= TOL[dtype]
+    if dtype is np.complex128:
+        # SURVEY P4 at config 3's full size (16384 unknowns): 96 seeded random rows of the front,
+        # evaluated entry by entry from the Helmholtz kernel (brute force, no compression), times
+        # X, against the oracle's sampled-row apply and the GPU's output rows: both must sit
+        # within the compression tolerance (BJ config 3: rel. tol 1e-4; bound 10 eps as in
+        # tests/test_construction_pins.py)
+        rows = np.sort(np.random.default_rng(5).choice(H.n, 96, replace=False))
+        Arows = H.meta["kernel"](rows, np.arange(H.n))
+        ref = Arows @ X[:, :32]
+        assert oracle.rel_err(oracle.hodbf_rows_apply(H, rows, X[:, :32]), ref) <= 10 * 1e-4
+        assert oracle.rel_err(run(h, X, "N")[rows, :32], ref) <= 10 * 1e-4
 
 
 def test_cfg4():
