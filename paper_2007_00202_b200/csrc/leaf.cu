@@ -22,8 +22,8 @@
 
 namespace bfa {
 
-template <class Pol, int MODE>
-__global__ void __launch_bounds__(LEAF_THREADS, 1) k_leaf(const __grid_constant__ LeafArgs A) {
+template <class Pol, int MODE, int NW = LEAF_NCONS>
+__global__ void __launch_bounds__(NW * 32, 1) k_leaf(const __grid_constant__ LeafArgs A) {
   using E = typename Pol::E;
   constexpr int KS = Pol::KS;
   constexpr int NT = Pol::NT;
@@ -196,7 +196,7 @@ bool fast_make_xmap(int dtype, const void* X, int64_t rows, int64_t nrhs, int64_
 
 constexpr size_t LEAF_SMEM = 227 * 1024;
 
-template <class Pol, int MODE>
+template <class Pol, int MODE, int NW = LEAF_NCONS>
 static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
   const int nsm = device_sm_count();
   using E = typename Pol::E;
@@ -206,7 +206,7 @@ static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
   a.stage_bytes = (int64_t)((a_chunk + b_bytes + 1023) & ~size_t(1023));
   const size_t avail = LEAF_SMEM - 64 * 8;  // barriers
   const size_t stg = (size_t)a.stage_bytes;
-  const int np = LEAF_NCONS;  // item-owning warps
+  const int np = NW;  // item-owning warps
   int dep = (int)(avail / ((size_t)np * stg));
   int maxdep = 4;
   if (const char* e = getenv("BF_LEAF_DEP")) maxdep = atoi(e);  // tuning knob
@@ -216,10 +216,23 @@ static void launch_leaf_t(LeafArgs& a, cudaStream_t st) {
   a.nst = np * dep;
   const size_t smem = (size_t)a.nst * stg + (size_t)a.nst * 8;
   static std::atomic<size_t> attr[BF_MAX_DEVICES];
-  ensure_smem_attr(attr, (const void*)k_leaf<Pol, MODE>, smem);
+  ensure_smem_attr(attr, (const void*)k_leaf<Pol, MODE, NW>, smem);
   const int64_t items = a.nleaf * ((a.nrhs + FAST_NB - 1) / FAST_NB);
   const unsigned grid = (unsigned)(items < nsm ? items : nsm);
-  launch_pdl(k_leaf<Pol, MODE>, grid, LEAF_THREADS, smem, st, a);
+  launch_pdl(k_leaf<Pol, MODE, NW>, grid, NW * 32, smem, st, a);
+}
+
+// full 32-column tiles: item-owning warps per CTA (8 by default; env BF_LEAF_NW_IN / BF_LEAF_NW_OUT
+// = 12 or 16 for the A/B of more warps against the register cap and the stage depth they leave)
+template <class Pol, int MODE>
+static void launch_leaf_nw(LeafArgs& a, cudaStream_t st) {
+  static const int nw = []() {
+    const char* e = getenv(MODE == 0 ? "BF_LEAF_NW_IN" : "BF_LEAF_NW_OUT");
+    return e ? atoi(e) : LEAF_NCONS;
+  }();
+  if (nw == 16) launch_leaf_t<Pol, MODE, 16>(a, st);
+  else if (nw == 12) launch_leaf_t<Pol, MODE, 12>(a, st);
+  else launch_leaf_t<Pol, MODE, LEAF_NCONS>(a, st);
 }
 
 void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
@@ -243,8 +256,8 @@ void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
       if (a.mode == 0) launch_leaf_t<PolC128<2>, 0>(a, st);
       else launch_leaf_t<PolC128<2>, 1>(a, st);
     } else {
-      if (a.mode == 0) launch_leaf_t<PolC128<4>, 0>(a, st);
-      else launch_leaf_t<PolC128<4>, 1>(a, st);
+      if (a.mode == 0) launch_leaf_nw<PolC128<4>, 0>(a, st);
+      else launch_leaf_nw<PolC128<4>, 1>(a, st);
     }
   } else {
     if (eight) {
@@ -254,8 +267,8 @@ void launch_leaf(int dtype, LeafArgs& a, cudaStream_t st) {
       if (a.mode == 0) launch_leaf_t<PolC64<2>, 0>(a, st);
       else launch_leaf_t<PolC64<2>, 1>(a, st);
     } else {
-      if (a.mode == 0) launch_leaf_t<PolC64<4>, 0>(a, st);
-      else launch_leaf_t<PolC64<4>, 1>(a, st);
+      if (a.mode == 0) launch_leaf_nw<PolC64<4>, 0>(a, st);
+      else launch_leaf_nw<PolC64<4>, 1>(a, st);
     }
   }
 }
